@@ -1,0 +1,290 @@
+"""Device-side driver: torch owns device memory and the stream, the C ABI
+(libftkb200.so) does every numeric operation.  No CPU fallback exists; every
+entry point raises when CUDA or the extension is missing.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+_CTX = {}
+_VARIANT = {"auto": N.VARIANT_AUTO, "exact": N.VARIANT_EXACT, "tc": N.VARIANT_TC}
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device visible: the B200 engine has no CPU fallback")
+    return torch
+
+
+def device():
+    t = _torch()
+    return t.device("cuda", t.cuda.current_device())
+
+
+def ctx():
+    t = _torch()
+    dev = t.cuda.current_device()
+    if dev not in _CTX:
+        lib = N.load()
+        c = lib.ftk_ctx_create(dev)
+        if not c:
+            raise N.FTKError("ftk_ctx_create failed: " + lib.ftk_last_error().decode())
+        _CTX[dev] = c
+    return _CTX[dev]
+
+
+def stream():
+    return _torch().cuda.current_stream().cuda_stream
+
+
+def code(dtype):
+    return N.FTK_F32 if np.dtype(dtype) == np.float32 else N.FTK_F64
+
+
+def tdtype(dtype):
+    t = _torch()
+    return t.float32 if np.dtype(dtype) == np.float32 else t.float64
+
+
+def ndtype(tensor_dtype):
+    t = _torch()
+    return np.dtype(np.float32) if tensor_dtype == t.float32 else np.dtype(np.float64)
+
+
+def ptr(t):
+    return None if t is None else (t.data_ptr() or None)
+
+
+def to_dev(a, dtype=None):
+    """numpy / torch (any device) -> contiguous CUDA tensor."""
+    t = _torch()
+    if isinstance(a, t.Tensor):
+        out = a.to(device=device(), dtype=tdtype(dtype) if dtype is not None else a.dtype,
+                   non_blocking=True)
+        return out.contiguous()
+    arr = np.ascontiguousarray(a, dtype=dtype)
+    return t.from_numpy(arr).to(device(), non_blocking=False)
+
+
+def to_host(tensor):
+    return tensor.detach().cpu().numpy()
+
+
+def variant_code(variant):
+    if variant not in _VARIANT:
+        raise ValueError(f"unknown kernel variant {variant!r}")
+    return _VARIANT[variant]
+
+
+# ------------------------------------------------------------- hooks -----
+class DevInjection:
+    """FaultHook.kernel_arrays (8 host arrays) mirrored on the device."""
+
+    def __init__(self, arrs):
+        t = _torch()
+        bi, bj, ei, ej, bit, applied, before, after = arrs
+        n = len(bi)
+        self.n = n
+        self.host = arrs
+        idx = np.stack([np.asarray(v, np.int64) for v in (bi, bj, ei, ej, bit)]) if n else \
+            np.zeros((5, 0), np.int64)
+        self.idx = t.from_numpy(np.ascontiguousarray(idx)).to(device())
+        self.applied = t.zeros(max(n, 1), dtype=t.int64, device=device())
+        self.ba = t.zeros((2, max(n, 1)), dtype=t.float64, device=device())
+        base = self.idx.data_ptr()
+        self.struct = N.Injection(
+            n, *(base + 8 * n * c for c in range(5)), self.applied.data_ptr(),
+            self.ba[0].data_ptr(), self.ba[1].data_ptr())
+
+    def ref(self):
+        import ctypes
+
+        return ctypes.byref(self.struct)
+
+    def finish(self):
+        """Copy applied/before/after back into the hook's host arrays."""
+        if self.n == 0:
+            return
+        applied = to_host(self.applied)[: self.n]
+        ba = to_host(self.ba)[:, : self.n]
+        self.host[5][:] = applied
+        self.host[6][:] = ba[0]
+        self.host[7][:] = ba[1]
+
+
+def injection_for(hook, iteration, dtype):
+    if hook is None:
+        return None
+    arrs = hook.kernel_arrays(iteration, np.dtype(dtype))
+    if arrs is None:
+        return None
+    return DevInjection(arrs)
+
+
+class DevEvents:
+    """Detection-event ring on the device (abft.py:281-294)."""
+
+    def __init__(self, cap):
+        t = _torch()
+        self.cap = int(cap)
+        self.rec = t.zeros((max(self.cap, 1), 7), dtype=t.int64, device=device())
+        self.delta = t.zeros(max(self.cap, 1), dtype=t.float64, device=device())
+        self.count = t.zeros(1, dtype=t.int64, device=device())
+        self.struct = N.Events(self.cap, self.rec.data_ptr(), self.delta.data_ptr(),
+                               self.count.data_ptr())
+
+    def ref(self):
+        import ctypes
+
+        return ctypes.byref(self.struct)
+
+    def reset(self):
+        self.count.zero_()
+
+    def read(self):
+        """-> (overflowed, [(rec7..., delta)])"""
+        n = int(self.count.item())
+        m = min(n, self.cap)
+        if m == 0:
+            return n > self.cap, []
+        rec = to_host(self.rec[:m])
+        delta = to_host(self.delta[:m])
+        return n > self.cap, [(tuple(int(v) for v in rec[i]), float(delta[i])) for i in range(m)]
+
+
+# ------------------------------------------------------------ kernels ----
+def row_sq_norms_dev(x_t):
+    t = _torch()
+    out = t.empty(x_t.shape[0], dtype=x_t.dtype, device=x_t.device)
+    N.check(N.load().ftk_row_sq_norms(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), x_t.shape[0],
+                                      x_t.shape[1], ptr(out), stream()), "ftk_row_sq_norms")
+    return out
+
+
+def row_sq_norms(x):
+    if x.shape[0] == 0:
+        return np.empty(0, dtype=x.dtype)
+    return to_host(row_sq_norms_dev(to_dev(x)))
+
+
+def assign_dev(x_t, y_t, yn_t, block, variant="auto", inj=None, checked=False, delta_rel=0.0,
+               abs_tol=0.0, iteration=0, events=None, out_idx=None, out_val=None):
+    """Launch the fused assignment; returns (labels int32 tensor, min_dists tensor)."""
+    t = _torch()
+    m, d = x_t.shape
+    k = y_t.shape[0]
+    dt = ndtype(x_t.dtype)
+    if out_idx is None:
+        out_idx = t.empty(m, dtype=t.int32, device=x_t.device)
+    if out_val is None:
+        out_val = t.empty(m, dtype=x_t.dtype, device=x_t.device)
+    bm, bn, bk = (int(v) for v in block)
+    lib = N.load()
+    injp = inj.ref() if inj is not None else None
+    if checked:
+        rc = lib.ftk_checked_assign(ctx(), code(dt), variant_code(variant), ptr(x_t), ptr(y_t),
+                                    ptr(yn_t), m, k, d, bm, bn, bk, float(delta_rel),
+                                    float(abs_tol), int(iteration), ptr(out_idx), ptr(out_val),
+                                    injp, events.ref(), stream())
+        N.check(rc, "ftk_checked_assign")
+    else:
+        rc = lib.ftk_assign(ctx(), code(dt), variant_code(variant), ptr(x_t), ptr(y_t),
+                            ptr(yn_t), m, k, d, bm, bn, bk, ptr(out_idx), ptr(out_val), injp,
+                            stream())
+        N.check(rc, "ftk_assign")
+    return out_idx, out_val
+
+
+def gemm_dev(x_t, y_t, block, inj=None, checked=False, delta_rel=0.0, abs_tol=0.0, iteration=0,
+             events=None):
+    t = _torch()
+    m, d = x_t.shape
+    k = y_t.shape[0]
+    out = t.empty((m, k), dtype=x_t.dtype, device=x_t.device)
+    bm, bn, bk = (int(v) for v in block)
+    rc = N.load().ftk_gemm(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), ptr(y_t), m, k, d, bm, bn,
+                           bk, float(delta_rel), float(abs_tol), int(iteration), ptr(out),
+                           inj.ref() if inj is not None else None,
+                           events.ref() if (checked and events is not None) else None, stream())
+    N.check(rc, "ftk_gemm")
+    return out
+
+
+def update_sums_dev(x_t, labels_i32, k, dmr=False):
+    t = _torch()
+    m, d = x_t.shape
+    dev = x_t.device
+    sums_a = t.empty((k, d), dtype=t.float64, device=dev)
+    counts_a = t.empty(k, dtype=t.int64, device=dev)
+    sums_b = t.empty((k, d), dtype=t.float64, device=dev) if dmr else None
+    counts_b = t.empty(k, dtype=t.int64, device=dev) if dmr else None
+    rc = N.load().ftk_update_sums(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), ptr(labels_i32), m, d,
+                                  k, ptr(sums_a), ptr(counts_a), ptr(sums_b), ptr(counts_b),
+                                  stream())
+    N.check(rc, "ftk_update_sums")
+    return sums_a, counts_a, sums_b, counts_b
+
+
+def dmr_mismatch_dev(sa, ca, sb, cb, flag):
+    k, d = sa.shape
+    N.check(N.load().ftk_dmr_compare(ctx(), ptr(sa), ptr(ca), ptr(sb), ptr(cb), k, d, ptr(flag),
+                                     stream()), "ftk_dmr_compare")
+
+
+def finalize_dev(sums, counts, dtype, out=None, n_empty=None):
+    t = _torch()
+    k, d = sums.shape
+    if out is None:
+        out = t.empty((k, d), dtype=tdtype(dtype), device=sums.device)
+    N.check(N.load().ftk_update_finalize(ctx(), code(dtype), ptr(sums), ptr(counts), k, d,
+                                         ptr(out), ptr(n_empty), stream()), "ftk_update_finalize")
+    return out
+
+
+def reseed_dev(x_t, counts, sq, cent):
+    m, d = x_t.shape
+    N.check(N.load().ftk_reseed_empty(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), m, d,
+                                      ptr(counts), counts.shape[0], ptr(sq), ptr(cent), stream()),
+            "ftk_reseed_empty")
+
+
+def sq_dists_dev(md, xsq, out):
+    N.check(N.load().ftk_sq_dists(ctx(), code(ndtype(md.dtype)), ptr(md), ptr(xsq), md.shape[0],
+                                  ptr(out), stream()), "ftk_sq_dists")
+    return out
+
+
+def pairwise_sum_dev(a, out):
+    N.check(N.load().ftk_pairwise_sum(ctx(), ptr(a), a.shape[0], ptr(out), stream()),
+            "ftk_pairwise_sum")
+    return out
+
+
+def movement_dev(new_c, old_c, eps, out):
+    k, d = new_c.shape
+    N.check(N.load().ftk_movement(ctx(), code(ndtype(new_c.dtype)), ptr(new_c), ptr(old_c), k, d,
+                                  float(eps), ptr(out), stream()), "ftk_movement")
+    return out
+
+
+def labels_equal_dev(a, b, out):
+    N.check(N.load().ftk_labels_equal(ctx(), ptr(a), ptr(b), a.shape[0], ptr(out), stream()),
+            "ftk_labels_equal")
+    return out
+
+
+def flip_f64_dev(a, i, j, bit, ba):
+    N.check(N.load().ftk_flip_f64(ctx(), ptr(a), a.shape[1], int(i), int(j), int(bit), ptr(ba),
+                                  stream()), "ftk_flip_f64")
+
+
+def own_sq_dists_dev(x_t, labels_i32, cent64, out):
+    m, d = x_t.shape
+    N.check(N.load().ftk_own_sq_dists(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), ptr(labels_i32),
+                                      ptr(cent64), m, d, ptr(out), stream()), "ftk_own_sq_dists")
+    return out

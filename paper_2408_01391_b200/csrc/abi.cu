@@ -1,0 +1,203 @@
+// abi.cu -- extern "C" entry points (include/ftk_b200.h), context, errors.
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+
+namespace ftk {
+
+static thread_local std::string g_err;
+static std::atomic<int64_t> g_launches{0};
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return FTK_ERR_CUDA;
+}
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st) {
+    Scratch &s = ctx->slots[slot];
+    if (bytes == 0) bytes = 16;
+    if (s.bytes >= bytes) return s.ptr;
+    if (s.ptr) {
+        cudaStreamSynchronize(st);
+        cudaFree(s.ptr);
+        s.ptr = nullptr;
+        s.bytes = 0;
+    }
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&s.ptr, want);
+    if (e != cudaSuccess) {
+        cuda_fail(e, "scratch cudaMalloc");
+        s.ptr = nullptr;
+        return nullptr;
+    }
+    s.bytes = want;
+    return s.ptr;
+}
+
+// implemented in exact.cu / update.cu / tc.cu
+int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t, int64_t,
+              int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
+              const ftk_injection *, ftk_events *, cudaStream_t);
+int row_sq_norms_run(int, const void *, int64_t, int64_t, void *, cudaStream_t);
+int update_sums_run(ftk_ctx *, int, const void *, const int32_t *, int64_t, int64_t, int64_t,
+                    double *, int64_t *, double *, int64_t *, cudaStream_t);
+int dmr_compare_run(const double *, const int64_t *, const double *, const int64_t *, int64_t,
+                    int64_t, int32_t *, cudaStream_t);
+int finalize_run(int, const double *, const int64_t *, int64_t, int64_t, void *, int32_t *,
+                 cudaStream_t);
+int reseed_run(ftk_ctx *, int, const void *, int64_t, int64_t, const int64_t *, int64_t, double *,
+               void *, cudaStream_t);
+int sq_dists_run(int, const void *, const double *, int64_t, double *, cudaStream_t);
+int pairwise_sum_run(ftk_ctx *, const double *, int64_t, double *, cudaStream_t);
+int movement_run(ftk_ctx *, int, const void *, const void *, int64_t, int64_t, double, double *,
+                 cudaStream_t);
+int labels_equal_run(const int32_t *, const int32_t *, int64_t, int32_t *, cudaStream_t);
+int own_sq_dists_run(ftk_ctx *, int, const void *, const int32_t *, const double *, int64_t,
+                     int64_t, double *, cudaStream_t);
+int flip_f64_run(double *, int64_t, int64_t, int64_t, int64_t, double *, cudaStream_t);
+int tc_assign_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
+                  int64_t, int32_t *, void *, cudaStream_t);
+
+static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
+
+}  // namespace ftk
+
+using namespace ftk;
+
+extern "C" {
+
+const char *ftk_last_error(void) { return g_err.c_str(); }
+int ftk_version(void) { return 1; }
+int64_t ftk_launch_count(void) { return g_launches.load(); }
+
+ftk_ctx *ftk_ctx_create(int device) {
+    if (cudaSetDevice(device) != cudaSuccess) {
+        set_error("cudaSetDevice failed");
+        return nullptr;
+    }
+    ftk_ctx *c = new ftk_ctx();
+    c->device = device;
+    return c;
+}
+
+void ftk_ctx_destroy(ftk_ctx *ctx) {
+    if (!ctx) return;
+    cudaDeviceSynchronize();
+    for (auto &s : ctx->slots)
+        if (s.ptr) cudaFree(s.ptr);
+    delete ctx;
+}
+
+int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,
+                     void *stream) {
+    (void)ctx;
+    if (!dtype_ok(dtype) || n < 1) { set_error("bad dtype/shape"); return FTK_ERR_ARG; }
+    return row_sq_norms_run(dtype, x, m, n, out, as_stream(stream));
+}
+
+int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *y,
+               const void *ynorms, int64_t m, int64_t k, int64_t d, int64_t bm, int64_t bn,
+               int64_t bk, int32_t *out_idx, void *out_val, const ftk_injection *inj,
+               void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    cudaStream_t st = as_stream(stream);
+    bool has_inj = inj && inj->n > 0;
+    if (variant == FTK_VARIANT_TC || (variant == FTK_VARIANT_AUTO && !has_inj)) {
+        int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st);
+        if (rc != FTK_ERR_UNSUPPORTED || variant == FTK_VARIANT_TC) return rc;
+    }
+    return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
+                     false, 0.0, 0.0, 0, inj, nullptr, st);
+}
+
+int ftk_checked_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *y,
+                       const void *ynorms, int64_t m, int64_t k, int64_t d, int64_t bm,
+                       int64_t bn, int64_t bk, double delta_rel, double abs_tol,
+                       int64_t iteration, int32_t *out_idx, void *out_val,
+                       const ftk_injection *inj, ftk_events *ev, void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    (void)variant;
+    return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
+                     true, delta_rel, abs_tol, iteration, inj, ev, as_stream(stream));
+}
+
+int ftk_gemm(ftk_ctx *ctx, int dtype, const void *x, const void *y, int64_t m, int64_t k,
+             int64_t d, int64_t bm, int64_t bn, int64_t bk, double delta_rel, double abs_tol,
+             int64_t iteration, void *out, const ftk_injection *inj, ftk_events *ev,
+             void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    return exact_run(ctx, dtype, x, y, nullptr, m, k, d, bm, bn, bk, nullptr, nullptr, out,
+                     ev != nullptr, delta_rel, abs_tol, iteration, inj, ev, as_stream(stream));
+}
+
+int ftk_update_sums(ftk_ctx *ctx, int dtype, const void *x, const int32_t *labels, int64_t m,
+                    int64_t d, int64_t k, double *sums_a, int64_t *counts_a, double *sums_b,
+                    int64_t *counts_b, void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    return update_sums_run(ctx, dtype, x, labels, m, d, k, sums_a, counts_a, sums_b, counts_b,
+                           as_stream(stream));
+}
+
+int ftk_dmr_compare(ftk_ctx *ctx, const double *sums_a, const int64_t *counts_a,
+                    const double *sums_b, const int64_t *counts_b, int64_t k, int64_t d,
+                    int32_t *out_mismatch, void *stream) {
+    (void)ctx;
+    return dmr_compare_run(sums_a, counts_a, sums_b, counts_b, k, d, out_mismatch,
+                           as_stream(stream));
+}
+
+int ftk_update_finalize(ftk_ctx *ctx, int dtype, const double *sums, const int64_t *counts,
+                        int64_t k, int64_t d, void *centroids, int32_t *n_empty, void *stream) {
+    (void)ctx;
+    if (!dtype_ok(dtype)) { set_error("bad dtype"); return FTK_ERR_ARG; }
+    return finalize_run(dtype, sums, counts, k, d, centroids, n_empty, as_stream(stream));
+}
+
+int ftk_reseed_empty(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d,
+                     const int64_t *counts, int64_t k, double *sq_dists, void *centroids,
+                     void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    return reseed_run(ctx, dtype, x, m, d, counts, k, sq_dists, centroids, as_stream(stream));
+}
+
+int ftk_sq_dists(ftk_ctx *ctx, int dtype, const void *min_dists, const double *x_sq, int64_t m,
+                 double *sq, void *stream) {
+    (void)ctx;
+    return sq_dists_run(dtype, min_dists, x_sq, m, sq, as_stream(stream));
+}
+
+int ftk_pairwise_sum(ftk_ctx *ctx, const double *a, int64_t n, double *out, void *stream) {
+    if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    return pairwise_sum_run(ctx, a, n, out, as_stream(stream));
+}
+
+int ftk_movement(ftk_ctx *ctx, int dtype, const void *new_c, const void *old_c, int64_t k,
+                 int64_t d, double eps, double *moved, void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    return movement_run(ctx, dtype, new_c, old_c, k, d, eps, moved, as_stream(stream));
+}
+
+int ftk_labels_equal(ftk_ctx *ctx, const int32_t *a, const int32_t *b, int64_t m, int32_t *out,
+                     void *stream) {
+    (void)ctx;
+    return labels_equal_run(a, b, m, out, as_stream(stream));
+}
+
+int ftk_own_sq_dists(ftk_ctx *ctx, int dtype, const void *x, const int32_t *labels,
+                     const double *cent64, int64_t m, int64_t d, double *out, void *stream) {
+    if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    return own_sq_dists_run(ctx, dtype, x, labels, cent64, m, d, out, as_stream(stream));
+}
+
+int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64_t bit,
+                 double *before_after, void *stream) {
+    (void)ctx;
+    return flip_f64_run(a, d, i, j, bit, before_after, as_stream(stream));
+}
+
+}  // extern "C"

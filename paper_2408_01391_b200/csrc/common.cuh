@@ -1,0 +1,104 @@
+// common.cuh -- shared helpers for the B200 FT K-means kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "../../include/ftk_b200.h"
+
+namespace ftk {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+void count_launch(int n = 1);
+
+#define FTK_CUDA(call)                                        \
+    do {                                                      \
+        cudaError_t e_ = (call);                              \
+        if (e_ != cudaSuccess) return ::ftk::cuda_fail(e_, #call); \
+    } while (0)
+
+#define FTK_LAUNCHED(what)                                           \
+    do {                                                             \
+        ::ftk::count_launch();                                       \
+        cudaError_t e_ = cudaGetLastError();                         \
+        if (e_ != cudaSuccess) return ::ftk::cuda_fail(e_, what);    \
+    } while (0)
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------- scratch --
+// Per-context cached device scratch (grown on demand, never shrunk).
+struct Scratch {
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+
+}  // namespace ftk
+
+struct ftk_ctx {
+    int device = 0;
+    ftk::Scratch slots[16];
+};
+
+namespace ftk {
+// Returns a device buffer of at least `bytes` for `slot` of this context.
+void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
+
+enum ScratchSlot {
+    SLOT_BMAX = 0,
+    SLOT_SORT_KEYS = 1,
+    SLOT_SORT_VALS = 2,
+    SLOT_SORT_TMP = 3,
+    SLOT_OFFSETS = 4,
+    SLOT_PAIRWISE = 5,
+    SLOT_MISC = 6,
+    SLOT_TC_A = 7,
+    SLOT_TC_B = 8,
+    SLOT_TC_ROWS = 9,
+    SLOT_TC_MISC = 10,
+    SLOT_INJ = 11,
+};
+
+// ------------------------------------------------------- float helpers --
+template <typename T> struct Bits;
+template <> struct Bits<float> { using U = uint32_t; static constexpr int W = 32; };
+template <> struct Bits<double> { using U = unsigned long long; static constexpr int W = 64; };
+
+// Correctly rounded single operations that nvcc may not contract into FMA.
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T flip_bit(T v, int64_t bit) {
+    using U = typename Bits<T>::U;
+    U u;
+    memcpy(&u, &v, sizeof(T));
+    u ^= (U(1) << U(bit));
+    T r;
+    memcpy(&r, &u, sizeof(T));
+    return r;
+}
+
+// Lexicographic (value, index) minimum with the reference's candidate rule:
+// a value only wins if it compares below the running best, so NaN and +inf
+// never win and the default is (+inf, 0) (_kernels.py:88-102, 450-452).
+template <typename T>
+__device__ __forceinline__ void argmin_merge(T &bv, int32_t &bj, T v, int32_t j) {
+    if (v < bv || (v == bv && j < bj)) {
+        bv = v;
+        bj = j;
+    }
+}
+
+}  // namespace ftk

@@ -1,0 +1,653 @@
+// exact.cu -- SIMT assignment / GEMM kernels that evaluate every accumulator
+// in the reference's exact floating-point order (sm_100a).
+//
+// Compiled with --fmad=false: every product and sum is a separate IEEE
+// rounding, k ascending from 0.0, exactly like the reference's numba tile
+// kernels (_kernels.py:44-70; no FMA, SURVEY.md App. B probe 2).  One CTA owns
+// one LOGICAL row block (TileConfig.block rows) and sweeps every logical
+// column block, so the fault grid, tile-local coordinates, checksum tolerance
+// and event records are the reference's own (_kernels.py:479-612).  Thread
+// (r, j) owns column j of the tile and TM consecutive rows, which makes the
+// e1 column checksum of _checked_range a per-thread quantity.
+//
+// This is the parity path: labels, min_dists, corrected values, events and
+// deltas are bit-identical to the reference.  It also serves rows the tensor
+// core screen cannot certify (tc.cu).
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace ftk {
+
+constexpr int KC = 16;  // k-chunk staged in shared memory per step
+
+struct ExactParams {
+    const void *x, *y, *yn;
+    int64_t m, k, d, bm, bn, bk;
+    int pb;  // physical tile width (live columns of a logical column block)
+    int32_t *out_idx;
+    void *out_val;
+    void *out_mat;  // materialise x @ y.T when non-null
+    // checked mode
+    double delta_rel, abs_tol;
+    int64_t iteration;
+    const double *bmax;  // per logical column block: max |y| over its rows
+    // injection (faults.py:261-277 arrays, device)
+    int64_t n_inj;
+    const int64_t *ibi, *ibj, *iei, *iej, *ibit;
+    int64_t *iapplied;
+    double *ibefore, *iafter;
+    // events (abft.py:281-294)
+    int64_t ev_cap;
+    int64_t *ev_rec;
+    double *ev_delta;
+    unsigned long long *ev_count;
+};
+
+struct SmemLayout {
+    size_t xs, cs, c1, tile, diag, red, total;
+};
+
+template <typename T>
+__host__ __device__ static SmemLayout smem_layout(int64_t bm, int pb, int64_t bk, bool checked, bool mat) {
+    SmemLayout L{};
+    size_t off = 0;
+#define take(bytes) (off += (((bytes) + 15) & ~size_t(15)), off - (((bytes) + 15) & ~size_t(15)))
+    L.xs = take(sizeof(T) * KC * bm);
+    L.cs = take(sizeof(T) * pb * (KC + 1));
+    L.c1 = take(sizeof(double) * KC);
+    L.tile = (checked || mat) ? take(sizeof(T) * bm * (pb + 1)) : 0;
+    // diag: s1 ref1 s2 ref2 (pb each), t1 t2 r1 r2 (bm each), rs1 rs2 c2 (bk each), ints
+    L.diag = checked ? take(sizeof(double) * (4 * pb + 4 * bm + 3 * bk) + 64) : 0;
+    size_t red = (sizeof(T) + sizeof(int32_t)) * bm * ((pb + 31) / 32 + 1) + 64;
+    L.red = take(red > 512 ? red : 512);
+#undef take
+    L.total = off;
+    return L;
+}
+
+// ------------------------------------------------------ block reductions --
+__device__ __forceinline__ int block_sum_int(int v, int *sh) {
+    __syncthreads();
+    if (threadIdx.x == 0) *sh = 0;
+    __syncthreads();
+    if (v) atomicAdd(sh, v);
+    __syncthreads();
+    int r = *sh;
+    __syncthreads();
+    return r;
+}
+
+// ------------------------------------------------ diagnose (rare path) --
+// Restates _diagnose (_kernels.py:321-405) and _recheck (298-317) with the
+// block cooperating where the reference's loops are independent and a
+// single thread where they are sequential.  `tile` holds the tile in dtype,
+// row stride ts.  Returns kind (0 corrected, 1 uncorrectable) via smem ints.
+template <typename T>
+__device__ void diagnose(const ExactParams &P, T *tile, int ts, double *s1, double *ref1,
+                         double *s2, double *ref2, double *t1, double *t2, double *r1,
+                         double *r2, double *rs1, double *rs2, double *c2, int *ints,
+                         int64_t i0, int mi, int64_t j0, int nj, int64_t t_last, double tol,
+                         double *out_delta) {
+    const T *a = static_cast<const T *>(P.x);
+    const T *b = static_cast<const T *>(P.y);
+    const int64_t kdim = P.d;
+    const int64_t bk = P.bk;
+    const int tid = threadIdx.x, nth = blockDim.x;
+
+    // _tile_colsums_w / _tile_rowsums
+    for (int j = tid; j < nj; j += nth) {
+        double s = 0.0;
+        for (int i = 0; i < mi; ++i) s = add_rn(s, mul_rn(double(i + 1), double(tile[i * ts + j])));
+        s2[j] = s;
+    }
+    for (int i = tid; i < mi; i += nth) {
+        double a1 = 0.0, a2 = 0.0;
+        for (int j = 0; j < nj; ++j) {
+            double v = double(tile[i * ts + j]);
+            a1 = add_rn(a1, v);
+            a2 = add_rn(a2, mul_rn(double(j + 1), v));
+        }
+        t1[i] = a1;
+        t2[i] = a2;
+        r1[i] = 0.0;
+        r2[i] = 0.0;
+    }
+    for (int j = tid; j < nj; j += nth) ref2[j] = 0.0;
+    __syncthreads();
+    // _row_refs_replay and _col_ref2_replay, interval by interval
+    for (int64_t tt = 0; tt <= t_last; ++tt) {
+        int64_t k0 = tt * bk;
+        int kk = int(bk < kdim - k0 ? bk : kdim - k0);
+        for (int k = tid; k < kk; k += nth) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int j = 0; j < nj; ++j) {
+                double v = double(b[(j0 + j) * kdim + k0 + k]);
+                a1 = add_rn(a1, v);
+                a2 = add_rn(a2, mul_rn(double(j + 1), v));
+            }
+            rs1[k] = a1;
+            rs2[k] = a2;
+            double c = 0.0;
+            for (int i = 0; i < mi; ++i)
+                c = add_rn(c, mul_rn(double(i + 1), double(a[(i0 + i) * kdim + k0 + k])));
+            c2[k] = c;
+        }
+        __syncthreads();
+        for (int i = tid; i < mi; i += nth) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int k = 0; k < kk; ++k) {
+                double v = double(a[(i0 + i) * kdim + k0 + k]);
+                a1 = add_rn(a1, mul_rn(v, rs1[k]));
+                a2 = add_rn(a2, mul_rn(v, rs2[k]));
+            }
+            r1[i] = add_rn(r1[i], a1);
+            r2[i] = add_rn(r2[i], a2);
+        }
+        for (int j = tid; j < nj; j += nth) {
+            double s = ref2[j];
+            for (int k = 0; k < kk; ++k)
+                s = add_rn(s, mul_rn(c2[k], double(b[(j0 + j) * kdim + k0 + k])));
+            ref2[j] = s;
+        }
+        __syncthreads();
+    }
+    // _count_viol on columns and rows: count + first index
+    if (tid == 0) {
+        ints[0] = 0; ints[1] = 0x7fffffff; ints[2] = 0; ints[3] = 0x7fffffff;
+    }
+    __syncthreads();
+    for (int j = tid; j < nj; j += nth) {
+        double dd = s1[j] - ref1[j];
+        if (!(fabs(dd) <= tol)) { atomicAdd(&ints[0], 1); atomicMin(&ints[1], j); }
+    }
+    for (int i = tid; i < mi; i += nth) {
+        double dd = t1[i] - r1[i];
+        if (!(fabs(dd) <= tol)) { atomicAdd(&ints[2], 1); atomicMin(&ints[3], i); }
+    }
+    __syncthreads();
+    // scalar decision logic (thread 0), result in ints[4..6]
+    if (tid == 0) {
+        int ncv = ints[0], jhat = ncv ? ints[1] : -1;
+        int nrv = ints[2], ihat = nrv ? ints[3] : -1;
+        int kind = -1;
+        double delta = 0.0;
+        auto saturate = [](double v) {
+            if (isnan(v)) return DBL_MAX;
+            if (v > DBL_MAX) return DBL_MAX;
+            if (v < -DBL_MAX) return -DBL_MAX;
+            return v;
+        };
+        if (ncv == 1 && nrv == 0) {
+            double dq1 = s1[jhat] - ref1[jhat];
+            double dq2 = s2[jhat] - ref2[jhat];
+            if (isfinite(dq1) && isfinite(dq2) && dq1 != 0.0) {
+                double q = floor(dq2 / dq1 + 0.5);
+                long long ri = (q >= -9.0e18 && q <= 9.0e18) ? (long long)q : LLONG_MIN;
+                if (ri >= 1 && ri <= mi) { ihat = int(ri - 1); nrv = 1; }
+            }
+        }
+        if (ncv != 1 || nrv != 1) {
+            double dd = jhat >= 0 ? s1[jhat] - ref1[jhat] : 0.0;
+            kind = 1;
+            delta = saturate(dd);
+        } else {
+            double dc1 = s1[jhat] - ref1[jhat];
+            double dc2 = s2[jhat] - ref2[jhat];
+            double dr1 = t1[ihat] - r1[ihat];
+            double dr2 = t2[ihat] - r2[ihat];
+            if (isfinite(dc1) && isfinite(dc2) && isfinite(dr1) && isfinite(dr2)) {
+                double lim = 0.05 * fabs(dc1);
+                if (!(fabs(dc1 - dr1) <= (tol > lim ? tol : lim))) {
+                    kind = 1;
+                    delta = saturate(dc1);
+                } else if (fabs(dc1) > 32.0 * tol) {
+                    double qi = dc2 / dc1, qj = dr2 / dr1;
+                    double fi = floor(qi + 0.5), fj = floor(qj + 0.5);
+                    long long ri = (fi >= -9.0e18 && fi <= 9.0e18) ? (long long)fi : LLONG_MIN;
+                    long long rj = (fj >= -9.0e18 && fj <= 9.0e18) ? (long long)fj : LLONG_MIN;
+                    if (fabs(qi - double(ri)) > 0.05 || fabs(qj - double(rj)) > 0.05 || ri < 1 ||
+                        ri > mi || rj < 1 || rj > nj || ri - 1 != ihat || rj - 1 != jhat) {
+                        kind = 1;
+                        delta = saturate(dc1);
+                    }
+                }
+                if (kind < 0) delta = dc1;
+            } else {
+                delta = saturate(dc1);
+            }
+            if (kind < 0) {
+                // acc[ihat, jhat] = ref1[jhat] - sum_{i != ihat} acc[i, jhat]
+                double other = 0.0;
+                for (int i = 0; i < mi; ++i)
+                    if (i != ihat) other = add_rn(other, double(tile[i * ts + jhat]));
+                tile[ihat * ts + jhat] = T(ref1[jhat] - other);
+                kind = 2;  // pending recheck
+            }
+        }
+        ints[4] = kind;
+        ints[5] = ihat;
+        ints[6] = jhat;
+        *out_delta = delta;
+        ints[7] = 0;  // recheck failures
+    }
+    __syncthreads();
+    if (ints[4] == 2) {
+        // _recheck: all four checksums of the corrected tile
+        for (int j = tid; j < nj; j += nth) {
+            double s = 0.0;
+            int i = 0;
+            for (; i + 4 <= mi; i += 4) {
+                T p = add_rn(add_rn(tile[i * ts + j], tile[(i + 1) * ts + j]),
+                             add_rn(tile[(i + 2) * ts + j], tile[(i + 3) * ts + j]));
+                s = add_rn(s, double(p));
+            }
+            for (; i < mi; ++i) s = add_rn(s, double(tile[i * ts + j]));
+            double w = 0.0;
+            for (int ii = 0; ii < mi; ++ii)
+                w = add_rn(w, mul_rn(double(ii + 1), double(tile[ii * ts + j])));
+            if (!(fabs(s - ref1[j]) <= tol)) atomicAdd(&ints[7], 1);
+            if (!(fabs(w - ref2[j]) <= tol * nj)) atomicAdd(&ints[7], 1);
+        }
+        for (int i = tid; i < mi; i += nth) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int j = 0; j < nj; ++j) {
+                double v = double(tile[i * ts + j]);
+                a1 = add_rn(a1, v);
+                a2 = add_rn(a2, mul_rn(double(j + 1), v));
+            }
+            if (!(fabs(a1 - r1[i]) <= tol)) atomicAdd(&ints[7], 1);
+            if (!(fabs(a2 - r2[i]) <= tol * mi)) atomicAdd(&ints[7], 1);
+        }
+        __syncthreads();
+        if (tid == 0) ints[4] = ints[7] ? 1 : 0;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ kernel --
+__host__ __device__ constexpr int exact_max_threads(int tm) {
+    return tm <= 4 ? 1024 : (tm == 8 ? 512 : 256);
+}
+
+template <typename T, int TM, bool CHECKED>
+__global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(ExactParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int pb = P.pb;
+    const int64_t bm = P.bm, bn = P.bn, kdim = P.d;
+    const SmemLayout L = smem_layout<T>(bm, pb, P.bk, CHECKED, P.out_mat != nullptr);
+    T *Xs = reinterpret_cast<T *>(smem + L.xs);
+    T *Cs = reinterpret_cast<T *>(smem + L.cs);
+    double *c1s = reinterpret_cast<double *>(smem + L.c1);
+    T *tile = reinterpret_cast<T *>(smem + L.tile);
+    const int ts = pb + 1;
+
+    const T *x = static_cast<const T *>(P.x);
+    const T *y = static_cast<const T *>(P.y);
+    const T *yn = static_cast<const T *>(P.yn);
+
+    const int tid = threadIdx.x, nth = blockDim.x;
+    const int jl = tid % pb;   // column within the tile
+    const int r = tid / pb;    // row group (r >= bm / TM: padding thread)
+    const bool real_row_group = r * TM < bm;
+    const int64_t bi = blockIdx.x;
+    const int64_t i0 = bi * bm;
+    const int mi = int(bm < P.m - i0 ? bm : P.m - i0);
+    const int64_t nbj = (P.k + bn - 1) / bn;
+    const int64_t nbk = (kdim + P.bk - 1) / P.bk;
+
+    T bestv[TM];
+    int32_t bestj[TM];
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+        bestv[t] = T(INFINITY);
+        bestj[t] = 0;
+    }
+
+    // checked-mode per-row-block quantity: amax over the row block (all D)
+    double amax_a = 0.0;
+    if (CHECKED) {
+        double am = 0.0;
+        for (int64_t e = tid; e < int64_t(mi) * kdim; e += nth) {
+            double v = double(x[i0 * kdim + e]);
+            double av = v < 0.0 ? -v : v;
+            am = av > am ? av : am;
+        }
+        // block max
+        for (int off = 16; off; off >>= 1) {
+            double o = __shfl_xor_sync(0xffffffffu, am, off);
+            am = o > am ? o : am;
+        }
+        double *red = reinterpret_cast<double *>(smem + L.red);
+        __syncthreads();
+        if ((tid & 31) == 0) red[tid >> 5] = am;
+        __syncthreads();
+        if (tid == 0) {
+            double mm = 0.0;
+            for (int w = 0; w < (nth + 31) / 32; ++w) mm = red[w] > mm ? red[w] : mm;
+            red[0] = mm;
+        }
+        __syncthreads();
+        amax_a = red[0];
+        __syncthreads();
+    }
+
+    for (int64_t bj = 0; bj < nbj; ++bj) {
+        const int64_t j0 = bj * bn;
+        const int nj = int(bn < P.k - j0 ? bn : P.k - j0);
+        const bool live_col = jl < nj;
+        T acc[TM];
+#pragma unroll
+        for (int t = 0; t < TM; ++t) acc[t] = T(0);
+        double ref1 = 0.0;
+
+        for (int64_t k0 = 0; k0 < kdim; k0 += KC) {
+            const int kc = int(KC < kdim - k0 ? KC : kdim - k0);
+            __syncthreads();
+            // stage X tile (transposed, k-major) and the centroid panel
+            for (int e = tid; e < mi * KC; e += nth) {
+                int i = e / KC, kk = e % KC;
+                Xs[kk * bm + i] = kk < kc ? x[(i0 + i) * kdim + k0 + kk] : T(0);
+            }
+            for (int e = tid; e < pb * KC; e += nth) {
+                int j = e / KC, kk = e % KC;
+                Cs[j * (KC + 1) + kk] = (j < nj && kk < kc) ? y[(j0 + j) * kdim + k0 + kk] : T(0);
+            }
+            __syncthreads();
+            if (CHECKED) {
+                // e1 column encoding of the row block (_encode_c1_amax)
+                for (int kk = tid; kk < kc; kk += nth) {
+                    double s = 0.0;
+                    for (int i = 0; i < mi; ++i) s = add_rn(s, double(Xs[kk * bm + i]));
+                    c1s[kk] = s;
+                }
+                __syncthreads();
+            }
+            const T *xr = Xs + r * TM;
+            const T *cr = Cs + jl * (KC + 1);
+            for (int kk = 0; kk < kc; ++kk) {
+                const T cv = cr[kk];
+                const T *xk = xr + kk * bm;
+#pragma unroll
+                for (int t = 0; t < TM; ++t) acc[t] = add_rn(acc[t], mul_rn(xk[t], cv));
+                if (CHECKED) ref1 = add_rn(ref1, mul_rn(c1s[kk], double(cv)));
+            }
+        }
+
+        // scheduled flips on the accumulator after the last k-interval
+        // (_kernels.py:462-474 / 568-583)
+        if (P.n_inj > 0 && live_col) {
+            for (int64_t q = 0; q < P.n_inj; ++q) {
+                if (P.ibi[q] != bi || P.ibj[q] != bj) continue;
+                int64_t ei = P.iei[q], ej = P.iej[q];
+                if (ej != jl || ei >= mi || ej >= nj) continue;
+#pragma unroll
+                for (int t = 0; t < TM; ++t) {
+                    if (r * TM + t == ei) {
+                        T before = acc[t];
+                        T after = flip_bit(before, P.ibit[q]);
+                        acc[t] = after;
+                        P.iapplied[q] = 1;
+                        P.ibefore[q] = double(before);
+                        P.iafter[q] = double(after);
+                    }
+                }
+            }
+        }
+
+        if (CHECKED || P.out_mat) {
+            __syncthreads();
+#pragma unroll
+            for (int t = 0; t < TM; ++t)
+                if (r * TM + t < mi) tile[(r * TM + t) * ts + jl] = acc[t];
+            __syncthreads();
+        }
+
+        if (CHECKED) {
+            double *dg = reinterpret_cast<double *>(smem + L.diag);
+            double *s1 = dg, *rf1 = dg + pb, *s2 = dg + 2 * pb, *rf2 = dg + 3 * pb;
+            double *t1 = dg + 4 * pb, *t2 = t1 + bm, *r1 = t2 + bm, *r2 = r1 + bm;
+            double *rs1 = r2 + bm, *rs2 = rs1 + P.bk, *c2 = rs2 + P.bk;
+            int *ints = reinterpret_cast<int *>(c2 + P.bk);
+            double scale = amax_a * P.bmax[bj];
+            if (scale < 1.0) scale = 1.0;
+            const double tol_base = P.delta_rel * scale;
+            const double tol = tol_base * double(kdim) + P.abs_tol;
+            int viol = 0;
+            if (r == 0 && live_col) {
+                // _tile_colsums: 4-row pre-reduce in dtype, then float64
+                double s = 0.0;
+                int i = 0;
+                for (; i + 4 <= mi; i += 4) {
+                    T p = add_rn(add_rn(tile[i * ts + jl], tile[(i + 1) * ts + jl]),
+                                 add_rn(tile[(i + 2) * ts + jl], tile[(i + 3) * ts + jl]));
+                    s = add_rn(s, double(p));
+                }
+                for (; i < mi; ++i) s = add_rn(s, double(tile[i * ts + jl]));
+                s1[jl] = s;
+                rf1[jl] = ref1;
+                viol = !(fabs(s - ref1) <= tol);
+            }
+            int nviol = block_sum_int(viol, ints + 8);
+            if (nviol) {
+                double delta = 0.0;
+                diagnose<T>(P, tile, ts, s1, rf1, s2, rf2, t1, t2, r1, r2, rs1, rs2, c2, ints,
+                            i0, mi, j0, nj, nbk - 1, tol, &delta);
+                if (tid == 0) {
+                    unsigned long long c = atomicAdd(P.ev_count, 1ull);
+                    if (int64_t(c) < P.ev_cap) {
+                        int64_t *rec = P.ev_rec + c * 7;
+                        rec[0] = P.iteration;
+                        rec[1] = bi;
+                        rec[2] = bj;
+                        rec[3] = ints[4];
+                        rec[4] = ints[5];
+                        rec[5] = ints[6];
+                        rec[6] = nbk - 1;
+                        P.ev_delta[c] = delta;
+                    }
+                }
+                __syncthreads();
+            }
+            // reload (possibly corrected) values
+#pragma unroll
+            for (int t = 0; t < TM; ++t)
+                if (r * TM + t < mi) acc[t] = tile[(r * TM + t) * ts + jl];
+        }
+
+        if (P.out_mat) {
+            T *out = static_cast<T *>(P.out_mat);
+            for (int e = tid; e < mi * nj; e += nth) {
+                int i = e / nj, j = e % nj;
+                out[(i0 + i) * P.k + j0 + j] = tile[i * ts + j];
+            }
+        } else if (live_col) {
+            const T ynj = yn[j0 + jl];
+            const int32_t gj = int32_t(j0 + jl);
+#pragma unroll
+            for (int t = 0; t < TM; ++t) {
+                T dd = sub_rn(ynj, add_rn(acc[t], acc[t]));
+                argmin_merge(bestv[t], bestj[t], dd, gj);
+            }
+        }
+    }
+
+    if (P.out_mat) return;
+    // cross-thread reduction of the per-thread running minima over the pb
+    // threads that share each row (order-independent: a min over a total order)
+    const int seg = pb < 32 ? pb : 32;
+#pragma unroll
+    for (int t = 0; t < TM; ++t) {
+        for (int off = seg / 2; off; off >>= 1) {
+            T ov = __shfl_xor_sync(0xffffffffu, bestv[t], off);
+            int32_t oj = __shfl_xor_sync(0xffffffffu, bestj[t], off);
+            argmin_merge(bestv[t], bestj[t], ov, oj);
+        }
+    }
+    const int nw = (pb + 31) / 32;
+    T *rv = reinterpret_cast<T *>(smem + L.red);
+    int32_t *rj = reinterpret_cast<int32_t *>(rv + bm * nw);
+    __syncthreads();
+    if (jl % seg == 0 && real_row_group) {
+        const int w = jl / 32;
+#pragma unroll
+        for (int t = 0; t < TM; ++t) {
+            rv[(r * TM + t) * nw + w] = bestv[t];
+            rj[(r * TM + t) * nw + w] = bestj[t];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < mi; i += nth) {
+        T bv = T(INFINITY);
+        int32_t bj = 0;
+        for (int w = 0; w < nw; ++w) argmin_merge(bv, bj, rv[i * nw + w], rj[i * nw + w]);
+        P.out_idx[i0 + i] = bj;
+        static_cast<T *>(P.out_val)[i0 + i] = bv;
+    }
+}
+
+// bmax[bj] = max |y| over the rows of logical column block bj (_block_absmax)
+template <typename T>
+__global__ void block_absmax_kernel(const T *y, int64_t k, int64_t d, int64_t bn, double *bmax) {
+    int64_t bj = blockIdx.x;
+    int64_t j0 = bj * bn;
+    int64_t nj = bn < k - j0 ? bn : k - j0;
+    double m = 0.0;
+    for (int64_t e = threadIdx.x; e < nj * d; e += blockDim.x) {
+        double v = fabs(double(y[j0 * d + e]));
+        m = v > m ? v : m;
+    }
+    __shared__ double sh[32];
+    for (int off = 16; off; off >>= 1) {
+        double o = __shfl_xor_sync(0xffffffffu, m, off);
+        m = o > m ? o : m;
+    }
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) mm = sh[w] > mm ? sh[w] : mm;
+        bmax[bj] = mm;
+    }
+}
+
+// _row_sq_norms: s = x0*x0; s += xj*xj, left to right in dtype
+template <typename T>
+__global__ void row_sq_norms_kernel(const T *x, int64_t m, int64_t n, T *out) {
+    int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    const T *row = x + i * n;
+    T s = mul_rn(row[0], row[0]);
+    for (int64_t j = 1; j < n; ++j) s = add_rn(s, mul_rn(row[j], row[j]));
+    out[i] = s;
+}
+
+// ------------------------------------------------------------ launch --
+template <typename T, int TM, bool CHECKED>
+static int launch_tm(const ExactParams &P, int threads, size_t smem, cudaStream_t st) {
+    auto kern = exact_tile_kernel<T, TM, CHECKED>;
+    if (smem > 48 * 1024)
+        FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(smem)));
+    int64_t nbi = (P.m + P.bm - 1) / P.bm;
+    kern<<<dim3(unsigned(nbi)), dim3(threads), smem, st>>>(P);
+    FTK_LAUNCHED("exact_tile_kernel");
+    return FTK_OK;
+}
+
+template <typename T, bool CHECKED>
+static int launch_exact(ExactParams P, cudaStream_t st) {
+    const bool f64 = sizeof(T) == 8;
+    const int tm_cap = f64 ? 32 : 64;
+    int tm = int(P.bm < (f64 ? 16 : 32) ? P.bm : (f64 ? 16 : 32));
+    auto nthreads = [&](int t) { return int((P.pb * (P.bm / t) + 31) / 32 * 32); };
+    while (nthreads(tm) < 128 && tm > 4) tm /= 2;
+    while (nthreads(tm) > exact_max_threads(tm) && tm < tm_cap && tm < P.bm) tm *= 2;
+    int threads = nthreads(tm);  // whole warps; padding threads own no rows
+    if (threads > exact_max_threads(tm)) {
+        set_error("tile too large for the exact kernel (bn * bm / 64 > 1024)");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    SmemLayout L = smem_layout<T>(P.bm, P.pb, P.bk, CHECKED, P.out_mat != nullptr);
+    if (L.total > 227 * 1024) {
+        set_error("tile too large for shared memory in the exact kernel");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    switch (tm) {
+        case 1: return launch_tm<T, 1, CHECKED>(P, threads, L.total, st);
+        case 2: return launch_tm<T, 2, CHECKED>(P, threads, L.total, st);
+        case 4: return launch_tm<T, 4, CHECKED>(P, threads, L.total, st);
+        case 8: return launch_tm<T, 8, CHECKED>(P, threads, L.total, st);
+        case 16: return launch_tm<T, 16, CHECKED>(P, threads, L.total, st);
+        case 32: return launch_tm<T, 32, CHECKED>(P, threads, L.total, st);
+        case 64: return launch_tm<T, 64, CHECKED>(P, threads, L.total, st);
+    }
+    set_error("bad tile geometry");
+    return FTK_ERR_ARG;
+}
+
+int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn, int64_t m,
+              int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk, int32_t *out_idx,
+              void *out_val, void *out_mat, bool checked, double delta_rel, double abs_tol,
+              int64_t iteration, const ftk_injection *inj, ftk_events *ev, cudaStream_t st) {
+    if (m <= 0) return FTK_OK;
+    if (bm < 1 || bn < 1 || bk < 1 || d < 1) {
+        set_error("bad tile/shape");
+        return FTK_ERR_ARG;
+    }
+    ExactParams P{};
+    P.x = x; P.y = y; P.yn = yn;
+    P.m = m; P.k = k; P.d = d; P.bm = bm; P.bn = bn; P.bk = bk;
+    int64_t live = bn < k ? bn : k;
+    if (live < 1) live = 1;
+    int64_t pb = 1;
+    while (pb < live) pb *= 2;
+    P.pb = int(pb);
+    P.out_idx = out_idx; P.out_val = out_val; P.out_mat = out_mat;
+    P.delta_rel = delta_rel; P.abs_tol = abs_tol; P.iteration = iteration;
+    if (inj && inj->n > 0) {
+        P.n_inj = inj->n;
+        P.ibi = inj->bi; P.ibj = inj->bj; P.iei = inj->ei; P.iej = inj->ej; P.ibit = inj->bit;
+        P.iapplied = inj->applied; P.ibefore = inj->before; P.iafter = inj->after;
+    }
+    if (checked) {
+        if (!ev) {
+            set_error("checked mode needs an event ring");
+            return FTK_ERR_ARG;
+        }
+        P.ev_cap = ev->cap; P.ev_rec = ev->rec; P.ev_delta = ev->delta;
+        P.ev_count = reinterpret_cast<unsigned long long *>(ev->count);
+        int64_t nbj = (k + bn - 1) / bn;
+        double *bmax = static_cast<double *>(scratch(ctx, SLOT_BMAX, sizeof(double) * (nbj + 1), st));
+        if (!bmax) return FTK_ERR_CUDA;
+        if (nbj > 0) {
+            if (dtype == FTK_F32)
+                block_absmax_kernel<float><<<unsigned(nbj), 256, 0, st>>>(
+                    static_cast<const float *>(y), k, d, bn, bmax);
+            else
+                block_absmax_kernel<double><<<unsigned(nbj), 256, 0, st>>>(
+                    static_cast<const double *>(y), k, d, bn, bmax);
+            FTK_LAUNCHED("block_absmax_kernel");
+        }
+        P.bmax = bmax;
+    }
+    if (dtype == FTK_F32)
+        return checked ? launch_exact<float, true>(P, st) : launch_exact<float, false>(P, st);
+    return checked ? launch_exact<double, true>(P, st) : launch_exact<double, false>(P, st);
+}
+
+int row_sq_norms_run(int dtype, const void *x, int64_t m, int64_t n, void *out, cudaStream_t st) {
+    if (m <= 0) return FTK_OK;
+    unsigned grid = unsigned((m + 255) / 256);
+    if (dtype == FTK_F32)
+        row_sq_norms_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float *>(x), m, n,
+                                                         static_cast<float *>(out));
+    else
+        row_sq_norms_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double *>(x), m, n,
+                                                          static_cast<double *>(out));
+    FTK_LAUNCHED("row_sq_norms_kernel");
+    return FTK_OK;
+}
+
+}  // namespace ftk

@@ -1,0 +1,687 @@
+// update.cu -- centroid update, inertia and convergence kernels (sm_100a).
+//
+// The reference accumulates per-cluster sums with numpy.bincount: float64,
+// ascending sample order, one pass per feature (kmeans.py:167-171).  Floating
+// point addition is not associative, so to reproduce those bits the update
+// walks each cluster's members in ascending sample index: a stable radix sort
+// of the labels gives every cluster its member list, then one warp per
+// (cluster, 32-feature group) runs the float64 chains with coalesced row
+// loads.  The chain for DMR mode carries two independent accumulators over
+// the same loaded values (the reference's duplicated accumulation,
+// kmeans.py:176-189); the compare is bitwise.
+//
+// Inertia uses numpy's pairwise summation tree (kmeans.py:275, 307) and the
+// movement test np.linalg.norm's per-row pairwise reduce (kmeans.py:289-293),
+// both evaluated on the device with the same association.
+//
+// Compiled with --fmad=false.
+
+#include <cub/cub.cuh>
+
+#include <functional>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ftk {
+
+// --------------------------------------------------------------- counts --
+__global__ void histogram_kernel(const int32_t *labels, int64_t m, int64_t k,
+                                 unsigned long long *counts) {
+    extern __shared__ unsigned int hist[];
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x) hist[c] = 0;
+    __syncthreads();
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&hist[labels[i]], 1u);
+    __syncthreads();
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x)
+        if (hist[c]) atomicAdd(&counts[c], (unsigned long long)hist[c]);
+}
+
+__global__ void histogram_global_kernel(const int32_t *labels, int64_t m,
+                                        unsigned long long *counts) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&counts[labels[i]], 1ull);
+}
+
+// Independent second count (DMR): segment boundaries of the sorted labels.
+__global__ void boundary_count_kernel(const int32_t *sorted, int64_t m, int64_t k,
+                                      unsigned long long *counts) {
+    // counts must be zeroed; segment end adds end, segment start subtracts
+    // start (two's complement wrap makes the unsigned atomics exact).
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int32_t c = sorted[i];
+        if (i == m - 1 || sorted[i + 1] != c) atomicAdd(&counts[c], (unsigned long long)(i + 1));
+        if (i == 0 || sorted[i - 1] != c) atomicAdd(&counts[c], (unsigned long long)(-i));
+    }
+}
+
+__global__ void exclusive_scan_small_kernel(const int64_t *counts, int64_t k, int64_t *offsets) {
+    // single block; k up to a few hundred thousand is fine
+    __shared__ int64_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < k; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int64_t v = i < k ? counts[i] : 0;
+        // block inclusive scan via warp shuffles + smem
+        __shared__ int64_t warp_tot[32];
+        int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        int64_t s = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            int64_t o = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += o;
+        }
+        if (lane == 31) warp_tot[w] = s;
+        __syncthreads();
+        if (w == 0) {
+            int64_t t = lane < int(blockDim.x / 32) ? warp_tot[lane] : 0;
+            for (int off = 1; off < 32; off <<= 1) {
+                int64_t o = __shfl_up_sync(0xffffffffu, t, off);
+                if (lane >= off) t += o;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        int64_t incl = s + (w ? warp_tot[w - 1] : 0);
+        if (i < k) offsets[i] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) offsets[k] = carry;
+}
+
+__global__ void iota_kernel(int32_t *v, int64_t m) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        v[i] = int32_t(i);
+}
+
+// ----------------------------------------------------- ordered chains --
+// One warp per (cluster, 32-feature group).  Lane f accumulates feature
+// g*32+f over the cluster's members in ascending sample order.
+template <typename T, bool DMR>
+__global__ void __launch_bounds__(256) chain_sums_kernel(const T *x, int64_t d,
+                                                         const int32_t *perm,
+                                                         const int64_t *offsets, int64_t k,
+                                                         double *sums_a, double *sums_b) {
+    const int warps_per_block = blockDim.x / 32;
+    const int64_t ngroups = (d + 31) / 32;
+    const int64_t wid = int64_t(blockIdx.x) * warps_per_block + (threadIdx.x >> 5);
+    if (wid >= k * ngroups) return;
+    const int64_t c = wid / ngroups;
+    const int64_t f = (wid % ngroups) * 32 + (threadIdx.x & 31);
+    const int lane = threadIdx.x & 31;
+    const bool live = f < d;
+    const int64_t lo = offsets[c], hi = offsets[c + 1];
+    double acc_a = 0.0, acc_b = 0.0;
+    constexpr int U = 8;
+    for (int64_t base = lo; base < hi; base += 32) {
+        const int nb = int(hi - base < 32 ? hi - base : 32);
+        const int32_t my_row = lane < nb ? perm[base + lane] : 0;
+        int t = 0;
+        for (; t + U <= nb; t += U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                int32_t row = __shfl_sync(0xffffffffu, my_row, t + u);
+                v[u] = live ? double(x[int64_t(row) * d + f]) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                acc_a = __dadd_rn(acc_a, v[u]);
+                if (DMR) acc_b = __dadd_rn(acc_b, v[u]);
+            }
+        }
+        for (; t < nb; ++t) {
+            int32_t row = __shfl_sync(0xffffffffu, my_row, t);
+            double v = live ? double(x[int64_t(row) * d + f]) : 0.0;
+            acc_a = __dadd_rn(acc_a, v);
+            if (DMR) acc_b = __dadd_rn(acc_b, v);
+        }
+    }
+    if (live) {
+        sums_a[c * d + f] = acc_a;
+        if (DMR) sums_b[c * d + f] = acc_b;
+    }
+}
+
+__global__ void u64_to_i64_kernel(const unsigned long long *a, int64_t *b, int64_t n) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        b[i] = int64_t(a[i]);
+}
+
+// ----------------------------------------------------------- finalize --
+template <typename T>
+__global__ void finalize_kernel(const double *sums, const int64_t *counts, int64_t k, int64_t d,
+                                T *cent, int32_t *n_empty) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < k * d;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        int64_t c = e / d;
+        int64_t n = counts[c];
+        double v = n > 0 ? __ddiv_rn(sums[e], double(n)) : 0.0;
+        cent[e] = T(v);
+        if (n <= 0 && e % d == 0 && n_empty) atomicAdd(n_empty, 1);
+    }
+}
+
+__global__ void dmr_compare_kernel(const unsigned long long *a, const unsigned long long *b,
+                                   int64_t n, int32_t *flag) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (a[i] != b[i]) atomicExch(flag, 1);
+}
+
+// ------------------------------------------------------ reseed empties --
+// argmax with numpy semantics (first maximum; NaN counts as the maximum).
+struct ArgMax {
+    double v;
+    int64_t i;
+};
+__device__ __forceinline__ bool am_better(double v, int64_t i, double bv, int64_t bi) {
+    bool vn = isnan(v), bn = isnan(bv);
+    if (vn != bn) return vn;  // NaN wins over non-NaN
+    if (vn && bn) return i < bi;
+    return v > bv || (v == bv && i < bi);
+}
+
+__global__ void argmax_partial_kernel(const double *a, int64_t n, ArgMax *part) {
+    double bv = -INFINITY;
+    int64_t bi = INT64_MAX;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        if (am_better(a[i], i, bv, bi)) { bv = a[i]; bi = i; }
+    }
+    for (int off = 16; off; off >>= 1) {
+        double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+        int64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (am_better(ov, oi, bv, bi)) { bv = ov; bi = oi; }
+    }
+    __shared__ ArgMax sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = {bv, bi};
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ArgMax r = sh[0];
+        for (int w = 1; w < int(blockDim.x / 32); ++w)
+            if (am_better(sh[w].v, sh[w].i, r.v, r.i)) r = sh[w];
+        part[blockIdx.x] = r;
+    }
+}
+
+template <typename T>
+__global__ void reseed_apply_kernel(const ArgMax *part, int nparts, const T *x, int64_t d,
+                                    int64_t j, double *sq, T *cent) {
+    __shared__ int64_t far;
+    if (threadIdx.x == 0) {
+        ArgMax r = part[0];
+        for (int p = 1; p < nparts; ++p)
+            if (am_better(part[p].v, part[p].i, r.v, r.i)) r = part[p];
+        far = r.i == INT64_MAX ? 0 : r.i;
+    }
+    __syncthreads();
+    for (int64_t f = threadIdx.x; f < d; f += blockDim.x) cent[j * d + f] = x[far * d + f];
+    __syncthreads();
+    if (threadIdx.x == 0) sq[far] = -INFINITY;
+}
+
+// ------------------------------------------------------------ inertia --
+template <typename T>
+__global__ void sq_dists_kernel(const T *md, const double *xsq, int64_t m, double *sq) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        sq[i] = __dadd_rn(double(md[i]), xsq[i]);
+}
+
+// numpy pairwise_sum leaf (n <= 128): 8 strided accumulators.
+__device__ double pairwise_leaf(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r = __dadd_rn(r, a[i]);
+        return r;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i;
+    for (i = 8; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+// Full recursion with an explicit stack (per-thread; used for rows of <= a
+// few thousand elements).  Post-order evaluation keeps numpy's association.
+__device__ double pairwise_sum_dev(const double *a, int64_t n) {
+    if (n <= 128) return pairwise_leaf(a, n);
+    struct Fr { int64_t off, n; int state; double left; };
+    Fr st[48];
+    int sp = 0;
+    st[0] = {0, n, 0, 0.0};
+    double ret = 0.0;
+    while (sp >= 0) {
+        Fr &f = st[sp];
+        if (f.n <= 128) {
+            ret = pairwise_leaf(a + f.off, f.n);
+            --sp;
+            continue;
+        }
+        int64_t n2 = f.n / 2;
+        n2 -= n2 % 8;
+        if (f.state == 0) {
+            f.state = 1;
+            st[sp + 1] = {f.off, n2, 0, 0.0};
+            ++sp;
+        } else if (f.state == 1) {
+            f.left = ret;
+            f.state = 2;
+            st[sp + 1] = {f.off + n2, f.n - n2, 0, 0.0};
+            ++sp;
+        } else {
+            ret = __dadd_rn(f.left, ret);
+            --sp;
+        }
+    }
+    return ret;
+}
+
+// Leaf sums: 8 lanes per leaf (one per accumulator), 4 leaves per warp.
+__global__ void pairwise_leaves_kernel(const double *a, const int64_t *leaf_start, int64_t nleaves,
+                                       double *vals) {
+    const int64_t gl = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 8;
+    const int j = threadIdx.x & 7;
+    const bool live = gl < nleaves;
+    int64_t off = 0, n = 0;
+    if (live) {
+        off = leaf_start[gl];
+        n = leaf_start[gl + 1] - off;
+    }
+    const double *p = a + off;
+    double r = 0.0;
+    const bool small = n < 8;
+    int64_t lim = n - (n % 8);
+    if (live && !small) {
+        r = p[j];
+        for (int64_t i = 8; i < lim; i += 8) r = __dadd_rn(r, p[i + j]);
+    }
+    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) within the 8-lane group
+    const unsigned mask = 0xffffffffu;
+    double o1 = __shfl_xor_sync(mask, r, 1);
+    double s1 = (j & 1) ? __dadd_rn(o1, r) : __dadd_rn(r, o1);  // pair sums (even lane has r_even+r_odd)
+    double o2 = __shfl_xor_sync(mask, s1, 2);
+    double s2 = (j & 2) ? __dadd_rn(o2, s1) : __dadd_rn(s1, o2);
+    double o4 = __shfl_xor_sync(mask, s2, 4);
+    double s4 = (j & 4) ? __dadd_rn(o4, s2) : __dadd_rn(s2, o4);
+    if (live && j == 0) {
+        double res;
+        if (small) {
+            res = 0.0;
+            for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, p[i]);
+        } else {
+            res = s4;
+            for (int64_t i = lim; i < n; ++i) res = __dadd_rn(res, p[i]);
+        }
+        vals[gl] = res;
+    }
+}
+
+// Internal nodes, level by level (height order), single block.
+__global__ void pairwise_tree_kernel(double *vals, const int2 *nodes, const int64_t *level_start,
+                                     int nlevels, int64_t nleaves, double *out) {
+    for (int L = 0; L < nlevels; ++L) {
+        for (int64_t q = level_start[L] + threadIdx.x; q < level_start[L + 1]; q += blockDim.x) {
+            int2 ch = nodes[q];
+            vals[nleaves + q] = __dadd_rn(vals[ch.x], vals[ch.y]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        int64_t total = level_start[nlevels];
+        *out = total > 0 ? vals[nleaves + total - 1] : vals[0];
+    }
+}
+
+// ---------------------------------------------------------- movement --
+template <typename T>
+__global__ void movement_kernel(const T *nc, const T *oc, int64_t k, int64_t d, double eps,
+                                double *tmp, unsigned long long *moved_bits) {
+    int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    double *a = tmp + j * 2 * d;
+    double *b = a + d;
+    for (int64_t f = 0; f < d; ++f) {
+        double o = double(oc[j * d + f]);
+        double diff = __dsub_rn(double(nc[j * d + f]), o);
+        a[f] = __dmul_rn(diff, diff);
+        b[f] = __dmul_rn(o, o);
+    }
+    double num = sqrt(pairwise_sum_dev(a, d));
+    double den = __dadd_rn(sqrt(pairwise_sum_dev(b, d)), eps);
+    double r = __ddiv_rn(num, den);
+    unsigned long long bits = isnan(r) ? 0x7ff8000000000000ull : __double_as_longlong(r);
+    atomicMax(moved_bits, bits);  // non-negative doubles order like their bits
+}
+
+// sq[i] = pairwise_sum_f((x[i,f] - cent64[label[i], f])^2)  (kmeans.py:199-201)
+template <typename T>
+__global__ void own_sq_dists_kernel(const T *x, const int32_t *lab, const double *c64, int64_t m,
+                                    int64_t d, double *tmp, double *out) {
+    const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    double *a = tmp + tid * d;
+    for (int64_t i = tid; i < m; i += int64_t(gridDim.x) * blockDim.x) {
+        const double *c = c64 + int64_t(lab[i]) * d;
+        for (int64_t f = 0; f < d; ++f) {
+            double diff = __dsub_rn(double(x[i * d + f]), c[f]);
+            a[f] = __dmul_rn(diff, diff);
+        }
+        out[i] = pairwise_sum_dev(a, d);
+    }
+}
+
+__global__ void labels_equal_kernel(const int32_t *a, const int32_t *b, int64_t m, int32_t *flag) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += int64_t(gridDim.x) * blockDim.x)
+        if (a[i] != b[i]) atomicExch(flag, 0);
+}
+
+__global__ void flip_f64_kernel(double *a, int64_t idx, int64_t bit, double *ba) {
+    double before = a[idx];
+    double after = flip_bit(before, bit);
+    a[idx] = after;
+    if (ba) { ba[0] = before; ba[1] = after; }
+}
+
+__global__ void set_i32_kernel(int32_t *p, int32_t v) { *p = v; }
+
+// =================================================================== host ==
+static unsigned grid_for(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return unsigned(g);
+}
+
+int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *labels, int64_t m,
+                    int64_t d, int64_t k, double *sums_a, int64_t *counts_a, double *sums_b,
+                    int64_t *counts_b, cudaStream_t st) {
+    if (k <= 0) return FTK_OK;
+    // counts (privatised histogram when k fits in shared memory)
+    FTK_CUDA(cudaMemsetAsync(counts_a, 0, sizeof(int64_t) * k, st));
+    if (m > 0) {
+        if (k <= 12 * 1024) {
+            histogram_kernel<<<grid_for(m, 512), 512, sizeof(unsigned) * k, st>>>(
+                labels, m, k, reinterpret_cast<unsigned long long *>(counts_a));
+        } else {
+            histogram_global_kernel<<<grid_for(m, 512), 512, 0, st>>>(
+                labels, m, reinterpret_cast<unsigned long long *>(counts_a));
+        }
+        FTK_LAUNCHED("histogram_kernel");
+    }
+    // stable sort of (label, index) -> member lists in ascending sample order
+    int bits = 1;
+    while ((int64_t(1) << bits) < k) ++bits;
+    int32_t *keys_out = static_cast<int32_t *>(scratch(ctx, SLOT_SORT_KEYS, sizeof(int32_t) * (m + 1) * 2, st));
+    int32_t *vals = static_cast<int32_t *>(scratch(ctx, SLOT_SORT_VALS, sizeof(int32_t) * (m + 1) * 2, st));
+    int64_t *offsets = static_cast<int64_t *>(scratch(ctx, SLOT_OFFSETS, sizeof(int64_t) * (k + 1), st));
+    if (!keys_out || !vals || !offsets) return FTK_ERR_CUDA;
+    int32_t *vals_in = vals, *vals_out = vals + (m + 1);
+    if (m > 0) {
+        iota_kernel<<<grid_for(m, 256), 256, 0, st>>>(vals_in, m);
+        FTK_LAUNCHED("iota_kernel");
+        size_t tmp_bytes = 0;
+        FTK_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, labels, keys_out, vals_in,
+                                                 vals_out, int(m), 0, bits, st));
+        void *tmp = scratch(ctx, SLOT_SORT_TMP, tmp_bytes, st);
+        if (!tmp) return FTK_ERR_CUDA;
+        FTK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, labels, keys_out, vals_in,
+                                                 vals_out, int(m), 0, bits, st));
+        count_launch((bits + 7) / 8 * 3);
+    }
+    exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets);
+    FTK_LAUNCHED("exclusive_scan_small_kernel");
+    if (counts_b) {
+        FTK_CUDA(cudaMemsetAsync(counts_b, 0, sizeof(int64_t) * k, st));
+        if (m > 0) {
+            boundary_count_kernel<<<grid_for(m, 256), 256, 0, st>>>(keys_out, m, k, reinterpret_cast<unsigned long long *>(counts_b));
+            FTK_LAUNCHED("boundary_count_kernel");
+        }
+    }
+    const int64_t warps = k * ((d + 31) / 32);
+    const int block = 256;
+    const unsigned grid = unsigned((warps * 32 + block - 1) / block);
+    const bool dmr = sums_b != nullptr;
+    if (dtype == FTK_F32) {
+        auto xx = static_cast<const float *>(x);
+        if (dmr) chain_sums_kernel<float, true><<<grid, block, 0, st>>>(xx, d, vals_out, offsets, k, sums_a, sums_b);
+        else chain_sums_kernel<float, false><<<grid, block, 0, st>>>(xx, d, vals_out, offsets, k, sums_a, nullptr);
+    } else {
+        auto xx = static_cast<const double *>(x);
+        if (dmr) chain_sums_kernel<double, true><<<grid, block, 0, st>>>(xx, d, vals_out, offsets, k, sums_a, sums_b);
+        else chain_sums_kernel<double, false><<<grid, block, 0, st>>>(xx, d, vals_out, offsets, k, sums_a, nullptr);
+    }
+    FTK_LAUNCHED("chain_sums_kernel");
+    return FTK_OK;
+}
+
+int dmr_compare_run(const double *sa, const int64_t *ca, const double *sb, const int64_t *cb,
+                    int64_t k, int64_t d, int32_t *flag, cudaStream_t st) {
+    set_i32_kernel<<<1, 1, 0, st>>>(flag, 0);
+    FTK_LAUNCHED("set_i32_kernel");
+    dmr_compare_kernel<<<grid_for(k * d, 256), 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long *>(sa),
+        reinterpret_cast<const unsigned long long *>(sb), k * d, flag);
+    FTK_LAUNCHED("dmr_compare_kernel");
+    dmr_compare_kernel<<<grid_for(k, 256), 256, 0, st>>>(
+        reinterpret_cast<const unsigned long long *>(ca),
+        reinterpret_cast<const unsigned long long *>(cb), k, flag);
+    FTK_LAUNCHED("dmr_compare_kernel");
+    return FTK_OK;
+}
+
+int finalize_run(int dtype, const double *sums, const int64_t *counts, int64_t k, int64_t d,
+                 void *cent, int32_t *n_empty, cudaStream_t st) {
+    if (n_empty) {
+        set_i32_kernel<<<1, 1, 0, st>>>(n_empty, 0);
+        FTK_LAUNCHED("set_i32_kernel");
+    }
+    if (dtype == FTK_F32)
+        finalize_kernel<float><<<grid_for(k * d, 256), 256, 0, st>>>(sums, counts, k, d, static_cast<float *>(cent), n_empty);
+    else
+        finalize_kernel<double><<<grid_for(k * d, 256), 256, 0, st>>>(sums, counts, k, d, static_cast<double *>(cent), n_empty);
+    FTK_LAUNCHED("finalize_kernel");
+    return FTK_OK;
+}
+
+int reseed_run(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d,
+               const int64_t *counts, int64_t k, double *sq, void *cent, cudaStream_t st) {
+    std::vector<int64_t> hc(k);
+    FTK_CUDA(cudaMemcpyAsync(hc.data(), counts, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, st));
+    FTK_CUDA(cudaStreamSynchronize(st));
+    const int nparts = 256;
+    ArgMax *part = static_cast<ArgMax *>(scratch(ctx, SLOT_MISC, sizeof(ArgMax) * nparts, st));
+    if (!part) return FTK_ERR_CUDA;
+    for (int64_t j = 0; j < k; ++j) {
+        if (hc[j] > 0) continue;
+        argmax_partial_kernel<<<nparts, 256, 0, st>>>(sq, m, part);
+        FTK_LAUNCHED("argmax_partial_kernel");
+        if (dtype == FTK_F32)
+            reseed_apply_kernel<float><<<1, 256, 0, st>>>(part, nparts, static_cast<const float *>(x), d, j, sq, static_cast<float *>(cent));
+        else
+            reseed_apply_kernel<double><<<1, 256, 0, st>>>(part, nparts, static_cast<const double *>(x), d, j, sq, static_cast<double *>(cent));
+        FTK_LAUNCHED("reseed_apply_kernel");
+    }
+    return FTK_OK;
+}
+
+int sq_dists_run(int dtype, const void *md, const double *xsq, int64_t m, double *sq,
+                 cudaStream_t st) {
+    if (m <= 0) return FTK_OK;
+    if (dtype == FTK_F32)
+        sq_dists_kernel<float><<<grid_for(m, 256), 256, 0, st>>>(static_cast<const float *>(md), xsq, m, sq);
+    else
+        sq_dists_kernel<double><<<grid_for(m, 256), 256, 0, st>>>(static_cast<const double *>(md), xsq, m, sq);
+    FTK_LAUNCHED("sq_dists_kernel");
+    return FTK_OK;
+}
+
+// Host-built numpy pairwise tree for length n (cached per context+n).
+struct PairwiseTree {
+    int64_t n = -1, nleaves = 0, nnodes = 0;
+    int nlevels = 0;
+    int64_t *d_leaf_start = nullptr;
+    int2 *d_nodes = nullptr;
+    int64_t *d_level_start = nullptr;
+};
+
+static std::mutex g_tree_mu;
+static std::map<std::pair<ftk_ctx *, int64_t>, PairwiseTree> g_trees;
+
+static int build_tree(int64_t n, std::vector<int64_t> &leaf_start, std::vector<int2> &nodes,
+                      std::vector<int64_t> &level_start) {
+    // returns the number of levels; node ids: leaves 0..L-1, internal L+q
+    struct Item { int64_t off, n; };
+    std::vector<int64_t> starts;
+    std::vector<std::pair<int, int>> height_node;  // (height, q) for sorting
+    std::vector<int2> raw;
+    std::vector<int> heights;
+    // recursive lambda returning (id, height)
+    std::function<std::pair<int, int>(int64_t, int64_t)> rec = [&](int64_t off, int64_t len) -> std::pair<int, int> {
+        if (len <= 128) {
+            starts.push_back(off);
+            return {int(starts.size() - 1), 0};
+        }
+        int64_t n2 = len / 2;
+        n2 -= n2 % 8;
+        auto L = rec(off, n2);
+        auto R = rec(off + n2, len - n2);
+        raw.push_back(int2{L.first, R.first});  // ids fixed up below (leaf vs internal)
+        int h = 1 + (L.second > R.second ? L.second : R.second);
+        heights.push_back(h);
+        return {-int(raw.size()), h};  // negative: internal node index (1-based)
+    };
+    auto root = rec(0, n);
+    (void)root;
+    int64_t L = int64_t(starts.size());
+    leaf_start = starts;
+    leaf_start.push_back(n);
+    // convert ids: leaf id stays; internal -q -> L + (q-1)
+    for (auto &c : raw) {
+        if (c.x < 0) c.x = int(L + (-c.x - 1));
+        if (c.y < 0) c.y = int(L + (-c.y - 1));
+    }
+    // order internal nodes by height, keeping creation order within a height
+    int maxh = 0;
+    for (int h : heights) maxh = h > maxh ? h : maxh;
+    std::vector<int> new_index(raw.size());
+    level_start.assign(maxh + 1, 0);
+    std::vector<int> order;
+    for (int h = 1; h <= maxh; ++h) {
+        level_start[h - 1] = int64_t(order.size());
+        for (size_t q = 0; q < raw.size(); ++q)
+            if (heights[q] == h) order.push_back(int(q));
+    }
+    level_start[maxh] = int64_t(order.size());
+    for (size_t p = 0; p < order.size(); ++p) new_index[order[p]] = int(p);
+    nodes.resize(raw.size());
+    for (size_t p = 0; p < order.size(); ++p) {
+        int2 c = raw[order[p]];
+        if (c.x >= L) c.x = int(L + new_index[c.x - L]);
+        if (c.y >= L) c.y = int(L + new_index[c.y - L]);
+        nodes[p] = c;
+    }
+    return maxh;
+}
+
+int pairwise_sum_run(ftk_ctx *ctx, const double *a, int64_t n, double *out, cudaStream_t st) {
+    if (n <= 0) {
+        FTK_CUDA(cudaMemsetAsync(out, 0, sizeof(double), st));
+        return FTK_OK;
+    }
+    PairwiseTree *T;
+    {
+        std::lock_guard<std::mutex> lk(g_tree_mu);
+        T = &g_trees[{ctx, n}];
+        if (T->n != n) {
+            std::vector<int64_t> ls, lev;
+            std::vector<int2> nodes;
+            int nl = build_tree(n, ls, nodes, lev);
+            T->n = n;
+            T->nleaves = int64_t(ls.size()) - 1;
+            T->nnodes = int64_t(nodes.size());
+            T->nlevels = nl;
+            FTK_CUDA(cudaMalloc(&T->d_leaf_start, sizeof(int64_t) * ls.size()));
+            FTK_CUDA(cudaMalloc(&T->d_nodes, sizeof(int2) * (nodes.size() + 1)));
+            FTK_CUDA(cudaMalloc(&T->d_level_start, sizeof(int64_t) * (lev.size() + 1)));
+            FTK_CUDA(cudaMemcpy(T->d_leaf_start, ls.data(), sizeof(int64_t) * ls.size(), cudaMemcpyHostToDevice));
+            if (!nodes.empty())
+                FTK_CUDA(cudaMemcpy(T->d_nodes, nodes.data(), sizeof(int2) * nodes.size(), cudaMemcpyHostToDevice));
+            FTK_CUDA(cudaMemcpy(T->d_level_start, lev.data(), sizeof(int64_t) * lev.size(), cudaMemcpyHostToDevice));
+        }
+    }
+    double *vals = static_cast<double *>(scratch(ctx, SLOT_PAIRWISE, sizeof(double) * (T->nleaves + T->nnodes + 1), st));
+    if (!vals) return FTK_ERR_CUDA;
+    int64_t threads = T->nleaves * 8;
+    pairwise_leaves_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(a, T->d_leaf_start, T->nleaves, vals);
+    FTK_LAUNCHED("pairwise_leaves_kernel");
+    pairwise_tree_kernel<<<1, 1024, 0, st>>>(vals, T->d_nodes, T->d_level_start, T->nlevels, T->nleaves, out);
+    FTK_LAUNCHED("pairwise_tree_kernel");
+    return FTK_OK;
+}
+
+int movement_run(ftk_ctx *ctx, int dtype, const void *nc, const void *oc, int64_t k, int64_t d,
+                 double eps, double *moved, cudaStream_t st) {
+    double *tmp = static_cast<double *>(scratch(ctx, SLOT_MISC, sizeof(double) * 2 * k * d + 64, st));
+    if (!tmp) return FTK_ERR_CUDA;
+    FTK_CUDA(cudaMemsetAsync(moved, 0, sizeof(double), st));
+    auto mb = reinterpret_cast<unsigned long long *>(moved);
+    unsigned grid = unsigned((k + 127) / 128);
+    if (dtype == FTK_F32)
+        movement_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float *>(nc), static_cast<const float *>(oc), k, d, eps, tmp, mb);
+    else
+        movement_kernel<double><<<grid, 128, 0, st>>>(static_cast<const double *>(nc), static_cast<const double *>(oc), k, d, eps, tmp, mb);
+    FTK_LAUNCHED("movement_kernel");
+    return FTK_OK;
+}
+
+int own_sq_dists_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *lab,
+                     const double *c64, int64_t m, int64_t d, double *out, cudaStream_t st) {
+    if (m <= 0) return FTK_OK;
+    const int block = 128, grid = 148 * 2;
+    double *tmp = static_cast<double *>(scratch(ctx, SLOT_MISC, sizeof(double) * block * grid * d, st));
+    if (!tmp) return FTK_ERR_CUDA;
+    if (dtype == FTK_F32)
+        own_sq_dists_kernel<float><<<grid, block, 0, st>>>(static_cast<const float *>(x), lab, c64, m, d, tmp, out);
+    else
+        own_sq_dists_kernel<double><<<grid, block, 0, st>>>(static_cast<const double *>(x), lab, c64, m, d, tmp, out);
+    FTK_LAUNCHED("own_sq_dists_kernel");
+    return FTK_OK;
+}
+
+int labels_equal_run(const int32_t *a, const int32_t *b, int64_t m, int32_t *out, cudaStream_t st) {
+    set_i32_kernel<<<1, 1, 0, st>>>(out, 1);
+    FTK_LAUNCHED("set_i32_kernel");
+    if (m > 0) {
+        labels_equal_kernel<<<grid_for(m, 256), 256, 0, st>>>(a, b, m, out);
+        FTK_LAUNCHED("labels_equal_kernel");
+    }
+    return FTK_OK;
+}
+
+int flip_f64_run(double *a, int64_t d, int64_t i, int64_t j, int64_t bit, double *ba,
+                 cudaStream_t st) {
+    flip_f64_kernel<<<1, 1, 0, st>>>(a, i * d + j, bit, ba);
+    FTK_LAUNCHED("flip_f64_kernel");
+    return FTK_OK;
+}
+
+}  // namespace ftk

@@ -1,0 +1,357 @@
+"""Lloyd's iteration on the B200 (reference kmeans.py).
+
+Same entry points, config/result types, stopping rules and fault-campaign
+planning as the reference; the data stays resident in HBM for the whole fit
+and each iteration is: assign (fused or checksum-protected kernel) -> inertia
+(device pairwise sum) -> label comparison -> update (ordered float64 member
+chains, optional DMR) -> finalize -> movement, with ONE small device->host
+control readback per iteration for the host-side stopping decision
+(kmeans.py:277, 295-297).  Results are bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _engine as E
+from .abft import DetectionEvent, DetectionReport, Threshold, checked_assign, events_from_ring
+from .abft import _scheduled_tiles
+from .errors import FaultEscalationError
+from .faults import NOOP_HOOK, FaultSpec, ScheduledFaultHook, plan_faults
+from .gemm import _as_operand, _dtype, _is_torch, fused_assign, get_variant, resolve_threads
+from .matrix import as_matrix
+from .tiles import TileConfig, default_config
+
+FT_MODES = ("off", "abft", "abft+dmr")
+INIT_METHODS = ("random-sample", "kmeanspp")
+
+
+@dataclass
+class KMeansConfig:
+    k: int
+    max_iters: int = 300
+    tol: float = 1e-4
+    seed: int = 0
+    ft_mode: str = "off"
+    init: str = "kmeanspp"
+    tile: object = "auto"
+    threshold: Threshold = None
+    threads: int = None
+    tune_table: object = None
+
+    def validate(self):
+        if self.k < 1:
+            raise ValueError(f"k must be >= 1, got {self.k}")
+        if self.max_iters < 0:
+            raise ValueError(f"max_iters must be >= 0, got {self.max_iters}")
+        if self.tol < 0:
+            raise ValueError(f"tol must be >= 0, got {self.tol}")
+        if self.ft_mode not in FT_MODES:
+            raise ValueError(f"ft_mode must be one of {FT_MODES}, got {self.ft_mode!r}")
+        if self.init not in INIT_METHODS:
+            raise ValueError(f"init must be one of {INIT_METHODS}, got {self.init!r}")
+        return self
+
+
+@dataclass
+class KMeansResult:
+    centroids: np.ndarray
+    assignments: np.ndarray
+    inertia: float
+    iters: int
+    converged: bool
+    report: DetectionReport
+    timings: dict = field(default_factory=dict)
+    inertia_history: list = field(default_factory=list)
+
+
+def init_centroids(x, k, seed=0, method="kmeanspp"):
+    """Deterministic seeding with the reference's Generator draws
+    (kmeans.py:69-103).  Host numpy: random-sample is a gather; kmeanspp's
+    D^2 loop is the reference's own float64 host algorithm."""
+    if _is_torch(x):
+        m = x.shape[0]
+        if k > m:
+            raise ValueError(f"k={k} exceeds the number of samples {m}")
+        if method not in INIT_METHODS:
+            raise ValueError(f"unknown init method {method!r}")
+        if method == "random-sample":
+            idx = np.random.default_rng(seed).choice(m, size=k, replace=False)
+            return E.to_host(x[E._torch().as_tensor(idx, device=x.device)])
+        x = E.to_host(x)
+    x = as_matrix(x)
+    m = x.shape[0]
+    if k > m:
+        raise ValueError(f"k={k} exceeds the number of samples {m}")
+    if method not in INIT_METHODS:
+        raise ValueError(f"unknown init method {method!r}")
+    rng = np.random.default_rng(seed)
+    if method == "random-sample":
+        return np.ascontiguousarray(x[rng.choice(m, size=k, replace=False)])
+    x64 = x.astype(np.float64)
+    cs = np.empty((k, x.shape[1]), dtype=np.float64)
+    cs[0] = x64[int(rng.integers(0, m))]
+    d2 = ((x64 - cs[0]) ** 2).sum(axis=1)
+    for c in range(1, k):
+        total = d2.sum()
+        if total <= 0:
+            pick = int(rng.integers(0, m))
+        else:
+            r = rng.random() * total
+            pick = min(int(np.searchsorted(np.cumsum(d2), r, side="right")), m - 1)
+        cs[c] = x64[pick]
+        d2 = np.minimum(d2, ((x64 - cs[c]) ** 2).sum(axis=1))
+    return np.ascontiguousarray(cs, dtype=x.dtype)
+
+
+def _resolve_tile(tile, x, k, tune_table):
+    if isinstance(tile, TileConfig):
+        return tile.validate()
+    if tile == "auto":
+        if tune_table is not None:
+            return tune_table.lookup((x.shape[0], x.shape[1], k), _dtype(x))
+        return default_config(_dtype(x))
+    raise ValueError(f"tile must be a TileConfig or 'auto', got {tile!r}")
+
+
+def assign_step(x, y, cfg=None, ft_mode="off", hook=NOOP_HOOK, thr=None, iteration=0,
+                threads=None):
+    """ft_mode 'off' -> fused kernel; otherwise the checksum-protected one."""
+    if ft_mode == "off":
+        return fused_assign(x, y, cfg=cfg, threads=threads, hook=hook, iteration=iteration), None
+    return checked_assign(x, y, cfg=cfg, thr=thr, hook=hook, iteration=iteration, threads=threads)
+
+
+def _site_pending(hook, iteration, tile=(0, 0)):
+    if hook is None or hook is NOOP_HOOK:
+        return False
+    probe = getattr(hook, "has_pending_site", None)
+    return probe(iteration, tile) if probe is not None else True
+
+
+def _corrupt_on_host(hook, iteration, sums_t):
+    """Run the hook's maybe_corrupt on a host copy of the device sums (the
+    reference's array fault site, kmeans.py:172-173) and write it back."""
+    host = E.to_host(sums_t).copy()
+    before = host.copy()
+    hook.maybe_corrupt(iteration, (0, 0), host)
+    if host.tobytes() != before.tobytes():
+        sums_t.copy_(E._torch().from_numpy(host).to(sums_t.device))
+
+
+def _update_dev(x_t, labels_i32, k, dtype, ft_mode, hook, iteration, ctl_i32):
+    """Sums/counts (+DMR) -> float64 sums and counts on the device, events."""
+    dmr = ft_mode == "abft+dmr"
+    events = []
+
+    def accumulate():
+        sa, ca, sb, cb = E.update_sums_dev(x_t, labels_i32, k, dmr=dmr)
+        if _site_pending(hook, iteration):
+            _corrupt_on_host(hook, iteration, sa)
+        return sa, ca, sb, cb
+
+    sa, ca, sb, cb = accumulate()
+    if dmr:
+        E.dmr_mismatch_dev(sa, ca, sb, cb, ctl_i32[2:3])
+        if int(ctl_i32[2].item()):
+            events.append(DetectionEvent(iteration=iteration, tile=(0, 0), kind="dmr-mismatch",
+                                         loc=(-1, -1), delta=0.0))
+            sa, ca, sb, cb = accumulate()
+            E.dmr_mismatch_dev(sa, ca, sb, cb, ctl_i32[2:3])
+            if int(ctl_i32[2].item()):
+                raise FaultEscalationError(
+                    f"update-phase DMR mismatch persisted after retry (iteration {iteration})")
+    return sa, ca, events
+
+
+def update_step(x, assignments, k, ft_mode="off", hook=NOOP_HOOK, iteration=0, sq_dists=None):
+    """Per-cluster means, float64 sums in ascending sample order; empty
+    clusters take successive farthest points.  -> (centroids, counts, events)."""
+    t = E._torch()
+    x = _as_operand(x)
+    dtype = _dtype(x)
+    lab = E.to_host(assignments) if _is_torch(assignments) else np.asarray(assignments)
+    m, n = x.shape
+    if lab.shape != (m,):
+        raise ValueError(f"assignments must have shape ({m},)")
+    if lab.size and (lab.min() < 0 or lab.max() >= k):
+        raise ValueError("assignments out of range")
+    x_t = E.to_dev(x)
+    lab_t = E.to_dev(lab.astype(np.int32))
+    ctl_i32 = t.zeros(8, dtype=t.int32, device=x_t.device)
+    sums, counts, events = _update_dev(x_t, lab_t, k, dtype, ft_mode, hook, iteration, ctl_i32)
+    cent = E.finalize_dev(sums, counts, dtype, n_empty=ctl_i32[1:2])
+    if int(ctl_i32[1].item()):
+        if sq_dists is None:
+            c64 = E.finalize_dev(sums, counts, np.float64)
+            sq = t.empty(m, dtype=t.float64, device=x_t.device)
+            E.own_sq_dists_dev(x_t, lab_t, c64, sq)
+        else:
+            sq = E.to_dev(np.asarray(sq_dists, dtype=np.float64)).clone()
+        E.reseed_dev(x_t, counts, sq, cent)
+    return E.to_host(cent), E.to_host(counts), events
+
+
+def _plan_hooks(fault_spec, cfg, m, n, k, max_iters, dtype):
+    if isinstance(fault_spec, str):
+        fault_spec = FaultSpec.parse(fault_spec)
+    gemm_hook = update_hook = NOOP_HOOK
+    if fault_spec is not None and fault_spec.mode != "none":
+        bm, bn = cfg.block[0], cfg.block[1]
+        grid = ((m + bm - 1) // bm, (k + bn - 1) // bn)
+        horizon = max(max_iters, 1)
+        if fault_spec.target in ("gemm-accumulator", "both"):
+            gemm_hook = ScheduledFaultHook(plan_faults(fault_spec, horizon, grid, (bm, bn),
+                                                       dtype=dtype, shape=(m, k)))
+        if fault_spec.target in ("update-accumulator", "both"):
+            spec = dataclasses.replace(fault_spec, seed=fault_spec.seed + 1)
+            update_hook = ScheduledFaultHook(plan_faults(spec, horizon, (1, 1), (k, n),
+                                                         dtype=np.float64, shape=(k, n)))
+    return gemm_hook, update_hook
+
+
+class _DeviceAssign:
+    """One assignment pass on resident data (fused or checked), hook protocol
+    and event decoding included."""
+
+    def __init__(self, x_t, m, k, dtype, cfg, ft_mode, thr, threads):
+        t = E._torch()
+        self.x_t, self.m, self.k, self.dtype, self.cfg = x_t, m, k, dtype, cfg
+        self.checked = ft_mode != "off"
+        self.delta_rel, self.abs_tol = (thr.kernel_params() if thr is not None else (0.0, 0.0))
+        self.nbi = (m + cfg.block[0] - 1) // cfg.block[0]
+        self.threads = threads
+        self.md = t.empty(m, dtype=x_t.dtype, device=x_t.device)
+        self.labels = [t.empty(m, dtype=t.int32, device=x_t.device) for _ in range(2)]
+        self.events = E.DevEvents(64 * max(1, min(threads, self.nbi))) if self.checked else None
+
+    def run(self, cent_t, yn_t, hook, iteration, slot):
+        inj = E.injection_for(hook, iteration, self.dtype)
+        if self.checked:
+            cap = ((inj.n if inj else 0) + 64) * max(1, min(self.threads, self.nbi))
+            if cap > self.events.cap:
+                self.events = E.DevEvents(cap)
+            self.events.reset()
+        E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=get_variant(), inj=inj,
+                     checked=self.checked, delta_rel=self.delta_rel, abs_tol=self.abs_tol,
+                     iteration=iteration, events=self.events, out_idx=self.labels[slot],
+                     out_val=self.md)
+        return inj
+
+    def finish(self, hook, iteration, inj):
+        """Host side of the pass: events -> report, applied flips -> hook."""
+        report = None
+        if self.checked:
+            overflow, raw = self.events.read()
+            if overflow:
+                raise RuntimeError("detection event buffer overflow; threshold likely "
+                                   "miscalibrated")
+            evs = events_from_ring(raw)
+            report = DetectionReport(events=evs)
+            sched = _scheduled_tiles(inj)
+            report.false_alarms = sum(1 for e in evs if e.tile not in sched)
+        if inj is not None:
+            inj.finish()
+            hook.absorb_kernel_results(iteration, inj.host[5], inj.host[6], inj.host[7])
+        elif hook is not None and hook is not NOOP_HOOK:
+            hook.absorb_kernel_results(iteration, np.zeros(0, np.int64), np.zeros(0), np.zeros(0))
+        return report
+
+
+def lloyd(x, config, fault_spec=None):
+    """Lloyd's iteration until labels repeat, movement < tol, or max_iters,
+    then one final assignment (kmeans.py:210-319)."""
+    x = _as_operand(x)
+    config.validate()
+    m, n = x.shape
+    dtype = _dtype(x)
+    k = config.k
+    if k > m:
+        raise ValueError(f"k={k} exceeds the number of samples {m}")
+    threads = resolve_threads(config.threads)
+    cfg = _resolve_tile(config.tile, x, k, config.tune_table)
+    thr = config.threshold or Threshold.default_for(dtype)
+    t = E._torch()
+    gemm_hook, update_hook = _plan_hooks(fault_spec, cfg, m, n, k, config.max_iters, dtype)
+
+    timings = {"init_ns": 0, "assign_ns": 0, "update_ns": 0, "total_ns": 0}
+    t_total = time.perf_counter_ns()
+    t0 = time.perf_counter_ns()
+    c0 = init_centroids(x, k, seed=config.seed, method=config.init)
+    timings["init_ns"] = time.perf_counter_ns() - t0
+
+    x_t = E.to_dev(x)
+    dev = x_t.device
+    xsq = E.row_sq_norms_dev(x_t).to(t.float64)
+    sq = t.empty(m, dtype=t.float64, device=dev)
+    ctl_f64 = t.zeros(4, dtype=t.float64, device=dev)    # inertia, moved
+    ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)      # equal, n_empty, dmr flag
+    ctl_host = t.zeros(4, dtype=t.float64).pin_memory()
+    ctl_i32_host = t.zeros(8, dtype=t.int32).pin_memory()
+    cent = E.to_dev(c0)
+    eps = float(np.finfo(dtype).eps)
+    A = _DeviceAssign(x_t, m, k, dtype, cfg, config.ft_mode, thr if config.ft_mode != "off"
+                      else None, threads)
+    report = DetectionReport()
+    history = []
+    converged = False
+    iters = 0
+    slot = 0
+    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+
+    for it in range(config.max_iters):
+        ev[0].record()
+        yn = E.row_sq_norms_dev(cent)
+        inj = A.run(cent, yn, gemm_hook, it, slot)
+        ev[1].record()
+        E.sq_dists_dev(A.md, xsq, sq)
+        E.pairwise_sum_dev(sq, ctl_f64[0:1])
+        if it > 0:
+            E.labels_equal_dev(A.labels[slot], A.labels[1 - slot], ctl_i32[0:1])
+        rep = A.finish(gemm_hook, it, inj)
+        if rep is not None:
+            report.merge(rep)
+        sums, counts, ev_upd = _update_dev(x_t, A.labels[slot], k, dtype, config.ft_mode,
+                                          update_hook, it, ctl_i32)
+        new_cent = E.finalize_dev(sums, counts, dtype, n_empty=ctl_i32[1:2])
+        E.movement_dev(new_cent, cent, eps, ctl_f64[1:2])
+        ev[2].record()
+        ctl_host.copy_(ctl_f64, non_blocking=True)
+        ctl_i32_host.copy_(ctl_i32, non_blocking=True)
+        ev[2].synchronize()
+        t.cuda.current_stream().synchronize()
+        if int(ctl_i32_host[1]):
+            E.reseed_dev(x_t, counts, sq, new_cent)  # sq is free after the inertia sum
+            E.movement_dev(new_cent, cent, eps, ctl_f64[1:2])
+            ctl_host.copy_(ctl_f64)
+        timings["assign_ns"] += int(ev[0].elapsed_time(ev[1]) * 1e6)
+        timings["update_ns"] += int(ev[1].elapsed_time(ev[2]) * 1e6)
+        report.events.extend(ev_upd)
+        history.append(max(0.0, float(ctl_host[0])))
+        unchanged = it > 0 and bool(int(ctl_i32_host[0]))
+        moved = float(ctl_host[1])
+        iters = it + 1
+        cent = new_cent
+        slot = 1 - slot
+        if unchanged or moved < config.tol:
+            converged = True
+            break
+
+    yn = E.row_sq_norms_dev(cent)
+    inj = A.run(cent, yn, gemm_hook, iters, slot)
+    E.sq_dists_dev(A.md, xsq, sq)
+    E.pairwise_sum_dev(sq, ctl_f64[0:1])
+    rep = A.finish(gemm_hook, iters, inj)
+    if rep is not None:
+        report.merge(rep)
+    labels = E.to_host(A.labels[slot]).astype(np.int64)
+    inertia = max(0.0, float(ctl_f64[0].item()))
+    centroids = E.to_host(cent)
+    timings["total_ns"] = time.perf_counter_ns() - t_total
+    return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,
+                        converged=converged, report=report, timings=timings,
+                        inertia_history=history)

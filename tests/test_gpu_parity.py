@@ -1,0 +1,325 @@
+"""Parity of the CUDA path (through the C ABI) with the reference and the oracle.
+
+Every comparison is bitwise: labels, min_dists, centroids, inertia, counts,
+corrected values and detection events must equal the reference's bits.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+P = pytest.importorskip("paper_2408_01391_b200")
+from paper_2408_01391_b200 import gemm as G  # noqa: E402
+from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook  # noqa: E402
+from paper_2408_01391_b200.tiles import MICRO_SINGLE, make_config  # noqa: E402
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+VARIANTS = ["exact", "auto"]
+
+
+@pytest.fixture(params=VARIANTS)
+def variant(request):
+    old = G.get_variant()
+    G.set_variant(request.param)
+    yield request.param
+    G.set_variant(old)
+
+
+def _hook(entries):
+    return ScheduledFaultHook(FaultSchedule([FaultEntry(*e) for e in entries]))
+
+
+def test_row_sq_norms_golden(golden):
+    z = golden("assign_cases.npz")
+    for t in range(int(z["n"])):
+        assert P.row_sq_norms(z[f"c{t}_y"]).tobytes() == z[f"c{t}_yn"].tobytes()
+        assert P.row_sq_norms(z[f"c{t}_x"]).tobytes() == z[f"c{t}_xn"].tobytes()
+
+
+def test_fused_assign_golden(golden, variant):
+    z = golden("assign_cases.npz")
+    for t in range(int(z["n"])):
+        r = P.fused_assign(z[f"c{t}_x"], z[f"c{t}_y"])
+        assert r.assignments.dtype == np.int64
+        assert np.array_equal(r.assignments, z[f"c{t}_lab"]), t
+        assert r.min_dists.tobytes() == z[f"c{t}_val"].tobytes(), t
+    assert P.fused_assign(z["tie_x"], z["tie_y"]).assignments.tolist() == [0]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_fused_assign_vs_oracle(dt, variant):
+    rng = np.random.default_rng(77)
+    for m, d, k in [(1000, 128, 1024), (4097, 32, 64), (777, 7, 300), (2048, 256, 33),
+                    (513, 1, 5), (1, 3, 1), (300, 513, 17), (5000, 4, 4096)]:
+        x = np.ascontiguousarray(rng.standard_normal((m, d)), dtype=dt)
+        y = np.ascontiguousarray(rng.standard_normal((k, d)), dtype=dt)
+        r = P.fused_assign(x, y)
+        lab, val = O.assign(x, y)
+        assert np.array_equal(r.assignments, lab), (m, d, k)
+        assert r.min_dists.tobytes() == val.tobytes(), (m, d, k)
+
+
+def test_custom_tiles_same_result():
+    rng = np.random.default_rng(5)
+    x = np.ascontiguousarray(rng.standard_normal((333, 40)), dtype=np.float32)
+    y = np.ascontiguousarray(rng.standard_normal((70, 40)), dtype=np.float32)
+    lab, val = O.assign(x, y)
+    for blk in [(128, 64, 16), (32, 32, 8), (16, 16, 4), (64, 128, 32), (8, 8, 8), (2, 4, 2),
+                (256, 256, 64), (1, 1, 1)]:
+        r = _assign_block(x, y, blk)
+        assert np.array_equal(r[0], lab), blk
+        assert r[1].tobytes() == val.tobytes(), blk
+
+
+def _assign_block(x, y, blk):
+    from paper_2408_01391_b200 import _engine as E
+    x_t, y_t = E.to_dev(x), E.to_dev(y)
+    idx, val = E.assign_dev(x_t, y_t, E.row_sq_norms_dev(y_t), blk, variant="exact")
+    return E.to_host(idx).astype(np.int64), E.to_host(val)
+
+
+def test_gemm_tiled_exact():
+    rng = np.random.default_rng(9)
+    a = np.ascontiguousarray(rng.standard_normal((70, 37)), dtype=np.float32)
+    b = np.ascontiguousarray(rng.standard_normal((45, 37)), dtype=np.float32)
+    out = P.gemm_tiled(a, b)
+    for i in range(0, 70, 7):
+        for j in range(0, 45, 5):
+            assert out[i, j] == O.exact_dot(a[i], b[j])
+    assert P.gemm_tiled(np.eye(2, dtype=np.float32),
+                        np.array([[5, 6], [7, 8]], np.float32)).tolist() == [[5, 7], [6, 8]]
+
+
+def test_update_golden(golden):
+    z = golden("update_cases.npz")
+    for t in range(int(z["n"])):
+        c, counts, ev = P.update_step(z[f"u{t}_x"], z[f"u{t}_lab"], int(z[f"u{t}_k"]),
+                                      sq_dists=z[f"u{t}_sq"])
+        assert counts.tolist() == z[f"u{t}_counts"].tolist(), t
+        assert c.tobytes() == z[f"u{t}_c"].tobytes(), t
+        assert ev == []
+
+
+def test_update_empty_cluster_own_dists():
+    rng = np.random.default_rng(4)
+    x = np.ascontiguousarray(rng.random((50, 3)), dtype=np.float32)
+    lab = np.zeros(50, dtype=np.int64)
+    c, counts, _ = P.update_step(x, lab, 2)
+    ref, _ = O.update_step(x, lab, 2)
+    assert counts.tolist() == [50, 0]
+    assert c.tobytes() == ref.tobytes()
+
+
+def _lloyd_case(z, t):
+    rows, cols, blobs, k, mi, seed = (int(v) for v in z[f"l{t}_args"])
+    spread, tol = (float(v) for v in z[f"l{t}_meta"])
+    x, _, _ = P.gaussian_mixture(rows, cols, blobs, spread, precision=str(z[f"l{t}_prec"]),
+                                 seed=seed)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z[f"l{t}_xsha"])
+    return x, P.KMeansConfig(k=k, seed=seed, init=str(z[f"l{t}_init"]), max_iters=mi, tol=tol)
+
+
+def test_lloyd_golden(golden, variant):
+    z = golden("lloyd_cases.npz")
+    for t in range(int(z["n"])):
+        x, cfg = _lloyd_case(z, t)
+        r = P.lloyd(x, cfg)
+        assert r.iters == int(z[f"l{t}_iters"]), t
+        assert r.converged == bool(z[f"l{t}_conv"]), t
+        assert np.array_equal(r.assignments, z[f"l{t}_lab"]), t
+        assert r.centroids.tobytes() == z[f"l{t}_c"].tobytes(), t
+        assert r.inertia == float(z[f"l{t}_inertia"]), t
+        assert r.inertia_history == z[f"l{t}_hist"].tolist(), t
+
+
+def test_lloyd_c1_golden(golden, variant):
+    """BASELINE configs[0]: N=100k, D=32, K=64 f32, 20 iterations, seed 0."""
+    z = golden("lloyd_c1.npz")
+    x, _, _ = P.gaussian_mixture(100000, 32, 64, 0.25, precision="single", seed=0)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == str(z["xsha"])
+    r = P.lloyd(x, P.KMeansConfig(k=64, max_iters=20, tol=0.0, seed=0, init="random-sample"))
+    assert r.iters == int(z["iters"]) == 20
+    assert np.array_equal(r.assignments, z["lab"].astype(np.int64))
+    assert r.centroids.tobytes() == z["c"].tobytes()
+    assert r.inertia_history == z["hist"].tolist()
+    assert r.inertia == float(z["inertia"])
+
+
+def test_checked_assign_golden(golden):
+    z = golden("checked_cases.npz")
+    for n in [str(v) for v in z["names"]]:
+        x, y, ent = z[f"{n}_x"], z[f"{n}_y"], z[f"{n}_ent"]
+        blk = tuple(int(v) for v in z[f"{n}_block"])
+        cfg = None if blk[0] < 0 else make_config(blk, blk, MICRO_SINGLE)
+        entries = [(int(e[0]), (int(e[1]), int(e[2])), (int(e[3]), int(e[4])), int(e[5]))
+                   for e in ent]
+        h1 = _hook(entries)
+        res, rep = P.checked_assign(x, y, cfg=cfg, hook=h1)
+        assert np.array_equal(res.assignments, z[f"{n}_lab"]), n
+        assert res.min_dists.tobytes() == z[f"{n}_val"].tobytes(), n
+        ev = np.array([[e.iteration, e.tile[0], e.tile[1],
+                        0 if e.kind == "detected-corrected" else 1, e.loc[0], e.loc[1]]
+                       for e in rep.events], np.int64).reshape(-1, 6)
+        assert ev.tolist() == z[f"{n}_ev"].tolist(), n
+        assert [e.delta for e in rep.events] == z[f"{n}_evdelta"].tolist(), n
+        inj = np.array([[d["before"], d["after"]] for d in h1.injected]).reshape(-1, 2)
+        assert inj.tobytes() == z[f"{n}_inj"].tobytes(), n
+        # unprotected: corruption flows to the result exactly like the reference
+        h2 = _hook(entries)
+        plain = P.fused_assign(x, y, cfg=cfg, hook=h2)
+        assert np.array_equal(plain.assignments, z[f"{n}_plain_lab"]), n
+        assert plain.min_dists.tobytes() == z[f"{n}_plain_val"].tobytes(), n
+        clean = P.fused_assign(x, y, cfg=cfg)
+        assert np.array_equal(clean.assignments, z[f"{n}_clean_lab"]), n
+
+
+def test_fault_free_checked_is_bit_identical_and_silent():
+    rng = np.random.default_rng(202)
+    for case in range(120):
+        m, n, k = int(rng.integers(1, 192)), int(rng.integers(1, 64)), int(rng.integers(1, 80))
+        dt = np.float32 if case % 2 == 0 else np.float64
+        scale = 100.0 if case % 5 == 0 else 1.0
+        x = np.ascontiguousarray(rng.standard_normal((m, n)) * scale, dtype=dt)
+        y = np.ascontiguousarray(rng.standard_normal((k, n)), dtype=dt)
+        out, rep = P.checked_gemm(x, y)
+        assert rep.detections == 0, case
+        assert out.tobytes() == P.gemm_tiled(x, y).tobytes(), case
+        res, rep2 = P.checked_assign(x, y)
+        plain = P.fused_assign(x, y)
+        assert rep2.detections == 0
+        assert np.array_equal(res.assignments, plain.assignments)
+        assert res.min_dists.tobytes() == plain.min_dists.tobytes()
+
+
+def test_exhaustive_single_error_sweep(golden):
+    """Acceptance 3: every (element, bit) flip of an 8x8 f32 tile -> same
+    outcome, location and corrected output bits as the reference."""
+    z = golden("sweep_cases.npz")
+    a, b, ref = z["a"], z["b"], z["ref"]
+    assert P.gemm_tiled(a, b).tobytes() == ref.tobytes()
+    rows, outs = z["rows"], z["outs"]
+    silent = 0
+    for q, (i, j, bit, det, corr, li, lj) in enumerate(rows.tolist()):
+        out, rep = P.checked_gemm(a, b, hook=_hook([(0, (0, 0), (i, j), bit)]))
+        assert (rep.detections, rep.corrections) == (det, corr), (i, j, bit)
+        if rep.events:
+            assert rep.events[0].loc == (li, lj)
+        assert out.tobytes() == outs[q].tobytes(), (i, j, bit)
+        err = float(np.abs(out.astype(np.float64) - ref.astype(np.float64)).max())
+        silent += not ((corr == 1 or det == 0) and err <= 1e-4 * 8)
+    assert silent == 0
+
+
+def test_lloyd_ft_transparency_golden(golden):
+    z = golden("lloyd_ft_cases.npz")
+    for t in range(int(z["n"])):
+        seed = int(z[f"f{t}_seed"])
+        x, _, _ = P.gaussian_mixture(2048, 8, 4, 0.2, precision="single", seed=seed)
+        base = P.lloyd(x, P.KMeansConfig(k=4, seed=seed))
+        prot = P.lloyd(x, P.KMeansConfig(k=4, seed=seed, ft_mode=str(z[f"f{t}_mode"])),
+                       fault_spec=str(z[f"f{t}_spec"]))
+        assert np.array_equal(base.assignments, z[f"f{t}_base_lab"])
+        assert np.array_equal(prot.assignments, z[f"f{t}_lab"])
+        assert prot.iters == int(z[f"f{t}_iters"])
+        r = prot.report
+        assert [r.detections, r.corrections, r.uncorrectable, r.dmr_mismatches] == \
+            z[f"f{t}_counts"].tolist()
+        ev = np.array([[e.iteration, e.tile[0], e.tile[1], e.loc[0], e.loc[1]]
+                       for e in r.events], np.int64).reshape(-1, 5)
+        assert ev.tolist() == z[f"f{t}_ev"].tolist()
+
+
+@pytest.mark.slow
+def test_acceptance4_ft_transparency(golden):
+    z = golden("acceptance4_cases.npz")
+    x, _, _ = P.gaussian_mixture(65536, 8, 4, 0.25, precision="single", seed=404)
+    for k in (4, 128):
+        base = P.lloyd(x, P.KMeansConfig(k=k, seed=404, max_iters=50))
+        prot = P.lloyd(x, P.KMeansConfig(k=k, seed=404, max_iters=50, ft_mode="abft+dmr"),
+                       fault_spec=P.FaultSpec(mode="fixed-count", count=10, seed=405))
+        assert np.array_equal(base.assignments, z[f"k{k}_base_lab"].astype(np.int64))
+        assert base.centroids.tobytes() == z[f"k{k}_base_c"].tobytes()
+        assert base.inertia_history == z[f"k{k}_base_hist"].tolist()
+        assert np.array_equal(prot.assignments, z[f"k{k}_prot_lab"].astype(np.int64))
+        assert prot.centroids.tobytes() == z[f"k{k}_prot_c"].tobytes()
+        assert prot.iters == int(z[f"k{k}_prot_iters"])
+        r = prot.report
+        assert [r.detections, r.corrections, r.uncorrectable, r.dmr_mismatches] == \
+            z[f"k{k}_prot_counts"].tolist()
+        ev = np.array([[e.iteration, e.tile[0], e.tile[1], e.loc[0], e.loc[1],
+                        0 if e.kind == "detected-corrected" else 1] for e in r.events
+                       if e.kind != "dmr-mismatch"], np.int64).reshape(-1, 6)
+        assert ev.tolist() == z[f"k{k}_prot_ev"].tolist()
+
+
+def test_dmr_update_golden(golden):
+    z = golden("dmr_cases.npz")
+    for t, (ci, cj, bit, nev) in enumerate(z["meta"].tolist()):
+        x, lab = z[f"t{t}_x"], z[f"t{t}_lab"]
+        got, _, ev = P.update_step(x, lab, 5, ft_mode="abft+dmr",
+                                   hook=_hook([(0, (0, 0), (ci, cj), bit)]))
+        assert len(ev) == nev and all(e.kind == "dmr-mismatch" for e in ev)
+        assert got.tobytes() == z[f"t{t}_got"].tobytes() == z[f"t{t}_clean"].tobytes()
+        off, _, _ = P.update_step(x, lab, 5, hook=_hook([(0, (0, 0), (ci, cj), bit)]))
+        assert off.tobytes() == z[f"t{t}_off"].tobytes()
+
+
+def test_dmr_persistent_escalates():
+    class AlwaysCorrupt:
+        def maybe_corrupt(self, iteration, tile, acc):
+            acc[0, 0] += 1.0
+
+    x = np.ones((8, 2), dtype=np.float32)
+    with pytest.raises(P.FaultEscalationError):
+        P.update_step(x, np.zeros(8, dtype=np.int64), 1, ft_mode="abft+dmr",
+                      hook=AlwaysCorrupt())
+
+
+def test_estimator_surface():
+    from sklearn.base import clone
+    from sklearn.metrics import adjusted_rand_score
+
+    x, labels, _ = P.gaussian_mixture(1500, 6, 3, 0.1, precision="single", seed=31)
+    est = P.FTKMeans(n_clusters=3, random_state=2).fit(x)
+    assert est.cluster_centers_.shape == (3, 6) and est.labels_.dtype == np.int64
+    assert est.converged_ and est.detection_report_.detections == 0
+    assert adjusted_rand_score(labels, est.labels_) >= 0.99
+    assert np.array_equal(est.predict(x), est.labels_)
+    assert est.score(x) == pytest.approx(-est.inertia_, rel=1e-5)
+    ref = O.lloyd(x, 3, seed=2)
+    assert np.array_equal(est.labels_, ref["assignments"])
+    assert est.cluster_centers_.tobytes() == ref["centroids"].tobytes()
+    prot = P.FTKMeans(n_clusters=3, random_state=6, ft_mode="abft+dmr", inject="fixed:2").fit(x)
+    clean = P.FTKMeans(n_clusters=3, random_state=6).fit(x)
+    assert prot.detection_report_.corrections > 0
+    assert np.array_equal(prot.labels_, clean.labels_)
+    assert clone(est).get_params() == est.get_params()
+    d64 = P.FTKMeans(n_clusters=3, random_state=7).fit(x.astype(np.float64))
+    assert d64.cluster_centers_.dtype == np.float64
+    with pytest.raises(ValueError):
+        bad = x.copy()
+        bad[3, 1] = np.nan
+        P.FTKMeans(n_clusters=2).fit(bad)
+
+
+def test_native_library_is_the_one_loaded():
+    from paper_2408_01391_b200 import _native
+
+    before = _native.launch_count()
+    P.fused_assign(np.ones((8, 4), np.float32), np.ones((2, 4), np.float32))
+    assert _native.launch_count() > before
+    import os
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libftkb200.so" in maps
