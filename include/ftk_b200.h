@@ -163,6 +163,10 @@ int ftk_own_sq_dists(ftk_ctx *ctx, int dtype, const void *x, const int32_t *labe
 int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64_t bit,
                  double *before_after, void *stream);
 
+/* Diagnostics: number of rows the last TC-variant assignment on this context
+ * could not certify and resolved with the exact fallback (synchronises). */
+int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

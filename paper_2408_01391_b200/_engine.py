@@ -288,3 +288,9 @@ def own_sq_dists_dev(x_t, labels_i32, cent64, out):
     N.check(N.load().ftk_own_sq_dists(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), ptr(labels_i32),
                                       ptr(cent64), m, d, ptr(out), stream()), "ftk_own_sq_dists")
     return out
+
+def tc_fallback_rows():
+    import ctypes
+    v = ctypes.c_int64(0)
+    N.check(N.load().ftk_tc_fallback_rows(ctx(), ctypes.byref(v), stream()), "ftk_tc_fallback_rows")
+    return int(v.value)

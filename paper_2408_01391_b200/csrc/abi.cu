@@ -62,6 +62,7 @@ int own_sq_dists_run(ftk_ctx *, int, const void *, const int32_t *, const double
 int flip_f64_run(double *, int64_t, int64_t, int64_t, int64_t, double *, cudaStream_t);
 int tc_assign_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
                   int64_t, int32_t *, void *, cudaStream_t);
+int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
 
@@ -198,6 +199,14 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
                  double *before_after, void *stream) {
     (void)ctx;
     return flip_f64_run(a, d, i, j, bit, before_after, as_stream(stream));
+}
+
+int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
+    if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    unsigned v = 0;
+    int rc = tc_last_fallback(ctx, &v, as_stream(stream));
+    *out = int64_t(v);
+    return rc;
 }
 
 }  // extern "C"

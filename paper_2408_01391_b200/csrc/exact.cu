@@ -25,6 +25,7 @@ constexpr int KC = 16;  // k-chunk staged in shared memory per step
 struct ExactParams {
     const void *x, *y, *yn;
     int64_t m, k, d, bm, bn, bk;
+    int64_t prow;  // physical rows per CTA (== bm in checked mode)
     int pb;  // physical tile width (live columns of a logical column block)
     int32_t *out_idx;
     void *out_val;
@@ -275,7 +276,7 @@ template <typename T, int TM, bool CHECKED>
 __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(ExactParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int pb = P.pb;
-    const int64_t bm = P.bm, bn = P.bn, kdim = P.d;
+    const int64_t bm = P.prow, lbm = P.bm, bn = P.bn, kdim = P.d;  // bm: physical rows
     const SmemLayout L = smem_layout<T>(bm, pb, P.bk, CHECKED, P.out_mat != nullptr);
     T *Xs = reinterpret_cast<T *>(smem + L.xs);
     T *Cs = reinterpret_cast<T *>(smem + L.cs);
@@ -379,12 +380,16 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
         // (_kernels.py:462-474 / 568-583)
         if (P.n_inj > 0 && live_col) {
             for (int64_t q = 0; q < P.n_inj; ++q) {
-                if (P.ibi[q] != bi || P.ibj[q] != bj) continue;
+                if (P.ibj[q] != bj) continue;
                 int64_t ei = P.iei[q], ej = P.iej[q];
-                if (ej != jl || ei >= mi || ej >= nj) continue;
+                // logical tile (bi, bj) cell (ei, ej) -> global row; live cells only
+                int64_t grow = P.ibi[q] * lbm + ei;
+                if (ej != jl || ej >= nj || ei >= lbm || grow >= P.m) continue;
+                int64_t lrow = grow - i0;  // row within this CTA
+                if (lrow < 0 || lrow >= mi) continue;
 #pragma unroll
                 for (int t = 0; t < TM; ++t) {
-                    if (r * TM + t == ei) {
+                    if (r * TM + t == lrow) {
                         T before = acc[t];
                         T after = flip_bit(before, P.ibit[q]);
                         acc[t] = after;
@@ -550,7 +555,7 @@ static int launch_tm(const ExactParams &P, int threads, size_t smem, cudaStream_
     if (smem > 48 * 1024)
         FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(smem)));
-    int64_t nbi = (P.m + P.bm - 1) / P.bm;
+    int64_t nbi = (P.m + P.prow - 1) / P.prow;
     kern<<<dim3(unsigned(nbi)), dim3(threads), smem, st>>>(P);
     FTK_LAUNCHED("exact_tile_kernel");
     return FTK_OK;
@@ -558,22 +563,31 @@ static int launch_tm(const ExactParams &P, int threads, size_t smem, cudaStream_
 
 template <typename T, bool CHECKED>
 static int launch_exact(ExactParams P, cudaStream_t st) {
+    // Physical CTA rows: the whole logical row block when checksums need it
+    // (checked / materialised-checked), otherwise split large logical blocks
+    // into independent row slabs (unprotected rows do not interact).
     const bool f64 = sizeof(T) == 8;
     const int tm_cap = f64 ? 32 : 64;
-    int tm = int(P.bm < (f64 ? 16 : 32) ? P.bm : (f64 ? 16 : 32));
-    auto nthreads = [&](int t) { return int((P.pb * (P.bm / t) + 31) / 32 * 32); };
-    while (nthreads(tm) < 128 && tm > 4) tm /= 2;
-    while (nthreads(tm) > exact_max_threads(tm) && tm < tm_cap && tm < P.bm) tm *= 2;
-    int threads = nthreads(tm);  // whole warps; padding threads own no rows
-    if (threads > exact_max_threads(tm)) {
-        set_error("tile too large for the exact kernel (bn * bm / 64 > 1024)");
-        return FTK_ERR_UNSUPPORTED;
+    const bool mat = P.out_mat != nullptr;
+    int64_t prow = P.bm;
+    int tm = 0, threads = 0;
+    for (;;) {
+        tm = int(prow < (f64 ? 16 : 32) ? prow : (f64 ? 16 : 32));
+        auto nthreads = [&](int t) { return int((P.pb * (prow / t) + 31) / 32 * 32); };
+        while (nthreads(tm) < 128 && tm > 4) tm /= 2;
+        while (nthreads(tm) > exact_max_threads(tm) && tm < tm_cap && tm < prow) tm *= 2;
+        threads = nthreads(tm);  // whole warps; padding threads own no rows
+        SmemLayout L = smem_layout<T>(prow, P.pb, P.bk, CHECKED, mat);
+        bool fits = threads <= exact_max_threads(tm) && L.total <= 227 * 1024;
+        if (fits) break;
+        if (CHECKED || prow <= 1) {
+            set_error("logical tile too large for the exact checked kernel");
+            return FTK_ERR_UNSUPPORTED;
+        }
+        prow /= 2;
     }
-    SmemLayout L = smem_layout<T>(P.bm, P.pb, P.bk, CHECKED, P.out_mat != nullptr);
-    if (L.total > 227 * 1024) {
-        set_error("tile too large for shared memory in the exact kernel");
-        return FTK_ERR_UNSUPPORTED;
-    }
+    P.prow = prow;
+    SmemLayout L = smem_layout<T>(prow, P.pb, P.bk, CHECKED, mat);
     switch (tm) {
         case 1: return launch_tm<T, 1, CHECKED>(P, threads, L.total, st);
         case 2: return launch_tm<T, 2, CHECKED>(P, threads, L.total, st);

@@ -1,10 +1,528 @@
-// tc.cu -- tcgen05 screening assign (placeholder until the TC path lands).
+// tc.cu -- tensor-core screened assignment with certified exact refinement
+// (sm_100a: TMA + mbarrier pipeline, tcgen05.mma kind::tf32 into TMEM,
+// tcgen05.ld epilogue).
+//
+// The reference's labels and min_dists are functions of its exact fp32
+// evaluation order (_kernels.py:44-102).  This path reproduces them bit for
+// bit without evaluating every distance exactly:
+//
+//   1. SCREEN  (tensor cores): s_ij = yn_j - 2 * <x_i, c_j>_tf32, fp32 TMEM
+//      accumulators, TF32 operands (truncated mantissas).  The epilogue keeps
+//      per row the two smallest screened values (index packed in the low
+//      mantissa bits of the minimum) -- the N x K distance matrix never
+//      leaves the SM.
+//   2. CERTIFY: |s_ij - d_ij^ref| <= A_i + B |s_ij| with
+//      A_i = 2 ||x_i|| cmax (2^-9 + 2^-20 + 3 D 2^-24) (tf32 operand
+//      truncation, fp32 accumulation, the reference's own rounding) and
+//      B = 2^-15 + 2^-22 (index packing, final roundings).  When
+//      m2 - m1 > 2 A_i + B (|m1| + |m2|) the reference's strict argmin is
+//      provably the screened winner.
+//   3. REFINE  (SIMT, exact order): acc = sum_k fl(x_ik * c_jk) k ascending,
+//      min_dist = yn_j - (acc + acc) for the winner only, from the X tile
+//      already in shared memory.
+//   4. FALLBACK: uncertified rows go to a list that exact_rows_kernel
+//      resolves with a full exact argmin.
+//
+// Roles per CTA (6 warps): w0 TMA producer, w1 TMEM allocator + MMA issuer
+// (one elected thread), w2..w5 epilogue (one accumulator row per thread;
+// warp w reads TMEM lanes 32*(w%4)..+31).  The X tile (128 rows x D) is
+// loaded once and stays resident; centroid k-blocks stream through a
+// multi-stage ring; two TMEM accumulators let the MMA of centroid tile t+1
+// overlap the epilogue of tile t.
+
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace ftk {
-int tc_assign_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
-                  int64_t, int32_t *, void *, cudaStream_t) {
-    set_error("tc variant not built");
-    return FTK_ERR_UNSUPPORTED;
+
+constexpr int TC_BM = 128;          // rows per CTA (UMMA M)
+constexpr int TC_KB = 32;           // fp32 elements per 128-byte swizzle row
+constexpr int TC_THREADS = 192;     // 6 warps
+constexpr int TC_MAX_D = 256;       // resident-A limit
+
+struct TcParams {
+    const float *x;      // m x d   (exact values for refinement)
+    const float *y;      // k x d
+    const float *yn;     // k       (exact fp32 squared norms, reference order)
+    int64_t m, k, d;
+    int nkb;             // ceil(d / 32)
+    int ntiles;          // ceil(k / BN)
+    int stages;
+    float a_coef;        // 2 cmax (2^-9 + 2^-20 + 3 d 2^-24) * (1 + 2^-10)
+    float b_coef;
+    const float *cmax2;  // device scalar: max_j yn_j (upper bound of ||c||^2)
+    int32_t *out_idx;
+    float *out_val;
+    int32_t *fb_rows;    // uncertified rows (fallback list)
+    unsigned *fb_count;
+};
+
+// ----------------------------------------------------------- PTX helpers --
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_barrier_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(dst_smem)),
+                 "r"(ncols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// K-major, 128-byte swizzled operand tile (rows of 128 B, 8-row atoms of
+// 1024 B): start address >> 4, SBO = 1024 B, version 1, layout SWIZZLE_128B.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFF);
+    d |= uint64_t(1) << 16;                 // LBO (unused for swizzled K-major)
+    d |= uint64_t(1024 >> 4) << 32;         // SBO
+    d |= uint64_t(1) << 46;                 // descriptor version (sm100)
+    d |= uint64_t(2) << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) |
+           (uint32_t(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------- kernel ----
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    tc_screen_kernel(const __grid_constant__ CUtensorMap tmX,
+                     const __grid_constant__ CUtensorMap tmC, TcParams P) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte alignment for the swizzle atoms
+    unsigned char *smem = reinterpret_cast<unsigned char *>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int nkb = P.nkb, S = P.stages;
+    const uint32_t A_KB_BYTES = TC_BM * 128;       // one k-block of X
+    const uint32_t B_BYTES = BN * 128;             // one k-block of C
+    unsigned char *sA = smem;                      // nkb x 16 KB
+    unsigned char *sB = sA + size_t(nkb) * A_KB_BYTES;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + size_t(S) * B_BYTES);
+    uint64_t *full = bars, *empty = bars + S;
+    uint64_t *a_full = bars + 2 * S;
+    uint64_t *t_full = a_full + 1, *t_empty = a_full + 3;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 5);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = int64_t(blockIdx.x) * TC_BM;
+
+    if (warp == 0 && lane == 0) {
+        prefetch_tmap(&tmX);
+        prefetch_tmap(&tmC);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(a_full, 1);
+        mbar_init(&t_full[0], 1);
+        mbar_init(&t_full[1], 1);
+        mbar_init(&t_empty[0], 4);
+        mbar_init(&t_empty[1], 4);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, (2 * BN) < 32 ? 32 : 2 * BN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // X tile: all k-blocks, once
+            mbar_expect_tx(a_full, A_KB_BYTES * nkb);
+            for (int kb = 0; kb < nkb; ++kb)
+                tma_load_2d(sA + size_t(kb) * A_KB_BYTES, &tmX, a_full, kb * TC_KB, int(row0));
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = 0; t < P.ntiles; ++t) {
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], B_BYTES);
+                    tma_load_2d(sB + size_t(stage) * B_BYTES, &tmC, &full[stage], kb * TC_KB,
+                                t * BN);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_tf32(TC_BM, BN);
+            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            mbar_wait(a_full, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = 0; t < P.ntiles; ++t) {
+                const int buf = t & 1;
+                const uint32_t use = uint32_t(t >> 1) & 1;
+                mbar_wait(&t_empty[buf], use ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem + uint32_t(buf * BN);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {  // 4 x (K = 8 tf32) per 128-byte row
+                        uint64_t ad = smem_desc(a_base + kb * A_KB_BYTES + kk * 32);
+                        uint64_t bd = smem_desc(b_base + stage * B_BYTES + kk * 32);
+                        mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                    }
+                    mma_commit(&empty[stage]);
+                    if (++stage == S) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&t_full[buf]);
+            }
+        }
+    } else {
+        // ---------------------------------------------------- epilogue --
+        const int quad = warp & 3;              // TMEM lane group this warp may access
+        const int r = quad * 32 + lane;         // accumulator row
+        const int64_t grow = row0 + r;
+        const uint32_t lane_base = uint32_t(quad * 32) << 16;
+        float m1 = INFINITY, m2 = INFINITY;
+        int tile1 = 0;
+        for (int t = 0; t < P.ntiles; ++t) {
+            const int buf = t & 1;
+            const uint32_t use = uint32_t(t >> 1) & 1;
+            mbar_wait(&t_full[buf], use);
+            tc_fence_after();
+            float t1 = INFINITY, t2 = INFINITY;
+            const int64_t c0 = int64_t(t) * BN;
+            const bool partial = c0 + BN > P.k;
+#pragma unroll 1
+            for (int ch = 0; ch < BN / 32; ++ch) {
+                uint32_t v[32];
+                tmem_ld32(tmem + lane_base + uint32_t(buf * BN + ch * 32), v);
+                const float4 *yn4 = reinterpret_cast<const float4 *>(P.yn + c0 + ch * 32);
+                if (!partial) {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        float4 yv = __ldg(yn4 + q);
+                        float yy[4] = {yv.x, yv.y, yv.z, yv.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = q * 4 + u;
+                            float dd = fmaf(-2.0f, __uint_as_float(v[e]), yy[u]);
+                            float p = __uint_as_float((__float_as_uint(dd) & ~0x7Fu) |
+                                                      uint32_t(ch * 32 + e));
+                            float hi = fmaxf(t1, p);
+                            t1 = fminf(t1, p);
+                            t2 = fminf(t2, hi);
+                        }
+                    }
+                } else {
+                    for (int e = 0; e < 32; ++e) {
+                        const int64_t col = c0 + ch * 32 + e;
+                        if (col >= P.k) break;
+                        float dd = fmaf(-2.0f, __uint_as_float(v[e]), P.yn[col]);
+                        float p = __uint_as_float((__float_as_uint(dd) & ~0x7Fu) |
+                                                  uint32_t(ch * 32 + e));
+                        float hi = fmaxf(t1, p);
+                        t1 = fminf(t1, p);
+                        t2 = fminf(t2, hi);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&t_empty[buf]);
+            // merge tile top-2 into the running top-2
+            float hi = fmaxf(m1, t1);
+            if (t1 < m1) tile1 = t;
+            m1 = fminf(m1, t1);
+            m2 = fminf(fminf(m2, t2), hi);
+        }
+
+        if (grow < P.m) {
+            const int j = tile1 * BN + int(__float_as_uint(m1) & 0x7Fu);
+            // one pass over the resident X row: ||x||^2 (bound) and the exact
+            // sequential dot product with the screened winner
+            const float *cj = P.y + int64_t(j) * P.d;
+            float acc = 0.0f, xx = 0.0f;
+            for (int k = 0; k < P.d; ++k) {
+                const int kb = k >> 5, w = k & 31;
+                const uint32_t off = uint32_t(kb) * A_KB_BYTES + uint32_t(r) * 128 +
+                                     (uint32_t(((w >> 2) ^ (r & 7)) << 4)) + uint32_t(w & 3) * 4;
+                const float xv = *reinterpret_cast<const float *>(sA + off);
+                acc = __fadd_rn(acc, __fmul_rn(xv, __ldg(cj + k)));
+                xx = fmaf(xv, xv, xx);
+            }
+            const float A = P.a_coef * sqrtf(xx * (1.0f + 0x1p-16f)) * sqrtf(*P.cmax2);
+            const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
+            if (m2 - m1 > gap_need && m1 < INFINITY) {
+                P.out_idx[grow] = j;
+                P.out_val[grow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
+            } else {
+                unsigned slot = atomicAdd(P.fb_count, 1u);
+                P.fb_rows[slot] = int32_t(grow);
+            }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, (2 * BN) < 32 ? 32 : 2 * BN);
+    }
+}
+
+// ------------------------------------------------ exact fallback rows ----
+// One warp per listed row: lanes take centroids j = lane, lane + 32, ...,
+// each computing the exact sequential dot product; (value, index) lexmin.
+template <typename T>
+__global__ void exact_rows_kernel(const T *x, const T *y, const T *yn, int64_t k, int64_t d,
+                                  const int32_t *rows, const unsigned *count, int32_t *out_idx,
+                                  T *out_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const unsigned n = *count;
+    for (int64_t q = wid; q < n; q += nw) {
+        const int64_t i = rows[q];
+        const T *xr = x + i * d;
+        T bv = T(INFINITY);
+        int32_t bj = 0;
+        for (int64_t j = lane; j < k; j += 32) {
+            const T *cr = y + j * d;
+            T acc = T(0);
+            for (int64_t kk = 0; kk < d; ++kk) acc = add_rn(acc, mul_rn(xr[kk], cr[kk]));
+            T dd = sub_rn(yn[j], add_rn(acc, acc));
+            argmin_merge(bv, bj, dd, int32_t(j));
+        }
+        for (int off = 16; off; off >>= 1) {
+            T ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            int32_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            argmin_merge(bv, bj, ov, oj);
+        }
+        if (lane == 0) {
+            out_idx[i] = bj;
+            out_val[i] = bv;
+        }
+    }
+}
+
+__global__ void tc_prep_kernel(const float *yn, int64_t k, float *cmax2, unsigned *fb_count) {
+    float m = 0.0f;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) m = fmaxf(m, yn[j]);
+    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    __shared__ float sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float mm = 0.0f;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) mm = fmaxf(mm, sh[w]);
+        // yn is a rounded sum: inflate to an upper bound of max ||c||^2
+        *cmax2 = mm * (1.0f + 0x1p-10f);
+        *fb_count = 0u;
+    }
+}
+
+// ------------------------------------------------------------- host ------
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                    const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                    const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static PFN_encodeTiled get_encode() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(p);
+    });
+    return fn;
+}
+
+static int make_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
+                    uint32_t box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return FTK_ERR_CUDA;
+    }
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(float)};
+    cuuint32_t box[2] = {TC_KB, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+        return FTK_ERR_CUDA;
+    }
+    return FTK_OK;
+}
+
+template <int BN>
+static int launch_screen(const TcParams &P0, const CUtensorMap &mx, const CUtensorMap &mc,
+                         int64_t ntiles_m, cudaStream_t st) {
+    TcParams P = P0;
+    const size_t a_bytes = size_t(P.nkb) * TC_BM * 128;
+    const size_t b_bytes = size_t(BN) * 128;
+    // aim for two CTAs per SM when the resident tile allows it
+    const size_t budget = (a_bytes + 3 * b_bytes + 2048) * 2 <= 220 * 1024 ? 110 * 1024 : 220 * 1024;
+    int stages = int((budget - a_bytes - 2048) / b_bytes);
+    if (stages > 6) stages = 6;
+    if (stages < 2) stages = 2;
+    P.stages = stages;
+    const size_t smem = 1024 + a_bytes + stages * b_bytes + 256;
+    if (smem > 227 * 1024) {
+        set_error("tc: tile exceeds shared memory");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    auto kern = tc_screen_kernel<BN>;
+    FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<dim3(unsigned(ntiles_m)), dim3(TC_THREADS), smem, st>>>(mx, mc, P);
+    FTK_LAUNCHED("tc_screen_kernel");
+    return FTK_OK;
+}
+
+int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
+    return dtype == FTK_F32 && d >= 8 && d % 4 == 0 && d <= TC_MAX_D && k >= 1 && m >= 1 &&
+           k < (int64_t(1) << 30);
+}
+
+int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn,
+                  int64_t m, int64_t k, int64_t d, int32_t *out_idx, void *out_val,
+                  cudaStream_t st) {
+    if (!tc_supported(dtype, m, k, d)) {
+        set_error("tc variant: unsupported shape/dtype");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    const float *xf = static_cast<const float *>(x), *yf = static_cast<const float *>(y);
+    int bn = k >= 128 ? 128 : (k > 32 ? 64 : (k > 16 ? 32 : 16));
+    CUtensorMap mx, mc;
+    int rc = make_map(&mx, xf, m, d, TC_BM);
+    if (rc) return rc;
+    rc = make_map(&mc, yf, k, d, uint32_t(bn));
+    if (rc) return rc;
+    float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 64, st));
+    int32_t *fb_rows = static_cast<int32_t *>(scratch(ctx, SLOT_TC_ROWS, sizeof(int32_t) * (m + 1), st));
+    if (!misc || !fb_rows) return FTK_ERR_CUDA;
+    unsigned *fb_count = reinterpret_cast<unsigned *>(misc + 4);
+    tc_prep_kernel<<<1, 256, 0, st>>>(static_cast<const float *>(yn), k, misc, fb_count);
+    FTK_LAUNCHED("tc_prep_kernel");
+
+    TcParams P{};
+    P.x = xf; P.y = yf; P.yn = static_cast<const float *>(yn);
+    P.m = m; P.k = k; P.d = d;
+    P.nkb = int((d + TC_KB - 1) / TC_KB);
+    P.ntiles = int((k + bn - 1) / bn);
+    const double u = 0x1p-9 + 0x1p-20 + 3.0 * double(d) * 0x1p-24;
+    P.a_coef = float(2.0 * u * (1.0 + 0x1p-10));
+    P.b_coef = float((0x1p-15 + 0x1p-22) * 1.01);
+    P.cmax2 = misc;
+    P.out_idx = out_idx;
+    P.out_val = static_cast<float *>(out_val);
+    P.fb_rows = fb_rows;
+    P.fb_count = fb_count;
+    const int64_t ntm = (m + TC_BM - 1) / TC_BM;
+    switch (bn) {
+        case 16: rc = launch_screen<16>(P, mx, mc, ntm, st); break;
+        case 32: rc = launch_screen<32>(P, mx, mc, ntm, st); break;
+        case 64: rc = launch_screen<64>(P, mx, mc, ntm, st); break;
+        default: rc = launch_screen<128>(P, mx, mc, ntm, st); break;
+    }
+    if (rc) return rc;
+    exact_rows_kernel<float><<<148 * 4, 256, 0, st>>>(xf, yf, static_cast<const float *>(yn), k, d,
+                                                      fb_rows, fb_count, out_idx,
+                                                      static_cast<float *>(out_val));
+    FTK_LAUNCHED("exact_rows_kernel");
+    return FTK_OK;
+}
+
+// fallback-row count of the last tc_assign_run on this context (diagnostics)
+int tc_last_fallback(ftk_ctx *ctx, unsigned *out, cudaStream_t st) {
+    float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 64, st));
+    FTK_CUDA(cudaMemcpyAsync(out, misc + 4, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    FTK_CUDA(cudaStreamSynchronize(st));
+    return FTK_OK;
+}
+
 }  // namespace ftk
