@@ -262,6 +262,91 @@ class _DeviceAssign:
         return report
 
 
+class LloydEngine:
+    """Device-resident Lloyd state: one ``step`` per iteration (assign ->
+    inertia -> label compare -> update -> finalize -> movement) with a single
+    control readback.  ``lloyd`` drives it with the reference's stopping
+    rules; bench.py times exact step counts through it."""
+
+    def __init__(self, x_t, c0, k, dtype, cfg, ft_mode, thr, threads, gemm_hook=NOOP_HOOK,
+                 update_hook=NOOP_HOOK, dist=None):
+        t = E._torch()
+        self.t = t
+        self.dist = dist  # parallel.ShardComm for row-sharded multi-GPU runs
+        self.x_t, self.k, self.dtype, self.cfg = x_t, k, np.dtype(dtype), cfg
+        self.ft_mode = ft_mode
+        self.gemm_hook, self.update_hook = gemm_hook, update_hook
+        m = x_t.shape[0]
+        dev = x_t.device
+        self.xsq = E.row_sq_norms_dev(x_t).to(t.float64)
+        self.sq = t.empty(m, dtype=t.float64, device=dev)
+        self.ctl_f64 = t.zeros(4, dtype=t.float64, device=dev)   # inertia, moved
+        self.ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)     # equal, n_empty, dmr flag
+        self.ctl_host = t.zeros(4, dtype=t.float64).pin_memory()
+        self.ctl_i32_host = t.zeros(8, dtype=t.int32).pin_memory()
+        self.cent = E.to_dev(c0) if not _is_torch(c0) else c0.to(dev).contiguous()
+        self.eps = float(np.finfo(self.dtype).eps)
+        self.A = _DeviceAssign(x_t, m, k, self.dtype, cfg, ft_mode,
+                               thr if ft_mode != "off" else None, threads)
+        self.report = DetectionReport()
+        self.slot = 0
+        self.ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
+        self.assign_ms = 0.0
+        self.update_ms = 0.0
+
+    def step(self, it):
+        """One Lloyd iteration; returns (inertia, unchanged, moved)."""
+        t, A, ev = self.t, self.A, self.ev
+        ev[0].record()
+        yn = E.row_sq_norms_dev(self.cent)
+        inj = A.run(self.cent, yn, self.gemm_hook, it, self.slot)
+        ev[1].record()
+        E.sq_dists_dev(A.md, self.xsq, self.sq)
+        E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
+        if it > 0:
+            E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
+        rep = A.finish(self.gemm_hook, it, inj)
+        if rep is not None:
+            self.report.merge(rep)
+        sums, counts, ev_upd = _update_dev(self.x_t, A.labels[self.slot], self.k, self.dtype,
+                                          self.ft_mode, self.update_hook, it, self.ctl_i32)
+        if self.dist is not None:
+            self.dist.reduce_partials(sums, counts, self.ctl_f64, self.ctl_i32, it)
+        new_cent = E.finalize_dev(sums, counts, self.dtype, n_empty=self.ctl_i32[1:2])
+        E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+        ev[2].record()
+        self.ctl_host.copy_(self.ctl_f64, non_blocking=True)
+        self.ctl_i32_host.copy_(self.ctl_i32, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        if int(self.ctl_i32_host[1]):
+            if self.dist is not None:
+                self.dist.reseed(self.x_t, counts, self.sq, new_cent)
+            else:
+                E.reseed_dev(self.x_t, counts, self.sq, new_cent)  # sq is free after the sum
+            E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+            self.ctl_host.copy_(self.ctl_f64)
+        self.assign_ms = ev[0].elapsed_time(ev[1])
+        self.update_ms = ev[1].elapsed_time(ev[2])
+        self.report.events.extend(ev_upd)
+        unchanged = it > 0 and bool(int(self.ctl_i32_host[0]))
+        self.cent = new_cent
+        self.slot = 1 - self.slot
+        return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
+
+    def final(self, iteration):
+        """Final assignment against the current centroids -> (labels, inertia)."""
+        A = self.A
+        yn = E.row_sq_norms_dev(self.cent)
+        inj = A.run(self.cent, yn, self.gemm_hook, iteration, self.slot)
+        E.sq_dists_dev(A.md, self.xsq, self.sq)
+        E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
+        rep = A.finish(self.gemm_hook, iteration, inj)
+        if rep is not None:
+            self.report.merge(rep)
+        labels = E.to_host(A.labels[self.slot]).astype(np.int64)
+        return labels, max(0.0, float(self.ctl_f64[0].item()))
+
+
 def lloyd(x, config, fault_spec=None):
     """Lloyd's iteration until labels repeat, movement < tol, or max_iters,
     then one final assignment (kmeans.py:210-319)."""
@@ -275,7 +360,7 @@ def lloyd(x, config, fault_spec=None):
     threads = resolve_threads(config.threads)
     cfg = _resolve_tile(config.tile, x, k, config.tune_table)
     thr = config.threshold or Threshold.default_for(dtype)
-    t = E._torch()
+    E._torch()
     gemm_hook, update_hook = _plan_hooks(fault_spec, cfg, m, n, k, config.max_iters, dtype)
 
     timings = {"init_ns": 0, "assign_ns": 0, "update_ns": 0, "total_ns": 0}
@@ -284,74 +369,23 @@ def lloyd(x, config, fault_spec=None):
     c0 = init_centroids(x, k, seed=config.seed, method=config.init)
     timings["init_ns"] = time.perf_counter_ns() - t0
 
-    x_t = E.to_dev(x)
-    dev = x_t.device
-    xsq = E.row_sq_norms_dev(x_t).to(t.float64)
-    sq = t.empty(m, dtype=t.float64, device=dev)
-    ctl_f64 = t.zeros(4, dtype=t.float64, device=dev)    # inertia, moved
-    ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)      # equal, n_empty, dmr flag
-    ctl_host = t.zeros(4, dtype=t.float64).pin_memory()
-    ctl_i32_host = t.zeros(8, dtype=t.int32).pin_memory()
-    cent = E.to_dev(c0)
-    eps = float(np.finfo(dtype).eps)
-    A = _DeviceAssign(x_t, m, k, dtype, cfg, config.ft_mode, thr if config.ft_mode != "off"
-                      else None, threads)
-    report = DetectionReport()
+    eng = LloydEngine(E.to_dev(x), c0, k, dtype, cfg, config.ft_mode, thr, threads, gemm_hook,
+                      update_hook)
     history = []
     converged = False
     iters = 0
-    slot = 0
-    ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
-
     for it in range(config.max_iters):
-        ev[0].record()
-        yn = E.row_sq_norms_dev(cent)
-        inj = A.run(cent, yn, gemm_hook, it, slot)
-        ev[1].record()
-        E.sq_dists_dev(A.md, xsq, sq)
-        E.pairwise_sum_dev(sq, ctl_f64[0:1])
-        if it > 0:
-            E.labels_equal_dev(A.labels[slot], A.labels[1 - slot], ctl_i32[0:1])
-        rep = A.finish(gemm_hook, it, inj)
-        if rep is not None:
-            report.merge(rep)
-        sums, counts, ev_upd = _update_dev(x_t, A.labels[slot], k, dtype, config.ft_mode,
-                                          update_hook, it, ctl_i32)
-        new_cent = E.finalize_dev(sums, counts, dtype, n_empty=ctl_i32[1:2])
-        E.movement_dev(new_cent, cent, eps, ctl_f64[1:2])
-        ev[2].record()
-        ctl_host.copy_(ctl_f64, non_blocking=True)
-        ctl_i32_host.copy_(ctl_i32, non_blocking=True)
-        ev[2].synchronize()
-        t.cuda.current_stream().synchronize()
-        if int(ctl_i32_host[1]):
-            E.reseed_dev(x_t, counts, sq, new_cent)  # sq is free after the inertia sum
-            E.movement_dev(new_cent, cent, eps, ctl_f64[1:2])
-            ctl_host.copy_(ctl_f64)
-        timings["assign_ns"] += int(ev[0].elapsed_time(ev[1]) * 1e6)
-        timings["update_ns"] += int(ev[1].elapsed_time(ev[2]) * 1e6)
-        report.events.extend(ev_upd)
-        history.append(max(0.0, float(ctl_host[0])))
-        unchanged = it > 0 and bool(int(ctl_i32_host[0]))
-        moved = float(ctl_host[1])
+        inertia, unchanged, moved = eng.step(it)
+        timings["assign_ns"] += int(eng.assign_ms * 1e6)
+        timings["update_ns"] += int(eng.update_ms * 1e6)
+        history.append(inertia)
         iters = it + 1
-        cent = new_cent
-        slot = 1 - slot
         if unchanged or moved < config.tol:
             converged = True
             break
-
-    yn = E.row_sq_norms_dev(cent)
-    inj = A.run(cent, yn, gemm_hook, iters, slot)
-    E.sq_dists_dev(A.md, xsq, sq)
-    E.pairwise_sum_dev(sq, ctl_f64[0:1])
-    rep = A.finish(gemm_hook, iters, inj)
-    if rep is not None:
-        report.merge(rep)
-    labels = E.to_host(A.labels[slot]).astype(np.int64)
-    inertia = max(0.0, float(ctl_f64[0].item()))
-    centroids = E.to_host(cent)
+    labels, inertia = eng.final(iters)
+    centroids = E.to_host(eng.cent)
     timings["total_ns"] = time.perf_counter_ns() - t_total
     return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,
-                        converged=converged, report=report, timings=timings,
+                        converged=converged, report=eng.report, timings=timings,
                         inertia_history=history)
