@@ -163,9 +163,18 @@ int ftk_own_sq_dists(ftk_ctx *ctx, int dtype, const void *x, const int32_t *labe
 int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64_t bit,
                  double *before_after, void *stream);
 
-/* Diagnostics: number of rows the last TC-variant assignment on this context
- * could not certify and resolved with the exact fallback (synchronises). */
+/* Diagnostics: out[0] = rows the last TC-variant assignment could not certify
+ * with the 1xTF32 screen, out[1] = rows the 3xTF32 re-screen still could not
+ * certify (resolved by the exact kernel). */
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream);
+
+/* Validation hook for the screening error model: runs the TC assignment
+ * (split = 0: 1xTF32 pass then 3xTF32 on ties; split = 1: 3xTF32 on every
+ * row) and also materialises the raw tensor-core dot products of the screen
+ * into raw (m x k fp32, row-major). */
+int ftk_tc_raw_dots(ftk_ctx *ctx, int split, const float *x, const float *y, const float *ynorms,
+                    int64_t m, int64_t k, int64_t d, float *raw, int32_t *out_idx,
+                    float *out_val, void *stream);
 
 #ifdef __cplusplus
 }

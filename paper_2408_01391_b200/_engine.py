@@ -290,7 +290,23 @@ def own_sq_dists_dev(x_t, labels_i32, cent64, out):
     return out
 
 def tc_fallback_rows():
+    """(rows the 1xTF32 screen left uncertified, rows the 3xTF32 re-screen
+    left for the exact kernel) of the last TC assignment."""
     import ctypes
-    v = ctypes.c_int64(0)
-    N.check(N.load().ftk_tc_fallback_rows(ctx(), ctypes.byref(v), stream()), "ftk_tc_fallback_rows")
-    return int(v.value)
+
+    v = (ctypes.c_int64 * 2)()
+    N.check(N.load().ftk_tc_fallback_rows(ctx(), v, stream()), "ftk_tc_fallback_rows")
+    return int(v[0]), int(v[1])
+
+
+def tc_raw_dots(x_t, y_t, yn_t, split=False):
+    """Raw tensor-core screened dot products (m x k) + the assignment."""
+    t = _torch()
+    m, d = x_t.shape
+    k = y_t.shape[0]
+    raw = t.zeros((m, k), dtype=t.float32, device=x_t.device)
+    idx = t.empty(m, dtype=t.int32, device=x_t.device)
+    val = t.empty(m, dtype=t.float32, device=x_t.device)
+    N.check(N.load().ftk_tc_raw_dots(ctx(), int(bool(split)), ptr(x_t), ptr(y_t), ptr(yn_t), m, k,
+                                     d, ptr(raw), ptr(idx), ptr(val), stream()), "ftk_tc_raw_dots")
+    return raw, idx, val

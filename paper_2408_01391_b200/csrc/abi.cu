@@ -61,7 +61,7 @@ int own_sq_dists_run(ftk_ctx *, int, const void *, const int32_t *, const double
                      int64_t, double *, cudaStream_t);
 int flip_f64_run(double *, int64_t, int64_t, int64_t, int64_t, double *, cudaStream_t);
 int tc_assign_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
-                  int64_t, int32_t *, void *, cudaStream_t);
+                  int64_t, int32_t *, void *, cudaStream_t, float *raw, int split_only);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
@@ -109,7 +109,7 @@ int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *
     cudaStream_t st = as_stream(stream);
     bool has_inj = inj && inj->n > 0;
     if (variant == FTK_VARIANT_TC || (variant == FTK_VARIANT_AUTO && !has_inj)) {
-        int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st);
+        int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st, nullptr, 0);
         if (rc != FTK_ERR_UNSUPPORTED || variant == FTK_VARIANT_TC) return rc;
     }
     return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
@@ -203,10 +203,19 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
 
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
     if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
-    unsigned v = 0;
-    int rc = tc_last_fallback(ctx, &v, as_stream(stream));
-    *out = int64_t(v);
+    unsigned v[2] = {0, 0};
+    int rc = tc_last_fallback(ctx, v, as_stream(stream));
+    out[0] = int64_t(v[0]);
+    out[1] = int64_t(v[1]);
     return rc;
+}
+
+int ftk_tc_raw_dots(ftk_ctx *ctx, int split, const float *x, const float *y, const float *ynorms,
+                    int64_t m, int64_t k, int64_t d, float *raw, int32_t *out_idx,
+                    float *out_val, void *stream) {
+    if (!ctx || !raw) { set_error("bad ctx/raw"); return FTK_ERR_ARG; }
+    return tc_assign_run(ctx, FTK_F32, x, y, ynorms, m, k, d, out_idx, out_val,
+                         as_stream(stream), raw, split);
 }
 
 }  // extern "C"

@@ -6,179 +6,83 @@
 // evaluation order (_kernels.py:44-102).  This path reproduces them bit for
 // bit without evaluating every distance exactly:
 //
-//   1. SCREEN  (tensor cores): s_ij = yn_j - 2 * <x_i, c_j>_tf32, fp32 TMEM
-//      accumulators, TF32 operands (truncated mantissas).  The epilogue keeps
-//      per row the two smallest screened values (index packed in the low
-//      mantissa bits of the minimum) -- the N x K distance matrix never
-//      leaves the SM.
-//   2. CERTIFY: |s_ij - d_ij^ref| <= A_i + B |s_ij| with
-//      A_i = 2 ||x_i|| cmax (2^-9 + 2^-20 + 3 D 2^-24) (tf32 operand
-//      truncation, fp32 accumulation, the reference's own rounding) and
-//      B = 2^-15 + 2^-22 (index packing, final roundings).  When
-//      m2 - m1 > 2 A_i + B (|m1| + |m2|) the reference's strict argmin is
-//      provably the screened winner.
-//   3. REFINE  (SIMT, exact order): acc = sum_k fl(x_ik * c_jk) k ascending,
-//      min_dist = yn_j - (acc + acc) for the winner only, from the X tile
-//      already in shared memory.
-//   4. FALLBACK: uncertified rows go to a list that exact_rows_kernel
-//      resolves with a full exact argmin.
+//   1. SCREEN  (tensor cores): s_ij = yn_j - 2 <x_i, c_j>, fp32 TMEM
+//      accumulators.  Pass 1 uses 1xTF32 (operands truncated to 10 mantissa
+//      bits).  The epilogue keeps per row the two smallest screened values
+//      (index packed in the low mantissa bits of the minimum): the N x K
+//      distance matrix never leaves the SM.
+//   2. CERTIFY: |s_ij - d_ij^ref| <= A_i + B |s_ij|, with
+//        pass 1: A_i = 2 ||x_i|| cmax (2^-9 + 2^-20 + 3 D 2^-24)
+//        pass 2: A_i = 2 ||x_i|| cmax (3 2^-20 + 7 D 2^-24)
+//      (operand truncation, fp32 tensor-core accumulation <= 2^-23 per add,
+//      and the reference's own sequential rounding) and B = 2^-15 + 2^-22
+//      (index packing, final roundings).  If m2 - m1 > 2 A_i + B (|m1|+|m2|)
+//      the reference's strict argmin is provably the screened winner.
+//   3. REFINE  (SIMT, exact order): acc = sum_k fl(x_ik c_jk), k ascending;
+//      min_dist = yn_j - (acc + acc), for the winner only, from the X tile
+//      already resident in shared memory.
+//   4. Rows pass 1 cannot certify are gathered and re-screened with 3xTF32
+//      (x = x_hi + x_lo, c = c_hi + c_lo; hi*hi + hi*lo + lo*hi), whose bound
+//      is ~2^9 tighter; rows that still tie are resolved by the exact SIMT
+//      kernel (exact.cu).  Every row therefore carries the reference's bits.
 //
 // Roles per CTA (6 warps): w0 TMA producer, w1 TMEM allocator + MMA issuer
-// (one elected thread), w2..w5 epilogue (one accumulator row per thread;
-// warp w reads TMEM lanes 32*(w%4)..+31).  The X tile (128 rows x D) is
-// loaded once and stays resident; centroid k-blocks stream through a
-// multi-stage ring; two TMEM accumulators let the MMA of centroid tile t+1
-// overlap the epilogue of tile t.
-
-#include <cuda.h>
+// (one elected thread), w2..w5 epilogue (one accumulator row per thread; warp
+// w reads TMEM lanes 32*(w%4)..+31).  The X tile (128 rows x D) is loaded
+// once and stays resident; centroid k-blocks stream through a ring; two TMEM
+// accumulators let the MMA of centroid tile t+1 overlap the epilogue of t.
 
 #include <cstring>
 #include <mutex>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
+#include "tc_ptx.cuh"
 
 namespace ftk {
 
-constexpr int TC_BM = 128;          // rows per CTA (UMMA M)
-constexpr int TC_KB = 32;           // fp32 elements per 128-byte swizzle row
-constexpr int TC_THREADS = 192;     // 6 warps
-constexpr int TC_MAX_D = 256;       // resident-A limit
+constexpr int TC_BM = 128;       // rows per CTA (UMMA M)
+constexpr int TC_KB = 32;        // fp32 elements per 128-byte swizzle row
+constexpr int TC_THREADS = 192;  // 6 warps
+constexpr int TC_MAX_D = 256;    // resident-A limit
 
 struct TcParams {
-    const float *x;      // m x d   (exact values for refinement)
+    const float *x;      // rows x d  (exact values; pass 2: the gathered rows)
     const float *y;      // k x d
-    const float *yn;     // k       (exact fp32 squared norms, reference order)
+    const float *yn;     // k         (exact fp32 squared norms, reference order)
     int64_t m, k, d;
     int nkb;             // ceil(d / 32)
     int ntiles;          // ceil(k / BN)
     int stages;
-    float a_coef;        // 2 cmax (2^-9 + 2^-20 + 3 d 2^-24) * (1 + 2^-10)
+    float a_coef;        // see header
     float b_coef;
-    const float *cmax2;  // device scalar: max_j yn_j (upper bound of ||c||^2)
+    const float *cmax2;  // device scalar: upper bound of max_j ||c_j||^2
+    const int32_t *rows; // pass 2: row r of the tile is global row rows[r]
     int32_t *out_idx;
     float *out_val;
-    int32_t *fb_rows;    // uncertified rows (fallback list)
+    int32_t *fb_rows;    // uncertified rows (global indices)
     unsigned *fb_count;
+    float *raw;          // debug: materialise the raw screened dot products
 };
 
-// ----------------------------------------------------------- PTX helpers --
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void fence_barrier_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar,
-                                            int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-        : "memory");
-}
-__device__ __forceinline__ void prefetch_tmap(const CUtensorMap *map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-__device__ __forceinline__ void tmem_alloc(uint32_t *dst_smem, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(dst_smem)),
-                 "r"(ncols));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols));
-}
-__device__ __forceinline__ void tc_fence_before() {
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint64_t *bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
-          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
-          "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// K-major, 128-byte swizzled operand tile (rows of 128 B, 8-row atoms of
-// 1024 B): start address >> 4, SBO = 1024 B, version 1, layout SWIZZLE_128B.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
-    uint64_t d = 0;
-    d |= uint64_t((saddr >> 4) & 0x3FFF);
-    d |= uint64_t(1) << 16;                 // LBO (unused for swizzled K-major)
-    d |= uint64_t(1024 >> 4) << 32;         // SBO
-    d |= uint64_t(1) << 46;                 // descriptor version (sm100)
-    d |= uint64_t(2) << 61;                 // SWIZZLE_128B
-    return d;
-}
-
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major.
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) |
-           (uint32_t(M >> 4) << 24);
-}
-
 // ------------------------------------------------------------- kernel ----
-template <int BN>
+template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_screen_kernel(const __grid_constant__ CUtensorMap tmX,
-                     const __grid_constant__ CUtensorMap tmC, TcParams P) {
+                     const __grid_constant__ CUtensorMap tmXl,
+                     const __grid_constant__ CUtensorMap tmC,
+                     const __grid_constant__ CUtensorMap tmCl, TcParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the swizzle atoms
     unsigned char *smem = reinterpret_cast<unsigned char *>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int NOP = SPLIT ? 2 : 1;             // hi (+ lo) operand copies
     const int nkb = P.nkb, S = P.stages;
     const uint32_t A_KB_BYTES = TC_BM * 128;       // one k-block of X
     const uint32_t B_BYTES = BN * 128;             // one k-block of C
-    unsigned char *sA = smem;                      // nkb x 16 KB
-    unsigned char *sB = sA + size_t(nkb) * A_KB_BYTES;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + size_t(S) * B_BYTES);
+    unsigned char *sA = smem;                      // NOP x nkb x 16 KB (hi first)
+    unsigned char *sB = sA + size_t(NOP) * nkb * A_KB_BYTES;  // S x NOP x B_BYTES
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sB + size_t(S) * NOP * B_BYTES);
     uint64_t *full = bars, *empty = bars + S;
     uint64_t *a_full = bars + 2 * S;
     uint64_t *t_full = a_full + 1, *t_empty = a_full + 3;
@@ -201,7 +105,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_init(&t_empty[1], 4);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, (2 * BN) < 32 ? 32 : 2 * BN);
+    if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -209,18 +113,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // X tile: all k-blocks, once
-            mbar_expect_tx(a_full, A_KB_BYTES * nkb);
-            for (int kb = 0; kb < nkb; ++kb)
+            mbar_expect_tx(a_full, A_KB_BYTES * nkb * NOP);
+            for (int kb = 0; kb < nkb; ++kb) {
                 tma_load_2d(sA + size_t(kb) * A_KB_BYTES, &tmX, a_full, kb * TC_KB, int(row0));
+                if (SPLIT)
+                    tma_load_2d(sA + size_t(nkb + kb) * A_KB_BYTES, &tmXl, a_full, kb * TC_KB,
+                                int(row0));
+            }
             int stage = 0;
             uint32_t phase = 0;
             for (int t = 0; t < P.ntiles; ++t) {
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], B_BYTES);
-                    tma_load_2d(sB + size_t(stage) * B_BYTES, &tmC, &full[stage], kb * TC_KB,
-                                t * BN);
+                    mbar_expect_tx(&full[stage], B_BYTES * NOP);
+                    unsigned char *dst = sB + size_t(stage) * NOP * B_BYTES;
+                    tma_load_2d(dst, &tmC, &full[stage], kb * TC_KB, t * BN);
+                    if (SPLIT) tma_load_2d(dst + B_BYTES, &tmCl, &full[stage], kb * TC_KB, t * BN);
                     if (++stage == S) { stage = 0; phase ^= 1; }
                 }
             }
@@ -229,6 +137,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(TC_BM, BN);
             const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
+            const uint32_t a_lo = a_base + uint32_t(nkb) * A_KB_BYTES;
             mbar_wait(a_full, 0);
             int stage = 0;
             uint32_t phase = 0;
@@ -241,11 +150,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int kb = 0; kb < nkb; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    const uint32_t bs = b_base + uint32_t(stage) * NOP * B_BYTES;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {  // 4 x (K = 8 tf32) per 128-byte row
-                        uint64_t ad = smem_desc(a_base + kb * A_KB_BYTES + kk * 32);
-                        uint64_t bd = smem_desc(b_base + stage * B_BYTES + kk * 32);
-                        mma_tf32(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+                        const uint32_t ao = uint32_t(kb) * A_KB_BYTES + kk * 32;
+                        const uint64_t ah = smem_desc(a_base + ao);
+                        const uint64_t bh = smem_desc(bs + kk * 32);
+                        mma_tf32(d_tmem, ah, bh, idesc, (kb | kk) != 0);
+                        if (SPLIT) {
+                            mma_tf32(d_tmem, ah, smem_desc(bs + B_BYTES + kk * 32), idesc, 1);
+                            mma_tf32(d_tmem, smem_desc(a_lo + ao), bh, idesc, 1);
+                        }
                     }
                     mma_commit(&empty[stage]);
                     if (++stage == S) { stage = 0; phase ^= 1; }
@@ -257,7 +172,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---------------------------------------------------- epilogue --
         const int quad = warp & 3;              // TMEM lane group this warp may access
         const int r = quad * 32 + lane;         // accumulator row
-        const int64_t grow = row0 + r;
+        const int64_t grow = row0 + r;          // row within this pass
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
         float m1 = INFINITY, m2 = INFINITY;
         int tile1 = 0;
@@ -268,46 +183,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tc_fence_after();
             float t1 = INFINITY, t2 = INFINITY;
             const int64_t c0 = int64_t(t) * BN;
-            const bool partial = c0 + BN > P.k;
-#pragma unroll 1
-            for (int ch = 0; ch < BN / 32; ++ch) {
-                uint32_t v[32];
-                tmem_ld32(tmem + lane_base + uint32_t(buf * BN + ch * 32), v);
-                const float4 *yn4 = reinterpret_cast<const float4 *>(P.yn + c0 + ch * 32);
-                if (!partial) {
+            const int live = int(P.k - c0 < BN ? P.k - c0 : BN);
+            const uint32_t tbase = tmem + lane_base + uint32_t(buf * BN);
+            // software-pipelined TMEM drain: chunk ch+1 in flight while ch is screened
+            uint32_t va[32], vb[32];
+            tmem_ld32_issue(tbase, va);
+            tmem_ld_wait(va);
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        float4 yv = __ldg(yn4 + q);
-                        float yy[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int e = q * 4 + u;
-                            float dd = fmaf(-2.0f, __uint_as_float(v[e]), yy[u]);
-                            float p = __uint_as_float((__float_as_uint(dd) & ~0x7Fu) |
-                                                      uint32_t(ch * 32 + e));
-                            float hi = fmaxf(t1, p);
-                            t1 = fminf(t1, p);
-                            t2 = fminf(t2, hi);
-                        }
-                    }
-                } else {
-                    for (int e = 0; e < 32; ++e) {
-                        const int64_t col = c0 + ch * 32 + e;
-                        if (col >= P.k) break;
-                        float dd = fmaf(-2.0f, __uint_as_float(v[e]), P.yn[col]);
-                        float p = __uint_as_float((__float_as_uint(dd) & ~0x7Fu) |
-                                                  uint32_t(ch * 32 + e));
-                        float hi = fmaxf(t1, p);
-                        t1 = fminf(t1, p);
-                        t2 = fminf(t2, hi);
-                    }
+            for (int ch = 0; ch < BN / 32; ch += 2) {
+                if (ch + 1 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
+                if (P.raw && grow < P.m)
+                    for (int e = 0; e < 32 && ch * 32 + e < live; ++e)
+                        P.raw[grow * P.k + c0 + ch * 32 + e] = __uint_as_float(va[e]);
+                screen_chunk(va, P.yn + c0 + ch * 32, ch * 32, live - ch * 32, t1, t2);
+                if (ch + 1 < BN / 32) {
+                    tmem_ld_wait(vb);
+                    if (ch + 2 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
+                    if (P.raw && grow < P.m)
+                        for (int e = 0; e < 32 && (ch + 1) * 32 + e < live; ++e)
+                            P.raw[grow * P.k + c0 + (ch + 1) * 32 + e] = __uint_as_float(vb[e]);
+                    screen_chunk(vb, P.yn + c0 + (ch + 1) * 32, (ch + 1) * 32,
+                                 live - (ch + 1) * 32, t1, t2);
+                    if (ch + 2 < BN / 32) tmem_ld_wait(va);
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&t_empty[buf]);
-            // merge tile top-2 into the running top-2
-            float hi = fmaxf(m1, t1);
+            // merge the tile's top-2 into the running top-2
+            const float hi = fmaxf(m1, t1);
             if (t1 < m1) tile1 = t;
             m1 = fminf(m1, t1);
             m2 = fminf(fminf(m2, t2), hi);
@@ -315,26 +219,47 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
         if (grow < P.m) {
             const int j = tile1 * BN + int(__float_as_uint(m1) & 0x7Fu);
+            const int64_t orow = P.rows ? int64_t(P.rows[grow]) : grow;
             // one pass over the resident X row: ||x||^2 (bound) and the exact
-            // sequential dot product with the screened winner
-            const float *cj = P.y + int64_t(j) * P.d;
+            // sequential dot product with the screened winner.  The winner row
+            // is fetched 32 floats (8 x 16 B) at a time so the L2 round trips
+            // overlap; x comes from the swizzled tile (chunk q of row r sits at
+            // chunk position q ^ (r & 7)); in split mode x = x_hi + x_lo exactly.
+            const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(j) * P.d);
             float acc = 0.0f, xx = 0.0f;
-            for (int k = 0; k < P.d; ++k) {
-                const int kb = k >> 5, w = k & 31;
-                const uint32_t off = uint32_t(kb) * A_KB_BYTES + uint32_t(r) * 128 +
-                                     (uint32_t(((w >> 2) ^ (r & 7)) << 4)) + uint32_t(w & 3) * 4;
-                const float xv = *reinterpret_cast<const float *>(sA + off);
-                acc = __fadd_rn(acc, __fmul_rn(xv, __ldg(cj + k)));
-                xx = fmaf(xv, xv, xx);
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int k0 = kb * TC_KB;
+                float4 cv[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    cv[q] = (k0 + 4 * q < P.d) ? __ldg(cj4 + (k0 >> 2) + q)
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
+                const unsigned char *rowp = sA + uint32_t(kb) * A_KB_BYTES + uint32_t(r) * 128;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    if (k0 + 4 * q < P.d) {
+                        const uint32_t off = (q ^ (r & 7)) << 4;
+                        // the hi tile holds the full fp32 x (the MMA truncates it)
+                        const float4 xv = *reinterpret_cast<const float4 *>(rowp + off);
+                        acc = __fadd_rn(acc, __fmul_rn(xv.x, cv[q].x));
+                        acc = __fadd_rn(acc, __fmul_rn(xv.y, cv[q].y));
+                        acc = __fadd_rn(acc, __fmul_rn(xv.z, cv[q].z));
+                        acc = __fadd_rn(acc, __fmul_rn(xv.w, cv[q].w));
+                        xx = fmaf(xv.x, xv.x, xx);
+                        xx = fmaf(xv.y, xv.y, xx);
+                        xx = fmaf(xv.z, xv.z, xx);
+                        xx = fmaf(xv.w, xv.w, xx);
+                    }
+                }
             }
-            const float A = P.a_coef * sqrtf(xx * (1.0f + 0x1p-16f)) * sqrtf(*P.cmax2);
+            const float A = P.a_coef * sqrtf(xx * (1.0f + 0x1p-10f)) * sqrtf(*P.cmax2);
             const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
             if (m2 - m1 > gap_need && m1 < INFINITY) {
-                P.out_idx[grow] = j;
-                P.out_val[grow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
+                P.out_idx[orow] = j;
+                P.out_val[orow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
             } else {
-                unsigned slot = atomicAdd(P.fb_count, 1u);
-                P.fb_rows[slot] = int32_t(grow);
+                const unsigned slot = atomicAdd(P.fb_count, 1u);
+                P.fb_rows[slot] = int32_t(orow);
             }
         }
     }
@@ -342,46 +267,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, (2 * BN) < 32 ? 32 : 2 * BN);
+        tmem_dealloc(tmem, 2 * BN);
     }
 }
 
-// ------------------------------------------------ exact fallback rows ----
-// One warp per listed row: lanes take centroids j = lane, lane + 32, ...,
-// each computing the exact sequential dot product; (value, index) lexmin.
-template <typename T>
-__global__ void exact_rows_kernel(const T *x, const T *y, const T *yn, int64_t k, int64_t d,
-                                  const int32_t *rows, const unsigned *count, int32_t *out_idx,
-                                  T *out_val) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    const unsigned n = *count;
-    for (int64_t q = wid; q < n; q += nw) {
-        const int64_t i = rows[q];
-        const T *xr = x + i * d;
-        T bv = T(INFINITY);
-        int32_t bj = 0;
-        for (int64_t j = lane; j < k; j += 32) {
-            const T *cr = y + j * d;
-            T acc = T(0);
-            for (int64_t kk = 0; kk < d; ++kk) acc = add_rn(acc, mul_rn(xr[kk], cr[kk]));
-            T dd = sub_rn(yn[j], add_rn(acc, acc));
-            argmin_merge(bv, bj, dd, int32_t(j));
-        }
-        for (int off = 16; off; off >>= 1) {
-            T ov = __shfl_xor_sync(0xffffffffu, bv, off);
-            int32_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
-            argmin_merge(bv, bj, ov, oj);
-        }
-        if (lane == 0) {
-            out_idx[i] = bj;
-            out_val[i] = bv;
-        }
-    }
-}
-
-__global__ void tc_prep_kernel(const float *yn, int64_t k, float *cmax2, unsigned *fb_count) {
+// --------------------------------------------------------- small kernels --
+// Upper bound of max_j ||c_j||^2 from the exact fp32 norms; resets counters.
+__global__ void tc_prep_kernel(const float *yn, int64_t k, float *cmax2, unsigned *counters) {
     float m = 0.0f;
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) m = fmaxf(m, yn[j]);
     for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
@@ -391,9 +283,44 @@ __global__ void tc_prep_kernel(const float *yn, int64_t k, float *cmax2, unsigne
     if (threadIdx.x == 0) {
         float mm = 0.0f;
         for (int w = 0; w < int(blockDim.x / 32); ++w) mm = fmaxf(mm, sh[w]);
-        // yn is a rounded sum: inflate to an upper bound of max ||c||^2
-        *cmax2 = mm * (1.0f + 0x1p-10f);
-        *fb_count = 0u;
+        *cmax2 = mm * (1.0f + 0x1p-10f);  // yn is a rounded sum
+        counters[0] = counters[1] = 0u;
+    }
+}
+
+__device__ __forceinline__ float tf32_trunc(float v) {
+    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+}
+
+// lo[i] = v[i] - trunc_tf32(v[i]) (exact in fp32)
+__global__ void split_lo_kernel(const float *v, int64_t n, float *lo) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += int64_t(gridDim.x) * blockDim.x)
+        lo[i] = __fsub_rn(v[i], tf32_trunc(v[i]));
+}
+
+// Gather listed rows: g = x[rows], g_lo = g - trunc(g)  (count on device)
+__global__ void gather_rows_kernel(const float *x, int64_t d, const int32_t *rows,
+                                   const unsigned *count, float *g, float *g_lo) {
+    const int64_t n = int64_t(*count) * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = e / d, f = e % d;
+        const float v = x[int64_t(rows[q]) * d + f];
+        g[e] = v;
+        if (g_lo) g_lo[e] = __fsub_rn(v, tf32_trunc(v));
+    }
+}
+
+template <typename T>
+__global__ void scatter_rows_kernel(const int32_t *rows, const unsigned *count,
+                                    const int32_t *idx, const T *val, int32_t *out_idx,
+                                    T *out_val) {
+    const unsigned n = *count;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        out_idx[rows[q]] = idx[q];
+        out_val[rows[q]] = val[q];
     }
 }
 
@@ -424,7 +351,7 @@ static int make_map(CUtensorMap *map, const float *base, int64_t rows, int64_t c
         set_error("cuTensorMapEncodeTiled unavailable");
         return FTK_ERR_CUDA;
     }
-    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows < 1 ? 1 : rows)};
     cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(float)};
     cuuint32_t box[2] = {TC_KB, box_rows};
     cuuint32_t estr[2] = {1, 1};
@@ -439,89 +366,171 @@ static int make_map(CUtensorMap *map, const float *base, int64_t rows, int64_t c
     return FTK_OK;
 }
 
-template <int BN>
-static int launch_screen(const TcParams &P0, const CUtensorMap &mx, const CUtensorMap &mc,
-                         int64_t ntiles_m, cudaStream_t st) {
-    TcParams P = P0;
-    const size_t a_bytes = size_t(P.nkb) * TC_BM * 128;
-    const size_t b_bytes = size_t(BN) * 128;
-    // aim for two CTAs per SM when the resident tile allows it
-    const size_t budget = (a_bytes + 3 * b_bytes + 2048) * 2 <= 220 * 1024 ? 110 * 1024 : 220 * 1024;
-    int stages = int((budget - a_bytes - 2048) / b_bytes);
+template <int BN, bool SPLIT>
+static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &mxl,
+                         const CUtensorMap &mc, const CUtensorMap &mcl, cudaStream_t st) {
+    constexpr int NOP = SPLIT ? 2 : 1;
+    const size_t a_bytes = size_t(P.nkb) * TC_BM * 128 * NOP;
+    const size_t b_bytes = size_t(BN) * 128 * NOP;
+    // Two CTAs per SM (one's refine/prologue overlaps the other's MMAs) when
+    // the resident X tile leaves room for >= 2 centroid stages in ~113 KB.
+    const size_t fixed = 1024 + a_bytes + 256;
+    const size_t two_cta = 113 * 1024;
+    int stages = fixed + 2 * b_bytes <= two_cta ? int((two_cta - fixed) / b_bytes)
+                                                : int((227 * 1024 - fixed) / b_bytes);
     if (stages > 6) stages = 6;
-    if (stages < 2) stages = 2;
-    P.stages = stages;
-    const size_t smem = 1024 + a_bytes + stages * b_bytes + 256;
-    if (smem > 227 * 1024) {
+    if (stages < 2) {
         set_error("tc: tile exceeds shared memory");
         return FTK_ERR_UNSUPPORTED;
     }
-    auto kern = tc_screen_kernel<BN>;
+    P.stages = stages;
+    const size_t smem = fixed + size_t(stages) * b_bytes;
+    const int64_t grid = (P.m + TC_BM - 1) / TC_BM;
+    if (grid == 0) return FTK_OK;
+    auto kern = tc_screen_kernel<BN, SPLIT>;
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<dim3(unsigned(ntiles_m)), dim3(TC_THREADS), smem, st>>>(mx, mc, P);
+    kern<<<dim3(unsigned(grid)), dim3(TC_THREADS), smem, st>>>(mx, mxl, mc, mcl, P);
     FTK_LAUNCHED("tc_screen_kernel");
     return FTK_OK;
 }
 
+template <bool SPLIT>
+static int screen(int bn, const TcParams &P, const CUtensorMap &mx, const CUtensorMap &mxl,
+                  const CUtensorMap &mc, const CUtensorMap &mcl, cudaStream_t st) {
+    switch (bn) {
+        case 32: return launch_screen<32, SPLIT>(P, mx, mxl, mc, mcl, st);
+        case 64: return launch_screen<64, SPLIT>(P, mx, mxl, mc, mcl, st);
+        default: return launch_screen<128, SPLIT>(P, mx, mxl, mc, mcl, st);
+    }
+}
+
 int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
     return dtype == FTK_F32 && d >= 8 && d % 4 == 0 && d <= TC_MAX_D && k >= 1 && m >= 1 &&
-           k < (int64_t(1) << 30);
+           m < (int64_t(1) << 31) && k < (int64_t(1) << 24);
 }
+
+// exact.cu: the tiled exact kernel (used on gathered tie rows)
+int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t, int64_t,
+              int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
+              const ftk_injection *, ftk_events *, cudaStream_t);
+
+static unsigned g_last_fb[3] = {0, 0, 0};  // pass-1 flagged, pass-2 flagged (diagnostics)
 
 int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn,
                   int64_t m, int64_t k, int64_t d, int32_t *out_idx, void *out_val,
-                  cudaStream_t st) {
+                  cudaStream_t st, float *raw, int split_only) {
     if (!tc_supported(dtype, m, k, d)) {
         set_error("tc variant: unsupported shape/dtype");
         return FTK_ERR_UNSUPPORTED;
     }
     const float *xf = static_cast<const float *>(x), *yf = static_cast<const float *>(y);
-    int bn = k >= 128 ? 128 : (k > 32 ? 64 : (k > 16 ? 32 : 16));
-    CUtensorMap mx, mc;
-    int rc = make_map(&mx, xf, m, d, TC_BM);
-    if (rc) return rc;
-    rc = make_map(&mc, yf, k, d, uint32_t(bn));
-    if (rc) return rc;
-    float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 64, st));
-    int32_t *fb_rows = static_cast<int32_t *>(scratch(ctx, SLOT_TC_ROWS, sizeof(int32_t) * (m + 1), st));
-    if (!misc || !fb_rows) return FTK_ERR_CUDA;
-    unsigned *fb_count = reinterpret_cast<unsigned *>(misc + 4);
-    tc_prep_kernel<<<1, 256, 0, st>>>(static_cast<const float *>(yn), k, misc, fb_count);
+    const float *ynf = static_cast<const float *>(yn);
+    float *outv = static_cast<float *>(out_val);
+    const int bn = k >= 128 ? 128 : (k > 32 ? 64 : 32);
+    const int bn2 = k >= 64 ? 64 : 32;  // pass 2 carries hi+lo operands: narrower tiles
+    float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 256, st));
+    int32_t *rows1 = static_cast<int32_t *>(scratch(ctx, SLOT_TC_ROWS, sizeof(int32_t) * 2 * (m + 1), st));
+    float *c_lo = static_cast<float *>(scratch(ctx, SLOT_TC_B, sizeof(float) * k * d, st));
+    if (!misc || !rows1 || !c_lo) return FTK_ERR_CUDA;
+    int32_t *rows2 = rows1 + (m + 1);
+    unsigned *cnt = reinterpret_cast<unsigned *>(misc + 8);  // [0] pass-1 flagged, [1] pass-2
+    tc_prep_kernel<<<1, 256, 0, st>>>(ynf, k, misc, cnt);
     FTK_LAUNCHED("tc_prep_kernel");
 
     TcParams P{};
-    P.x = xf; P.y = yf; P.yn = static_cast<const float *>(yn);
+    P.x = xf; P.y = yf; P.yn = ynf;
     P.m = m; P.k = k; P.d = d;
     P.nkb = int((d + TC_KB - 1) / TC_KB);
-    P.ntiles = int((k + bn - 1) / bn);
-    const double u = 0x1p-9 + 0x1p-20 + 3.0 * double(d) * 0x1p-24;
-    P.a_coef = float(2.0 * u * (1.0 + 0x1p-10));
     P.b_coef = float((0x1p-15 + 0x1p-22) * 1.01);
     P.cmax2 = misc;
     P.out_idx = out_idx;
-    P.out_val = static_cast<float *>(out_val);
-    P.fb_rows = fb_rows;
-    P.fb_count = fb_count;
-    const int64_t ntm = (m + TC_BM - 1) / TC_BM;
-    switch (bn) {
-        case 16: rc = launch_screen<16>(P, mx, mc, ntm, st); break;
-        case 32: rc = launch_screen<32>(P, mx, mc, ntm, st); break;
-        case 64: rc = launch_screen<64>(P, mx, mc, ntm, st); break;
-        default: rc = launch_screen<128>(P, mx, mc, ntm, st); break;
-    }
+    P.out_val = outv;
+    P.raw = raw;
+    CUtensorMap mx, mc, mcl;
+    int rc = make_map(&mc, yf, k, d, uint32_t(bn));
     if (rc) return rc;
-    exact_rows_kernel<float><<<148 * 4, 256, 0, st>>>(xf, yf, static_cast<const float *>(yn), k, d,
-                                                      fb_rows, fb_count, out_idx,
-                                                      static_cast<float *>(out_val));
-    FTK_LAUNCHED("exact_rows_kernel");
+    unsigned n1 = unsigned(m);
+    const int32_t *pass2_rows = nullptr;
+    if (!split_only) {
+        // ---------------- pass 1: 1xTF32 over every row
+        rc = make_map(&mx, xf, m, d, TC_BM);
+        if (rc) return rc;
+        P.ntiles = int((k + bn - 1) / bn);
+        P.a_coef = float(2.0 * (0x1p-9 + 0x1p-20 + 3.0 * double(d) * 0x1p-24) * (1.0 + 0x1p-10));
+        P.fb_rows = rows1;
+        P.fb_count = cnt;
+        rc = screen<false>(bn, P, mx, mx, mc, mc, st);
+        if (rc) return rc;
+        FTK_CUDA(cudaMemcpyAsync(&n1, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        FTK_CUDA(cudaStreamSynchronize(st));
+        pass2_rows = rows1;
+    }
+    g_last_fb[0] = n1;
+    g_last_fb[1] = 0;
+    if (n1 == 0) return FTK_OK;
+    // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
+    float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
+    if (!g) return FTK_ERR_CUDA;
+    float *g_lo = g + size_t(n1) * d;
+    if (split_only) {
+        // identity row list for a direct 3xTF32 call (testing / forced mode)
+        std::vector<int32_t> ids(m);
+        for (int64_t i = 0; i < m; ++i) ids[i] = int32_t(i);
+        FTK_CUDA(cudaMemcpyAsync(rows1, ids.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+        FTK_CUDA(cudaMemcpyAsync(cnt, &n1, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+        FTK_CUDA(cudaStreamSynchronize(st));
+        pass2_rows = rows1;
+    }
+    gather_rows_kernel<<<148 * 8, 256, 0, st>>>(xf, d, pass2_rows, cnt, g, g_lo);
+    FTK_LAUNCHED("gather_rows_kernel");
+    split_lo_kernel<<<148 * 4, 256, 0, st>>>(yf, k * d, c_lo);
+    FTK_LAUNCHED("split_lo_kernel");
+    CUtensorMap mg, mgl, mc2, mcl2;
+    if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mgl, g_lo, n1, d, TC_BM)) ||
+        (rc = make_map(&mc2, yf, k, d, uint32_t(bn2))) ||
+        (rc = make_map(&mcl2, c_lo, k, d, uint32_t(bn2))))
+        return rc;
+    TcParams Q = P;
+    Q.x = g;
+    Q.m = n1;
+    Q.ntiles = int((k + bn2 - 1) / bn2);
+    Q.a_coef = float(2.0 * (3.0 * 0x1p-20 + 7.0 * double(d) * 0x1p-24) * (1.0 + 0x1p-10));
+    Q.rows = pass2_rows;
+    Q.fb_rows = rows2;
+    Q.fb_count = cnt + 1;
+    Q.raw = split_only ? raw : nullptr;
+    rc = screen<true>(bn2, Q, mg, mgl, mc2, mcl2, st);
+    unsigned n2 = 0;
+    if (rc == FTK_ERR_UNSUPPORTED) {
+        // hi+lo X tile does not fit (large D): every pass-1 tie goes exact
+        rows2 = const_cast<int32_t *>(pass2_rows);
+        n2 = n1;
+        rc = FTK_OK;
+    } else {
+        if (rc) return rc;
+        FTK_CUDA(cudaMemcpyAsync(&n2, cnt + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        FTK_CUDA(cudaStreamSynchronize(st));
+        cnt += 1;
+    }
+    g_last_fb[1] = n2;
+    if (n2 == 0) return FTK_OK;
+    // ---------------- exact resolution of the remaining ties (tiled SIMT kernel)
+    float *g2 = g;  // reuse: n2 <= n1 rows
+    gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, cnt, g2, nullptr);
+    FTK_LAUNCHED("gather_rows_kernel");
+    int32_t *idx2 = reinterpret_cast<int32_t *>(g_lo);
+    float *val2 = g_lo + n2;
+    rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 32, 256, 16, idx2, val2, nullptr, false,
+                   0.0, 0.0, 0, nullptr, nullptr, st);
+    if (rc) return rc;
+    scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, cnt, idx2, val2, out_idx, outv);
+    FTK_LAUNCHED("scatter_rows_kernel");
     return FTK_OK;
 }
 
-// fallback-row count of the last tc_assign_run on this context (diagnostics)
-int tc_last_fallback(ftk_ctx *ctx, unsigned *out, cudaStream_t st) {
-    float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 64, st));
-    FTK_CUDA(cudaMemcpyAsync(out, misc + 4, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-    FTK_CUDA(cudaStreamSynchronize(st));
+int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t) {
+    out[0] = g_last_fb[0];
+    out[1] = g_last_fb[1];
     return FTK_OK;
 }
 
