@@ -64,6 +64,9 @@ enum ScratchSlot {
     SLOT_TC_ROWS = 9,
     SLOT_TC_MISC = 10,
     SLOT_INJ = 11,
+    SLOT_SEG_BASE = 12,
+    SLOT_SEG_PART = 13,
+    SLOT_SEG_FB = 14,
 };
 
 // ------------------------------------------------------- float helpers --

@@ -32,6 +32,7 @@
 // once and stays resident; centroid k-blocks stream through a ring; two TMEM
 // accumulators let the MMA of centroid tile t+1 overlap the epilogue of t.
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -55,15 +56,18 @@ struct TcParams {
     int nkb;             // ceil(d / 32)
     int ntiles;          // ceil(k / BN)
     int stages;
+    int abufs;           // resident X tile buffers (2: next tile prefetched)
     float a_coef;        // see header
     float b_coef;
     const float *cmax2;  // device scalar: upper bound of max_j ||c_j||^2
+    const float *ecmax2; // device scalar: upper bound of max_j ||c_j - tf32(c_j)||^2
     const int32_t *rows; // pass 2: row r of the tile is global row rows[r]
     int32_t *out_idx;
     float *out_val;
     int32_t *fb_rows;    // uncertified rows (global indices)
     unsigned *fb_count;
     float *raw;          // debug: materialise the raw screened dot products
+    int dbg;             // debug bit 1: skip the screening math (pipeline timing only)
 };
 
 // ------------------------------------------------------------- kernel ----
@@ -73,23 +77,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                      const __grid_constant__ CUtensorMap tmXl,
                      const __grid_constant__ CUtensorMap tmC,
                      const __grid_constant__ CUtensorMap tmCl, TcParams P) {
+    // Persistent: CTA b handles row tiles b, b + grid, ...; the X tile is
+    // double-buffered when it fits so the next tile streams in while this
+    // tile's last epilogue / refinement runs.
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char *smem = reinterpret_cast<unsigned char *>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align to 1024 B by pointer arithmetic on the __shared__ array itself so
+    // the compiler keeps the shared address space (LDS/STS, not generic LD/ST)
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr int NOP = SPLIT ? 2 : 1;             // hi (+ lo) operand copies
-    const int nkb = P.nkb, S = P.stages;
+    constexpr uint32_t IDX_MASK = BN > 128 ? 0xFFu : 0x7Fu;
+    const int nkb = P.nkb, S = P.stages, NA = P.abufs;
     const uint32_t A_KB_BYTES = TC_BM * 128;       // one k-block of X
+    const uint32_t A_BYTES = A_KB_BYTES * nkb * NOP;
     const uint32_t B_BYTES = BN * 128;             // one k-block of C
-    unsigned char *sA = smem;                      // NOP x nkb x 16 KB (hi first)
-    unsigned char *sB = sA + size_t(NOP) * nkb * A_KB_BYTES;  // S x NOP x B_BYTES
+    unsigned char *sA = smem;                      // NA x [NOP x nkb x 16 KB] (hi first)
+    unsigned char *sB = sA + size_t(NA) * A_BYTES; // S x NOP x B_BYTES
     uint64_t *bars = reinterpret_cast<uint64_t *>(sB + size_t(S) * NOP * B_BYTES);
     uint64_t *full = bars, *empty = bars + S;
-    uint64_t *a_full = bars + 2 * S;
-    uint64_t *t_full = a_full + 1, *t_empty = a_full + 3;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 5);
+    uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
+    uint64_t *t_full = a_full + 4, *t_empty = a_full + 6;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_full + 8);
+    float *yn_s = reinterpret_cast<float *>(a_full + 10);  // [2][BN] centroid norms
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row0 = int64_t(blockIdx.x) * TC_BM;
+    const int64_t ntm = (P.m + TC_BM - 1) / TC_BM;
 
     if (warp == 0 && lane == 0) {
         prefetch_tmap(&tmX);
@@ -98,11 +109,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(a_full, 1);
-        mbar_init(&t_full[0], 1);
-        mbar_init(&t_full[1], 1);
-        mbar_init(&t_empty[0], 4);
-        mbar_init(&t_empty[1], 4);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&a_full[a], 1);
+            mbar_init(&a_empty[a], 4);
+            mbar_init(&t_full[a], 1);
+            mbar_init(&t_empty[a], 4);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 2 * BN);
@@ -113,154 +125,221 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(a_full, A_KB_BYTES * nkb * NOP);
-            for (int kb = 0; kb < nkb; ++kb) {
-                tma_load_2d(sA + size_t(kb) * A_KB_BYTES, &tmX, a_full, kb * TC_KB, int(row0));
-                if (SPLIT)
-                    tma_load_2d(sA + size_t(nkb + kb) * A_KB_BYTES, &tmXl, a_full, kb * TC_KB,
-                                int(row0));
-            }
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = 0; t < P.ntiles; ++t) {
+            int it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntm; tile += gridDim.x, ++it) {
+                const int ab = it % NA;
+                const uint32_t ause = uint32_t(it / NA) & 1;
+                mbar_wait(&a_empty[ab], ause ^ 1);
+                unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
+                const int row0 = int(tile * TC_BM);
+                mbar_expect_tx(&a_full[ab], A_BYTES);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], B_BYTES * NOP);
-                    unsigned char *dst = sB + size_t(stage) * NOP * B_BYTES;
-                    tma_load_2d(dst, &tmC, &full[stage], kb * TC_KB, t * BN);
-                    if (SPLIT) tma_load_2d(dst + B_BYTES, &tmCl, &full[stage], kb * TC_KB, t * BN);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
+                    tma_load_2d(a_dst + size_t(kb) * A_KB_BYTES, &tmX, &a_full[ab], kb * TC_KB, row0);
+                    if (SPLIT)
+                        tma_load_2d(a_dst + size_t(nkb + kb) * A_KB_BYTES, &tmXl, &a_full[ab],
+                                    kb * TC_KB, row0);
+                }
+                for (int t = 0; t < P.ntiles; ++t) {
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], B_BYTES * NOP);
+                        unsigned char *dst = sB + size_t(stage) * NOP * B_BYTES;
+                        tma_load_2d(dst, &tmC, &full[stage], kb * TC_KB, t * BN);
+                        if (SPLIT)
+                            tma_load_2d(dst + B_BYTES, &tmCl, &full[stage], kb * TC_KB, t * BN);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_tf32(TC_BM, BN);
-            const uint32_t a_base = smem_u32(sA), b_base = smem_u32(sB);
-            const uint32_t a_lo = a_base + uint32_t(nkb) * A_KB_BYTES;
-            mbar_wait(a_full, 0);
+            const uint32_t b_base = smem_u32(sB);
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = 0; t < P.ntiles; ++t) {
-                const int buf = t & 1;
-                const uint32_t use = uint32_t(t >> 1) & 1;
-                mbar_wait(&t_empty[buf], use ^ 1);
-                tc_fence_after();
-                const uint32_t d_tmem = tmem + uint32_t(buf * BN);
-                for (int kb = 0; kb < nkb; ++kb) {
-                    mbar_wait(&full[stage], phase);
+            uint32_t g = 0;  // global accumulator-tile counter (TMEM buffer ring)
+            int it = 0;
+            for (int64_t tile = blockIdx.x; tile < ntm; tile += gridDim.x, ++it) {
+                const int ab = it % NA;
+                mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);
+                const uint32_t a_base = smem_u32(sA) + uint32_t(ab) * A_BYTES;
+                const uint32_t a_lo = a_base + uint32_t(nkb) * A_KB_BYTES;
+                for (int t = 0; t < P.ntiles; ++t, ++g) {
+                    const int buf = g & 1;
+                    mbar_wait(&t_empty[buf], ((g >> 1) & 1) ^ 1);
                     tc_fence_after();
-                    const uint32_t bs = b_base + uint32_t(stage) * NOP * B_BYTES;
+                    const uint32_t d_tmem = tmem + uint32_t(buf * BN);
+                    for (int kb = 0; kb < nkb; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t bs = b_base + uint32_t(stage) * NOP * B_BYTES;
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {  // 4 x (K = 8 tf32) per 128-byte row
-                        const uint32_t ao = uint32_t(kb) * A_KB_BYTES + kk * 32;
-                        const uint64_t ah = smem_desc(a_base + ao);
-                        const uint64_t bh = smem_desc(bs + kk * 32);
-                        mma_tf32(d_tmem, ah, bh, idesc, (kb | kk) != 0);
-                        if (SPLIT) {
-                            mma_tf32(d_tmem, ah, smem_desc(bs + B_BYTES + kk * 32), idesc, 1);
-                            mma_tf32(d_tmem, smem_desc(a_lo + ao), bh, idesc, 1);
+                        for (int kk = 0; kk < 4; ++kk) {  // 4 x (K = 8 tf32) per 128-byte row
+                            const uint32_t ao = uint32_t(kb) * A_KB_BYTES + kk * 32;
+                            const uint64_t ah = smem_desc(a_base + ao);
+                            const uint64_t bh = smem_desc(bs + kk * 32);
+                            mma_tf32(d_tmem, ah, bh, idesc, (kb | kk) != 0);
+                            if (SPLIT) {
+                                mma_tf32(d_tmem, ah, smem_desc(bs + B_BYTES + kk * 32), idesc, 1);
+                                mma_tf32(d_tmem, smem_desc(a_lo + ao), bh, idesc, 1);
+                            }
                         }
+                        mma_commit(&empty[stage]);
+                        if (++stage == S) { stage = 0; phase ^= 1; }
                     }
-                    mma_commit(&empty[stage]);
-                    if (++stage == S) { stage = 0; phase ^= 1; }
+                    mma_commit(&t_full[buf]);
                 }
-                mma_commit(&t_full[buf]);
             }
         }
     } else {
         // ---------------------------------------------------- epilogue --
         const int quad = warp & 3;              // TMEM lane group this warp may access
-        const int r = quad * 32 + lane;         // accumulator row
-        const int64_t grow = row0 + r;          // row within this pass
+        const int r = quad * 32 + lane;         // accumulator row within the tile
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
-        float m1 = INFINITY, m2 = INFINITY;
-        int tile1 = 0;
-        for (int t = 0; t < P.ntiles; ++t) {
-            const int buf = t & 1;
-            const uint32_t use = uint32_t(t >> 1) & 1;
-            mbar_wait(&t_full[buf], use);
-            tc_fence_after();
-            float t1 = INFINITY, t2 = INFINITY;
-            const int64_t c0 = int64_t(t) * BN;
-            const int live = int(P.k - c0 < BN ? P.k - c0 : BN);
-            const uint32_t tbase = tmem + lane_base + uint32_t(buf * BN);
-            // software-pipelined TMEM drain: chunk ch+1 in flight while ch is screened
-            uint32_t va[32], vb[32];
-            tmem_ld32_issue(tbase, va);
-            tmem_ld_wait(va);
+        const int et = threadIdx.x - 64;        // 0..127 among the epilogue threads
+        uint32_t g = 0;
+        int it = 0;
+        for (int64_t tile = blockIdx.x; tile < ntm; tile += gridDim.x, ++it) {
+            const int ab = it % NA;
+            const int64_t grow = tile * TC_BM + r;  // row within this pass
+            float m1 = INFINITY, m2 = INFINITY;
+            int tile1 = 0;
+            // centroid norms of tile t live in yn_s[t & 1]: each epilogue thread
+            // stages BN/128 values per tile, prefetched one tile ahead (named
+            // barrier 1 synchronises the 128 epilogue threads only)
+            for (int e = et; e < BN; e += 128) yn_s[e] = e < P.k ? __ldg(P.yn + e) : 0.0f;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            for (int t = 0; t < P.ntiles; ++t, ++g) {
+                const int buf = g & 1;
+                const int ybuf = t & 1;
+                const int64_t c0 = int64_t(t) * BN;
+                float yn_next[(BN + 127) / 128];
 #pragma unroll
-            for (int ch = 0; ch < BN / 32; ch += 2) {
-                if (ch + 1 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
-                if (P.raw && grow < P.m)
-                    for (int e = 0; e < 32 && ch * 32 + e < live; ++e)
-                        P.raw[grow * P.k + c0 + ch * 32 + e] = __uint_as_float(va[e]);
-                screen_chunk(va, P.yn + c0 + ch * 32, ch * 32, live - ch * 32, t1, t2);
-                if (ch + 1 < BN / 32) {
-                    tmem_ld_wait(vb);
-                    if (ch + 2 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
-                    if (P.raw && grow < P.m)
-                        for (int e = 0; e < 32 && (ch + 1) * 32 + e < live; ++e)
-                            P.raw[grow * P.k + c0 + (ch + 1) * 32 + e] = __uint_as_float(vb[e]);
-                    screen_chunk(vb, P.yn + c0 + (ch + 1) * 32, (ch + 1) * 32,
-                                 live - (ch + 1) * 32, t1, t2);
-                    if (ch + 2 < BN / 32) tmem_ld_wait(va);
+                for (int q = 0; q < (BN + 127) / 128; ++q) {
+                    const int e = et + q * 128;
+                    const int64_t cn = c0 + BN + e;
+                    yn_next[q] = (e < BN && cn < P.k) ? __ldg(P.yn + cn) : 0.0f;
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&t_empty[buf]);
-            // merge the tile's top-2 into the running top-2
-            const float hi = fmaxf(m1, t1);
-            if (t1 < m1) tile1 = t;
-            m1 = fminf(m1, t1);
-            m2 = fminf(fminf(m2, t2), hi);
-        }
-
-        if (grow < P.m) {
-            const int j = tile1 * BN + int(__float_as_uint(m1) & 0x7Fu);
-            const int64_t orow = P.rows ? int64_t(P.rows[grow]) : grow;
-            // one pass over the resident X row: ||x||^2 (bound) and the exact
-            // sequential dot product with the screened winner.  The winner row
-            // is fetched 32 floats (8 x 16 B) at a time so the L2 round trips
-            // overlap; x comes from the swizzled tile (chunk q of row r sits at
-            // chunk position q ^ (r & 7)); in split mode x = x_hi + x_lo exactly.
-            const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(j) * P.d);
-            float acc = 0.0f, xx = 0.0f;
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int k0 = kb * TC_KB;
-                float4 cv[8];
+                const float *ynt = yn_s + ybuf * BN;
+                mbar_wait(&t_full[buf], (g >> 1) & 1);
+                tc_fence_after();
+                float t1 = INFINITY, t2 = INFINITY;
+                const int live = int(P.k - c0 < BN ? P.k - c0 : BN);
+                const uint32_t tbase = tmem + lane_base + uint32_t(buf * BN);
+                // software-pipelined TMEM drain: chunk ch+1 in flight while ch is screened
+                uint32_t va[32], vb[32];
+                tmem_ld32_issue(tbase, va);
+                tmem_ld_wait(va);
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
-                    cv[q] = (k0 + 4 * q < P.d) ? __ldg(cj4 + (k0 >> 2) + q)
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-                const unsigned char *rowp = sA + uint32_t(kb) * A_KB_BYTES + uint32_t(r) * 128;
+                for (int ch = 0; ch < ((P.dbg & 1) ? 0 : BN / 32); ch += 2) {
+                    if (ch + 1 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
+                    if (P.raw && grow < P.m)
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    if (k0 + 4 * q < P.d) {
-                        const uint32_t off = (q ^ (r & 7)) << 4;
-                        // the hi tile holds the full fp32 x (the MMA truncates it)
-                        const float4 xv = *reinterpret_cast<const float4 *>(rowp + off);
-                        acc = __fadd_rn(acc, __fmul_rn(xv.x, cv[q].x));
-                        acc = __fadd_rn(acc, __fmul_rn(xv.y, cv[q].y));
-                        acc = __fadd_rn(acc, __fmul_rn(xv.z, cv[q].z));
-                        acc = __fadd_rn(acc, __fmul_rn(xv.w, cv[q].w));
-                        xx = fmaf(xv.x, xv.x, xx);
-                        xx = fmaf(xv.y, xv.y, xx);
-                        xx = fmaf(xv.z, xv.z, xx);
-                        xx = fmaf(xv.w, xv.w, xx);
+                        for (int e = 0; e < 32; ++e)  // static indices: va stays in registers
+                            if (ch * 32 + e < live)
+                                P.raw[grow * P.k + c0 + ch * 32 + e] = __uint_as_float(va[e]);
+                    screen_chunk(va, ynt + ch * 32, ch * 32, live - ch * 32, IDX_MASK, t1, t2);
+                    if (ch + 1 < BN / 32) {
+                        tmem_ld_wait(vb);
+                        if (ch + 2 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
+                        if (P.raw && grow < P.m)
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if ((ch + 1) * 32 + e < live)
+                                    P.raw[grow * P.k + c0 + (ch + 1) * 32 + e] =
+                                        __uint_as_float(vb[e]);
+                        screen_chunk(vb, ynt + (ch + 1) * 32, (ch + 1) * 32, live - (ch + 1) * 32,
+                                     IDX_MASK, t1, t2);
+                        if (ch + 2 < BN / 32) tmem_ld_wait(va);
                     }
                 }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&t_empty[buf]);
+                // stage the next tile's norms (that buffer was last read two
+                // tiles ago, before the previous barrier)
+#pragma unroll
+                for (int q = 0; q < (BN + 127) / 128; ++q)
+                    if (et + q * 128 < BN) yn_s[(ybuf ^ 1) * BN + et + q * 128] = yn_next[q];
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                // merge the tile's top-2 into the running top-2
+                const float hi = fmaxf(m1, t1);
+                if (t1 < m1) tile1 = t;
+                m1 = fminf(m1, t1);
+                m2 = fminf(fminf(m2, t2), hi);
             }
-            const float A = P.a_coef * sqrtf(xx * (1.0f + 0x1p-10f)) * sqrtf(*P.cmax2);
-            const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
-            if (m2 - m1 > gap_need && m1 < INFINITY) {
-                P.out_idx[orow] = j;
-                P.out_val[orow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
-            } else {
-                const unsigned slot = atomicAdd(P.fb_count, 1u);
-                P.fb_rows[slot] = int32_t(orow);
+
+            if (grow < P.m) {
+                const int j = tile1 * BN + int(__float_as_uint(m1) & IDX_MASK);
+                const int64_t orow = P.rows ? int64_t(P.rows[grow]) : grow;
+                // one pass over the resident X row: ||x||^2, the truncation
+                // residual, and the exact sequential dot product with the
+                // screened winner (fetched 32 floats at a time so the L2 round
+                // trips overlap).  Chunk q of row r sits at chunk position
+                // q ^ (r & 7) of the 128-byte swizzled row; the hi tile holds
+                // the full fp32 x (the MMA truncates it).
+                const unsigned char *sAt = sA + size_t(ab) * A_BYTES;
+                const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(j) * P.d);
+                float acc = 0.0f, xx = 0.0f, ee = 0.0f;
+                for (int kb = 0; kb < nkb; ++kb) {
+                    const int k0 = kb * TC_KB;
+                    float4 cv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        cv[q] = (k0 + 4 * q < P.d) ? __ldg(cj4 + (k0 >> 2) + q)
+                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const unsigned char *rowp = sAt + uint32_t(kb) * A_KB_BYTES + uint32_t(r) * 128;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        if (k0 + 4 * q < P.d) {
+                            const float4 xv =
+                                *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.x, cv[q].x));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.y, cv[q].y));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.z, cv[q].z));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.w, cv[q].w));
+                            xx = fmaf(xv.x, xv.x, xx);
+                            xx = fmaf(xv.y, xv.y, xx);
+                            xx = fmaf(xv.z, xv.z, xx);
+                            xx = fmaf(xv.w, xv.w, xx);
+                            if (!SPLIT) {  // truncation residual ||x - tf32(x)||^2
+                                const float r0 = xv.x - tf32_trunc(xv.x);
+                                const float r1 = xv.y - tf32_trunc(xv.y);
+                                const float r2 = xv.z - tf32_trunc(xv.z);
+                                const float r3 = xv.w - tf32_trunc(xv.w);
+                                ee = fmaf(r0, r0, ee);
+                                ee = fmaf(r1, r1, ee);
+                                ee = fmaf(r2, r2, ee);
+                                ee = fmaf(r3, r3, ee);
+                            }
+                        }
+                    }
+                }
+                const float xn = sqrtf(xx * (1.0f + 0x1p-10f));
+                const float cm = sqrtf(*P.cmax2 * (1.0f + 0x1p-10f));  // yn: rounded sum
+                // pass 1: |x.c - x~.c~| <= ||x - x~|| cmax + ||x|| max_j ||c_j - c~_j||
+                // (Cauchy-Schwarz on the actual truncation residuals) plus the
+                // accumulation terms; pass 2: the worst-case 3xTF32 coefficient.
+                const float A = SPLIT ? P.a_coef * xn * cm
+                                      : 2.0f * (1.0f + 0x1p-10f) *
+                                            (sqrtf(ee * (1.0f + 0x1p-10f)) * cm +
+                                             xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) +
+                                             P.a_coef * xn * cm);
+                const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
+                if (m2 - m1 > gap_need && m1 < INFINITY) {
+                    P.out_idx[orow] = j;
+                    P.out_val[orow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
+                } else {
+                    const unsigned slot = atomicAdd(P.fb_count, 1u);
+                    P.fb_rows[slot] = int32_t(orow);
+                }
             }
+            // this X buffer may be refilled once every epilogue warp is done with it
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_empty[ab]);
         }
     }
 
@@ -272,24 +351,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // --------------------------------------------------------- small kernels --
-// Upper bound of max_j ||c_j||^2 from the exact fp32 norms; resets counters.
-__global__ void tc_prep_kernel(const float *yn, int64_t k, float *cmax2, unsigned *counters) {
-    float m = 0.0f;
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) m = fmaxf(m, yn[j]);
-    for (int off = 16; off; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    __shared__ float sh[32];
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float mm = 0.0f;
-        for (int w = 0; w < int(blockDim.x / 32); ++w) mm = fmaxf(mm, sh[w]);
-        *cmax2 = mm * (1.0f + 0x1p-10f);  // yn is a rounded sum
-        counters[0] = counters[1] = 0u;
+// Upper bounds of max_j ||c_j||^2 (from the exact fp32 norms) and of
+// max_j ||c_j - tf32(c_j)||^2: one warp per centroid row, float maxima via
+// integer atomicMax (non-negative floats order like their bit patterns).
+// bounds[0..1] must be zeroed; the consumer inflates them for rounding.
+__global__ void tc_prep_kernel(const float *y, const float *yn, int64_t k, int64_t d,
+                               float *bounds) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    float m = 0.0f, e = 0.0f;
+    for (int64_t j = w0; j < k; j += nw) {
+        float s = 0.0f;
+        for (int64_t f = lane; f < d; f += 32) {
+            const float v = y[j * d + f];
+            const float r = v - tf32_trunc(v);
+            s = fmaf(r, r, s);
+        }
+        for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        e = fmaxf(e, s);
+        m = fmaxf(m, yn[j]);
     }
-}
-
-__device__ __forceinline__ float tf32_trunc(float v) {
-    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    if (lane == 0) {
+        atomicMax(reinterpret_cast<int *>(bounds), __float_as_int(m));
+        atomicMax(reinterpret_cast<int *>(bounds + 1), __float_as_int(e));
+    }
 }
 
 // lo[i] = v[i] - trunc_tf32(v[i]) (exact in fp32)
@@ -372,21 +458,28 @@ static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &m
     constexpr int NOP = SPLIT ? 2 : 1;
     const size_t a_bytes = size_t(P.nkb) * TC_BM * 128 * NOP;
     const size_t b_bytes = size_t(BN) * 128 * NOP;
-    // Two CTAs per SM (one's refine/prologue overlaps the other's MMAs) when
-    // the resident X tile leaves room for >= 2 centroid stages in ~113 KB.
-    const size_t fixed = 1024 + a_bytes + 256;
-    const size_t two_cta = 113 * 1024;
-    int stages = fixed + 2 * b_bytes <= two_cta ? int((two_cta - fixed) / b_bytes)
-                                                : int((227 * 1024 - fixed) / b_bytes);
-    if (stages > 6) stages = 6;
+    const size_t extra = 1024 + 256 + 2 * BN * sizeof(float);  // align slack, barriers, norms
+    const size_t cap = 227 * 1024;
+    // one persistent CTA per SM (TMEM: 2 x BN columns); prefer a double-
+    // buffered X tile with >= 3 centroid stages, else a single buffer
+    int abufs = 2;
+    if (extra + 2 * a_bytes + 3 * b_bytes > cap) abufs = 1;
+    if (const char *e = getenv("FTK_TC_ABUFS")) abufs = atoi(e) == 1 ? 1 : abufs;  // tuning
+    int stages = int((cap - extra - abufs * a_bytes) / b_bytes);
+    if (stages > 8) stages = 8;
+    if (const char *e = getenv("FTK_TC_STAGES")) stages = atoi(e) < stages ? atoi(e) : stages;
     if (stages < 2) {
         set_error("tc: tile exceeds shared memory");
         return FTK_ERR_UNSUPPORTED;
     }
     P.stages = stages;
-    const size_t smem = fixed + size_t(stages) * b_bytes;
-    const int64_t grid = (P.m + TC_BM - 1) / TC_BM;
-    if (grid == 0) return FTK_OK;
+    P.abufs = abufs;
+    const size_t smem = extra + abufs * a_bytes + size_t(stages) * b_bytes;
+    const int64_t ntm = (P.m + TC_BM - 1) / TC_BM;
+    if (ntm == 0) return FTK_OK;
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t grid = ntm < nsm ? ntm : nsm;
     auto kern = tc_screen_kernel<BN, SPLIT>;
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<dim3(unsigned(grid)), dim3(TC_THREADS), smem, st>>>(mx, mxl, mc, mcl, P);
@@ -400,7 +493,8 @@ static int screen(int bn, const TcParams &P, const CUtensorMap &mx, const CUtens
     switch (bn) {
         case 32: return launch_screen<32, SPLIT>(P, mx, mxl, mc, mcl, st);
         case 64: return launch_screen<64, SPLIT>(P, mx, mxl, mc, mcl, st);
-        default: return launch_screen<128, SPLIT>(P, mx, mxl, mc, mcl, st);
+        case 128: return launch_screen<128, SPLIT>(P, mx, mxl, mc, mcl, st);
+        default: return launch_screen<256, SPLIT>(P, mx, mxl, mc, mcl, st);
     }
 }
 
@@ -426,26 +520,34 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     const float *xf = static_cast<const float *>(x), *yf = static_cast<const float *>(y);
     const float *ynf = static_cast<const float *>(yn);
     float *outv = static_cast<float *>(out_val);
-    const int bn = k >= 128 ? 128 : (k > 32 ? 64 : 32);
-    const int bn2 = k >= 64 ? 64 : 32;  // pass 2 carries hi+lo operands: narrower tiles
+    int bn = k > 128 ? 256 : (k > 64 ? 128 : (k > 32 ? 64 : 32));
+    if (const char *e = getenv("FTK_TC_BN")) {  // tuning knob
+        const int want = atoi(e);
+        if ((want == 128 || want == 64 || want == 32) && want < bn) bn = want;
+    }
+    const int bn2 = k > 64 ? 128 : (k > 32 ? 64 : 32);  // pass 2: hi+lo operands
     float *misc = static_cast<float *>(scratch(ctx, SLOT_TC_MISC, 256, st));
     int32_t *rows1 = static_cast<int32_t *>(scratch(ctx, SLOT_TC_ROWS, sizeof(int32_t) * 2 * (m + 1), st));
     float *c_lo = static_cast<float *>(scratch(ctx, SLOT_TC_B, sizeof(float) * k * d, st));
     if (!misc || !rows1 || !c_lo) return FTK_ERR_CUDA;
     int32_t *rows2 = rows1 + (m + 1);
     unsigned *cnt = reinterpret_cast<unsigned *>(misc + 8);  // [0] pass-1 flagged, [1] pass-2
-    tc_prep_kernel<<<1, 256, 0, st>>>(ynf, k, misc, cnt);
+    FTK_CUDA(cudaMemsetAsync(misc, 0, 64, st));  // bounds + fallback counters
+    tc_prep_kernel<<<unsigned((k + 7) / 8 < 296 ? (k + 7) / 8 : 296), 256, 0, st>>>(yf, ynf, k, d,
+                                                                                misc);
     FTK_LAUNCHED("tc_prep_kernel");
 
     TcParams P{};
     P.x = xf; P.y = yf; P.yn = ynf;
     P.m = m; P.k = k; P.d = d;
     P.nkb = int((d + TC_KB - 1) / TC_KB);
-    P.b_coef = float((0x1p-15 + 0x1p-22) * 1.01);
+    P.b_coef = float((0x1p-14 + 0x1p-22) * 1.01);  // <= 255-ulp index packing + roundings
     P.cmax2 = misc;
+    P.ecmax2 = misc + 1;
     P.out_idx = out_idx;
     P.out_val = outv;
     P.raw = raw;
+    if (const char *e = getenv("FTK_TC_DEBUG")) P.dbg = atoi(e);  // pipeline-timing probe
     CUtensorMap mx, mc, mcl;
     int rc = make_map(&mc, yf, k, d, uint32_t(bn));
     if (rc) return rc;
@@ -456,7 +558,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         rc = make_map(&mx, xf, m, d, TC_BM);
         if (rc) return rc;
         P.ntiles = int((k + bn - 1) / bn);
-        P.a_coef = float(2.0 * (0x1p-9 + 0x1p-20 + 3.0 * double(d) * 0x1p-24) * (1.0 + 0x1p-10));
+        P.a_coef = float(3.0 * double(d) * 0x1p-24);  // accumulation terms (tight bound)
         P.fb_rows = rows1;
         P.fb_count = cnt;
         rc = screen<false>(bn, P, mx, mx, mc, mc, st);
@@ -520,7 +622,8 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     FTK_LAUNCHED("gather_rows_kernel");
     int32_t *idx2 = reinterpret_cast<int32_t *>(g_lo);
     float *val2 = g_lo + n2;
-    rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 32, 256, 16, idx2, val2, nullptr, false,
+    // 8-row slabs: few rows, so spread them over many CTAs
+    rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 8, 256, 16, idx2, val2, nullptr, false,
                    0.0, 0.0, 0, nullptr, nullptr, st);
     if (rc) return rc;
     scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, cnt, idx2, val2, out_idx, outv);

@@ -123,35 +123,49 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&v)[32]) {
                  : "memory");
 }
 
-// Screen 32 accumulator columns: s = yn - 2 acc, index packed into the low 7
-// mantissa bits (column within the 128-wide tile), running top-2 (t1 < t2).
-// `live` = number of valid columns in this chunk (<= 0: none).
-__device__ __forceinline__ void screen_chunk(const uint32_t (&v)[32], const float *yn, int cbase,
-                                             int live, float &t1, float &t2) {
+__device__ __forceinline__ float tf32_trunc(float v) {
+    return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+}
+
+// Running top-2 (t1 <= t2) update with two new values: 5 min/max ops per
+// pair (the compiler emits FMNMX3 for the 3-input minimum).
+__device__ __forceinline__ void top2_pair(float a, float b, float &t1, float &t2) {
+    const float u = fminf(t1, a), v = fmaxf(t1, a);
+    const float w = fmaxf(u, b);
+    t2 = fminf(fminf(t2, v), w);
+    t1 = fminf(u, b);
+}
+
+__device__ __forceinline__ float pack_col(float dd, uint32_t col, uint32_t mask) {
+    return __uint_as_float((__float_as_uint(dd) & ~mask) | col);
+}
+
+// Screen 32 accumulator columns: s = yn - 2 acc with the index packed into
+// the low 7 mantissa bits (column within the <=128-wide tile), folded into
+// the running top-2.  yn_s points at this chunk's 32 norms in SHARED memory
+// (broadcast reads); `live` = valid columns in the chunk (<= 0: none).
+__device__ __forceinline__ void screen_chunk(const uint32_t (&v)[32], const float *yn_s,
+                                             int cbase, int live, uint32_t mask, float &t1,
+                                             float &t2) {
     if (live >= 32) {
-        const float4 *yn4 = reinterpret_cast<const float4 *>(yn);
+        const float4 *yn4 = reinterpret_cast<const float4 *>(yn_s);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const float4 yv = __ldg(yn4 + q);
-            const float yy[4] = {yv.x, yv.y, yv.z, yv.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = q * 4 + u;
-                const float dd = fmaf(-2.0f, __uint_as_float(v[e]), yy[u]);
-                const float p =
-                    __uint_as_float((__float_as_uint(dd) & ~0x7Fu) | uint32_t(cbase + e));
-                const float hi = fmaxf(t1, p);
-                t1 = fminf(t1, p);
-                t2 = fminf(t2, hi);
-            }
+            const float4 yv = yn4[q];
+            const int e = q * 4;
+            const float p0 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 0]), yv.x), cbase + e + 0, mask);
+            const float p1 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 1]), yv.y), cbase + e + 1, mask);
+            const float p2 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 2]), yv.z), cbase + e + 2, mask);
+            const float p3 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 3]), yv.w), cbase + e + 3, mask);
+            top2_pair(p0, p1, t1, t2);
+            top2_pair(p2, p3, t1, t2);
         }
     } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
             if (e < live) {
-                const float dd = fmaf(-2.0f, __uint_as_float(v[e]), yn[e]);
                 const float p =
-                    __uint_as_float((__float_as_uint(dd) & ~0x7Fu) | uint32_t(cbase + e));
+                    pack_col(fmaf(-2.0f, __uint_as_float(v[e]), yn_s[e]), cbase + e, mask);
                 const float hi = fmaxf(t1, p);
                 t1 = fminf(t1, p);
                 t2 = fminf(t2, hi);

@@ -152,6 +152,158 @@ __global__ void __launch_bounds__(256) chain_sums_kernel(const T *x, int64_t d,
     }
 }
 
+// ------------------------------------------------ certified segmented sums --
+// The reference's float64 chain is order-dependent only if some partial sum
+// rounds.  For a (cluster, feature) chain whose values are all multiples of
+// 2^q (q = smallest ulp exponent among them), every partial sum of ANY subset
+// is a multiple of 2^q bounded by S = sum |v|; if S < 2^(53+q) all of them
+// are exact float64 numbers, so any association yields the reference's bits.
+// Segments of SEG members are summed in parallel; the combine step checks
+// the certificate and queues uncertified chains for the ordered kernel.
+constexpr int SEG = 256;
+
+template <typename T> __device__ __forceinline__ int ulp_exp(T v);
+template <> __device__ __forceinline__ int ulp_exp<float>(float v) {
+    const uint32_t e = (__float_as_uint(v) >> 23) & 0xFFu;
+    return int(e == 0 ? 1 : e) - 150;
+}
+template <> __device__ __forceinline__ int ulp_exp<double>(double v) {
+    const uint64_t e = (uint64_t(__double_as_longlong(v)) >> 52) & 0x7FFu;
+    return int(e == 0 ? 1 : e) - 1075;
+}
+
+__global__ void seg_count_kernel(const int64_t *counts, int64_t k, int64_t *nseg) {
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < k;
+         c += int64_t(gridDim.x) * blockDim.x)
+        nseg[c] = (counts[c] + SEG - 1) / SEG;
+}
+
+template <typename T, bool DMR>
+__global__ void __launch_bounds__(128) seg_partials_kernel(
+    const T *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
+    int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
+    __shared__ int32_t rows[SEG];
+    __shared__ int64_t info[3];
+    const int64_t s = blockIdx.x;
+    if (threadIdx.x == 0) {
+        // cluster owning segment s: largest c with seg_base[c] <= s
+        int64_t lo = 0, hi = k;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) / 2;
+            if (seg_base[mid] <= s) lo = mid; else hi = mid - 1;
+        }
+        info[0] = s < seg_base[k] ? lo : -1;
+        if (info[0] >= 0) {
+            const int64_t beg = offsets[lo] + (s - seg_base[lo]) * SEG;
+            const int64_t end = offsets[lo + 1];
+            info[1] = beg;
+            info[2] = (end - beg < SEG ? end - beg : SEG);
+        }
+    }
+    __syncthreads();
+    if (info[0] < 0) return;
+    const int64_t beg = info[1];
+    const int n = int(info[2]);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) rows[t] = perm[beg + t];
+    __syncthreads();
+    for (int64_t f = threadIdx.x; f < d; f += blockDim.x) {
+        double a = 0.0, b = 0.0, ab = 0.0;
+        int q = INT_MAX;
+        constexpr int U = 16;
+        int t = 0;
+        for (; t + U <= n; t += U) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = double(x[int64_t(rows[t + u]) * d + f]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a = __dadd_rn(a, v[u]);
+                if (DMR) b = __dadd_rn(b, v[u]);
+                ab = __dadd_rn(ab, fabs(v[u]));
+                if (v[u] != 0.0) q = min(q, ulp_exp<T>(T(v[u])));
+            }
+        }
+        for (; t < n; ++t) {
+            const double v = double(x[int64_t(rows[t]) * d + f]);
+            a = __dadd_rn(a, v);
+            if (DMR) b = __dadd_rn(b, v);
+            ab = __dadd_rn(ab, fabs(v));
+            if (v != 0.0) q = min(q, ulp_exp<T>(T(v)));
+        }
+        ps_a[s * d + f] = a;
+        if (DMR) ps_b[s * d + f] = b;
+        ps_abs[s * d + f] = ab;
+        ps_q[s * d + f] = q;
+    }
+}
+
+// Exponent of the lowest set bit of a float64 (s = odd * 2^e), INT_MAX for 0.
+__device__ __forceinline__ int lowbit_exp(double s) {
+    const uint64_t u = uint64_t(__double_as_longlong(s));
+    const uint64_t ef = (u >> 52) & 0x7FFu;
+    uint64_t mant = u & 0xFFFFFFFFFFFFFull;
+    if (ef == 0 && mant == 0) return INT_MAX;
+    if (ef != 0) mant |= (1ull << 52);
+    return int(ef == 0 ? 1 : ef) - 1075 + __ffsll((long long)mant) - 1;
+}
+
+// Fold the segments of one (cluster, feature) chain in member order.  A
+// segment whose values, joined to the running sum s, satisfy the exactness
+// certificate (|s| + sum|v| < 2^(53+q), q = min ulp exponent of s and of the
+// segment's values) contributes its precomputed partial exactly; a segment
+// that fails is re-walked member by member from s -- the reference's chain.
+template <typename T, bool DMR>
+__global__ void seg_fold_kernel(const T *x, int64_t d, const int32_t *perm,
+                                const int64_t *offsets, const int64_t *seg_base, int64_t k,
+                                const double *ps_a, const double *ps_b, const double *ps_abs,
+                                const int32_t *ps_q, double *sums_a, double *sums_b) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < k * d;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = e / d, f = e % d;
+        const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+        double a = 0.0, b = 0.0;
+        for (int64_t s = s0; s < s1; ++s) {
+            const int qseg = ps_q[s * d + f];
+            if (qseg == INT_MAX) continue;                 // all-zero segment: s + 0 == s
+            if (s == s0) {                                  // chain from 0 == the partial itself
+                a = ps_a[s * d + f];
+                if (DMR) b = ps_b[s * d + f];
+                continue;
+            }
+            const int qa = lowbit_exp(a);
+            const int q = qa < qseg ? qa : qseg;
+            const double bound = fabs(a) + ps_abs[s * d + f] * (1.0 + 0x1p-20);
+            const bool exact = q == INT_MAX || (q > -1000 && bound < ldexp(1.0, 53 + q));
+            if (exact && (!DMR || a == b)) {
+                a = __dadd_rn(a, ps_a[s * d + f]);
+                if (DMR) b = __dadd_rn(b, ps_b[s * d + f]);
+            } else {
+                const int64_t lo = offsets[c] + (s - s0) * SEG;
+                const int64_t hi = lo + SEG < offsets[c + 1] ? lo + SEG : offsets[c + 1];
+                constexpr int U = 16;
+                int64_t t = lo;
+                for (; t + U <= hi; t += U) {
+                    double v[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u] = double(x[int64_t(perm[t + u]) * d + f]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        a = __dadd_rn(a, v[u]);
+                        if (DMR) b = __dadd_rn(b, v[u]);
+                    }
+                }
+                for (; t < hi; ++t) {
+                    const double v = double(x[int64_t(perm[t]) * d + f]);
+                    a = __dadd_rn(a, v);
+                    if (DMR) b = __dadd_rn(b, v);
+                }
+            }
+        }
+        sums_a[e] = a;
+        if (DMR) sums_b[e] = b;
+    }
+}
+
 __global__ void u64_to_i64_kernel(const unsigned long long *a, int64_t *b, int64_t n) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -372,6 +524,52 @@ __global__ void movement_kernel(const T *nc, const T *oc, int64_t k, int64_t d, 
     atomicMax(moved_bits, bits);  // non-negative doubles order like their bits
 }
 
+// Warp per centroid (d <= 128: numpy's pairwise reduce is a single leaf):
+// lanes 0-7 hold the 8 strided accumulators of ||new - old||^2, lanes 8-15
+// those of ||old||^2; the leaf's fixed combine tree and tail follow.
+template <typename T>
+__global__ void movement_warp_kernel(const T *nc, const T *oc, int64_t k, int64_t d, double eps,
+                                     unsigned long long *moved_bits) {
+    const int lane = threadIdx.x & 31;
+    const int64_t j = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    if (j >= k) return;
+    const T *nr = nc + j * d, *orow = oc + j * d;
+    const int which = lane >> 3, jj = lane & 7;  // which: 0 num, 1 den
+    double r = 0.0;
+    const int64_t lim = d - (d % 8);
+    if (which < 2 && d >= 8) {
+        for (int64_t i = jj; i < lim; i += 8) {
+            const double o = double(orow[i]);
+            const double v = which == 0 ? __dsub_rn(double(nr[i]), o) : o;
+            const double sq = __dmul_rn(v, v);
+            r = i == jj ? sq : __dadd_rn(r, sq);
+        }
+    }
+    // ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7)) within each 8-lane group
+    const double s1 = __dadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+    const double s2 = __dadd_rn(s1, __shfl_xor_sync(0xffffffffu, s1, 2));
+    const double s4 = __dadd_rn(s2, __shfl_xor_sync(0xffffffffu, s2, 4));
+    double tot[2];
+    tot[0] = __shfl_sync(0xffffffffu, s4, 0);
+    tot[1] = __shfl_sync(0xffffffffu, s4, 8);
+    if (lane == 0) {
+        for (int w = 0; w < 2; ++w) {
+            double res = d >= 8 ? tot[w] : 0.0;
+            for (int64_t i = d >= 8 ? lim : 0; i < d; ++i) {
+                const double o = double(orow[i]);
+                const double v = w == 0 ? __dsub_rn(double(nr[i]), o) : o;
+                res = __dadd_rn(res, __dmul_rn(v, v));
+            }
+            tot[w] = res;
+        }
+        const double num = sqrt(tot[0]);
+        const double den = __dadd_rn(sqrt(tot[1]), eps);
+        const double q = __ddiv_rn(num, den);
+        const unsigned long long bits = isnan(q) ? 0x7ff8000000000000ull : __double_as_longlong(q);
+        atomicMax(moved_bits, bits);  // non-negative doubles order like their bits
+    }
+}
+
 // sq[i] = pairwise_sum_f((x[i,f] - cent64[label[i], f])^2)  (kmeans.py:199-201)
 template <typename T>
 __global__ void own_sq_dists_kernel(const T *x, const int32_t *lab, const double *c64, int64_t m,
@@ -389,9 +587,20 @@ __global__ void own_sq_dists_kernel(const T *x, const int32_t *lab, const double
 }
 
 __global__ void labels_equal_kernel(const int32_t *a, const int32_t *b, int64_t m, int32_t *flag) {
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+    // vectorised compare, one warp vote per 4 x 32 labels, one store per
+    // differing warp (no contended atomics)
+    bool diff = false;
+    const int64_t m4 = m / 4;
+    const int4 *a4 = reinterpret_cast<const int4 *>(a), *b4 = reinterpret_cast<const int4 *>(b);
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m4;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const int4 u = a4[i], v = b4[i];
+        diff |= (u.x != v.x) | (u.y != v.y) | (u.z != v.z) | (u.w != v.w);
+    }
+    for (int64_t i = m4 * 4 + int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x)
-        if (a[i] != b[i]) atomicExch(flag, 0);
+        diff |= a[i] != b[i];
+    if (__any_sync(0xffffffffu, diff) && (threadIdx.x & 31) == 0) *flag = 0;
 }
 
 __global__ void flip_f64_kernel(double *a, int64_t idx, int64_t bit, double *ba) {
@@ -460,6 +669,42 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     const int block = 256;
     const unsigned grid = unsigned((warps * 32 + block - 1) / block);
     const bool dmr = sums_b != nullptr;
+    if (dtype == FTK_F32 && m > 0) {
+        // certified segmented sums (float32 data): segments fold exactly
+        // unless their certificate fails, in which case only that segment is
+        // re-walked in member order
+        const int64_t max_seg = (m + SEG - 1) / SEG + k;
+        int64_t *seg_base = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_BASE, sizeof(int64_t) * (2 * k + 2), st));
+        size_t pbytes = size_t(max_seg) * d * (3 * sizeof(double) + sizeof(int32_t)) + 64;
+        char *pbuf = static_cast<char *>(scratch(ctx, SLOT_SEG_PART, pbytes, st));
+        if (!seg_base || !pbuf) return FTK_ERR_CUDA;
+        int64_t *nseg = seg_base + (k + 1);
+        double *ps_a = reinterpret_cast<double *>(pbuf);
+        double *ps_b = ps_a + max_seg * d;
+        double *ps_abs = ps_b + max_seg * d;
+        int32_t *ps_q = reinterpret_cast<int32_t *>(ps_abs + max_seg * d);
+        seg_count_kernel<<<grid_for(k, 256), 256, 0, st>>>(counts_a, k, nseg);
+        FTK_LAUNCHED("seg_count_kernel");
+        exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(nseg, k, seg_base);
+        FTK_LAUNCHED("exclusive_scan_small_kernel");
+        auto xx = static_cast<const float *>(x);
+        if (dmr) {
+            seg_partials_kernel<float, true><<<unsigned(max_seg), 128, 0, st>>>(
+                xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q);
+            FTK_LAUNCHED("seg_partials_kernel");
+            seg_fold_kernel<float, true><<<grid_for(k * d, 128), 128, 0, st>>>(
+                xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b);
+        } else {
+            seg_partials_kernel<float, false><<<unsigned(max_seg), 128, 0, st>>>(
+                xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q);
+            FTK_LAUNCHED("seg_partials_kernel");
+            seg_fold_kernel<float, false><<<grid_for(k * d, 128), 128, 0, st>>>(
+                xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q, sums_a,
+                nullptr);
+        }
+        FTK_LAUNCHED("seg_fold_kernel");
+        return FTK_OK;
+    }
     if (dtype == FTK_F32) {
         auto xx = static_cast<const float *>(x);
         if (dmr) chain_sums_kernel<float, true><<<grid, block, 0, st>>>(xx, d, vals_out, offsets, k, sums_a, sums_b);
@@ -644,6 +889,15 @@ int movement_run(ftk_ctx *ctx, int dtype, const void *nc, const void *oc, int64_
     if (!tmp) return FTK_ERR_CUDA;
     FTK_CUDA(cudaMemsetAsync(moved, 0, sizeof(double), st));
     auto mb = reinterpret_cast<unsigned long long *>(moved);
+    if (d <= 128) {
+        const unsigned g = unsigned((k * 32 + 255) / 256);
+        if (dtype == FTK_F32)
+            movement_warp_kernel<float><<<g, 256, 0, st>>>(static_cast<const float *>(nc), static_cast<const float *>(oc), k, d, eps, mb);
+        else
+            movement_warp_kernel<double><<<g, 256, 0, st>>>(static_cast<const double *>(nc), static_cast<const double *>(oc), k, d, eps, mb);
+        FTK_LAUNCHED("movement_warp_kernel");
+        return FTK_OK;
+    }
     unsigned grid = unsigned((k + 127) / 128);
     if (dtype == FTK_F32)
         movement_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float *>(nc), static_cast<const float *>(oc), k, d, eps, tmp, mb);
