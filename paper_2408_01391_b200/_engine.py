@@ -291,12 +291,13 @@ def own_sq_dists_dev(x_t, labels_i32, cent64, out):
 
 def tc_fallback_rows():
     """(rows the 1xTF32 screen left uncertified, rows the 3xTF32 re-screen
-    left for the exact kernel) of the last TC assignment."""
+    left for the exact kernel, rows whose TC row checksum failed) of the last
+    TC assignment."""
     import ctypes
 
-    v = (ctypes.c_int64 * 2)()
+    v = (ctypes.c_int64 * 3)()
     N.check(N.load().ftk_tc_fallback_rows(ctx(), v, stream()), "ftk_tc_fallback_rows")
-    return int(v[0]), int(v[1])
+    return int(v[0]), int(v[1]), int(v[2])
 
 
 def tc_raw_dots(x_t, y_t, yn_t, split=False):

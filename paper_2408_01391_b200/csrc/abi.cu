@@ -60,8 +60,14 @@ int labels_equal_run(const int32_t *, const int32_t *, int64_t, int32_t *, cudaS
 int own_sq_dists_run(ftk_ctx *, int, const void *, const int32_t *, const double *, int64_t,
                      int64_t, double *, cudaStream_t);
 int flip_f64_run(double *, int64_t, int64_t, int64_t, int64_t, double *, cudaStream_t);
+struct TcFt;
 int tc_assign_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
-                  int64_t, int32_t *, void *, cudaStream_t, float *raw, int split_only);
+                  int64_t, int32_t *, void *, cudaStream_t, float *raw, int split_only,
+                  const TcFt *ft);
+int tc_checked_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
+                   int64_t, int64_t, int64_t, int64_t, double, double, int64_t, int32_t *, void *,
+                   const ftk_injection *, ftk_events *, cudaStream_t);
+int tc_supported(int dtype, int64_t m, int64_t k, int64_t d);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
@@ -109,7 +115,8 @@ int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *
     cudaStream_t st = as_stream(stream);
     bool has_inj = inj && inj->n > 0;
     if (variant == FTK_VARIANT_TC || (variant == FTK_VARIANT_AUTO && !has_inj)) {
-        int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st, nullptr, 0);
+        int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st, nullptr, 0,
+                               nullptr);
         if (rc != FTK_ERR_UNSUPPORTED || variant == FTK_VARIANT_TC) return rc;
     }
     return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
@@ -122,9 +129,15 @@ int ftk_checked_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, cons
                        int64_t iteration, int32_t *out_idx, void *out_val,
                        const ftk_injection *inj, ftk_events *ev, void *stream) {
     if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
-    (void)variant;
+    cudaStream_t st = as_stream(stream);
+    // TC path: screened assignment with per-tile row checksums; flagged rows
+    // and the logical blocks carrying scheduled flips are resolved exactly
+    if ((variant == FTK_VARIANT_TC || variant == FTK_VARIANT_AUTO) &&
+        tc_supported(dtype, m, k, d) && bn >= 1 && bm >= 1)
+        return tc_checked_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, delta_rel, abs_tol,
+                              iteration, out_idx, out_val, inj, ev, st);
     return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
-                     true, delta_rel, abs_tol, iteration, inj, ev, as_stream(stream));
+                     true, delta_rel, abs_tol, iteration, inj, ev, st);
 }
 
 int ftk_gemm(ftk_ctx *ctx, int dtype, const void *x, const void *y, int64_t m, int64_t k,
@@ -203,10 +216,11 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
 
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
     if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
-    unsigned v[2] = {0, 0};
+    unsigned v[3] = {0, 0, 0};
     int rc = tc_last_fallback(ctx, v, as_stream(stream));
     out[0] = int64_t(v[0]);
     out[1] = int64_t(v[1]);
+    out[2] = int64_t(v[2]);
     return rc;
 }
 
@@ -215,7 +229,7 @@ int ftk_tc_raw_dots(ftk_ctx *ctx, int split, const float *x, const float *y, con
                     float *out_val, void *stream) {
     if (!ctx || !raw) { set_error("bad ctx/raw"); return FTK_ERR_ARG; }
     return tc_assign_run(ctx, FTK_F32, x, y, ynorms, m, k, d, out_idx, out_val,
-                         as_stream(stream), raw, split);
+                         as_stream(stream), raw, split, nullptr);
 }
 
 }  // extern "C"

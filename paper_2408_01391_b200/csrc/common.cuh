@@ -44,7 +44,7 @@ struct Scratch {
 
 struct ftk_ctx {
     int device = 0;
-    ftk::Scratch slots[16];
+    ftk::Scratch slots[24];
 };
 
 namespace ftk {
@@ -67,6 +67,9 @@ enum ScratchSlot {
     SLOT_SEG_BASE = 12,
     SLOT_SEG_PART = 13,
     SLOT_SEG_FB = 14,
+    SLOT_TC_CSUM1 = 15,
+    SLOT_TC_CSUM2 = 16,
+    SLOT_TC_INJROWS = 17,
 };
 
 // ------------------------------------------------------- float helpers --

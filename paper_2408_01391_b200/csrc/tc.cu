@@ -32,6 +32,8 @@
 // once and stays resident; centroid k-blocks stream through a ring; two TMEM
 // accumulators let the MMA of centroid tile t+1 overlap the epilogue of t.
 
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -68,10 +70,40 @@ struct TcParams {
     unsigned *fb_count;
     float *raw;          // debug: materialise the raw screened dot products
     int dbg;             // debug bit 1: skip the screening math (pipeline timing only)
+    // FT mode (CHK kernels): per-N-tile row checksums verified in the epilogue
+    const float *csum;   // nkb*32: checksum centroid sum_j c~_j over all K centroids
+    const float *camax;  // scalar: max |c|
+    float tau_coef;      // delta_rel * D * sqrt(K / 32): reference tolerance, K-column checksum
+    float tau_abs;
+    const int32_t *inj_col;    // per row: injected column (-1: none)
+    const float *inj_before;   // exact accumulator value before the flip
+    const float *inj_after;    // after the flip
+    unsigned *abft_count;      // rows whose checksum failed (diagnostics)
 };
 
 // ------------------------------------------------------------- kernel ----
-template <int BN, bool SPLIT>
+// ABFT reference for row r of the resident X tile and centroid tile t:
+// x~ . sum_j c~_j (x~ = tf32(x) in the 1xTF32 pass, x itself in the 3xTF32 one)
+template <bool SPLIT>
+__device__ __forceinline__ double row_checksum(const unsigned char *rowA, const float *csum, int t,
+                                              int nkb, int r) {
+    const float4 *cs4 = reinterpret_cast<const float4 *>(csum) + int64_t(t) * nkb * 8;
+    double rr = 0.0;  // float64: the reference side must be well below the tolerance
+    for (int kb = 0; kb < nkb; ++kb)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const float4 xv = *reinterpret_cast<const float4 *>(rowA + uint32_t(kb) * TC_BM * 128 +
+                                                                ((q ^ (r & 7)) << 4));
+            const float4 sv = __ldg(cs4 + kb * 8 + q);
+            rr = fma(double(SPLIT ? xv.x : tf32_trunc(xv.x)), double(sv.x), rr);
+            rr = fma(double(SPLIT ? xv.y : tf32_trunc(xv.y)), double(sv.y), rr);
+            rr = fma(double(SPLIT ? xv.z : tf32_trunc(xv.z)), double(sv.z), rr);
+            rr = fma(double(SPLIT ? xv.w : tf32_trunc(xv.w)), double(sv.w), rr);
+        }
+    return rr;
+}
+
+template <int BN, bool SPLIT, bool CHK>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_screen_kernel(const __grid_constant__ CUtensorMap tmX,
                      const __grid_constant__ CUtensorMap tmXl,
@@ -207,6 +239,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int64_t grow = tile * TC_BM + r;  // row within this pass
             float m1 = INFINITY, m2 = INFINITY;
             int tile1 = 0;
+            bool abft_bad = false;
+            float amax_i = 0.0f;
+            double rref = 0.0;
+            double rsum = 0.0;  // row checksum over all centroid tiles
+            int inj_c = -1;
+            float inj_b = 0.0f, inj_a = 0.0f;
+            const unsigned char *rowA = sA + size_t(ab) * A_BYTES + uint32_t(r) * 128;
+            if (CHK) {
+                if (grow < P.m && P.inj_col) {
+                    inj_c = P.inj_col[grow];
+                    if (inj_c >= 0) {
+                        inj_b = P.inj_before[grow];
+                        inj_a = P.inj_after[grow];
+                    }
+                }
+                mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // the X tile is resident
+                for (int kb = 0; kb < nkb; ++kb)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        const float4 xv = *reinterpret_cast<const float4 *>(
+                            rowA + uint32_t(kb) * A_KB_BYTES + ((q ^ (r & 7)) << 4));
+                        amax_i = fmaxf(amax_i, fmaxf(fmaxf(fabsf(xv.x), fabsf(xv.y)),
+                                                     fmaxf(fabsf(xv.z), fabsf(xv.w))));
+                    }
+                // the row's checksum reference x~ . sum_j c~_j, computed while the
+                // tensor core works on the first centroid tile
+                rref = row_checksum<SPLIT>(rowA, P.csum, 0, nkb, r);
+            }
             // centroid norms of tile t live in yn_s[t & 1]: each epilogue thread
             // stages BN/128 values per tile, prefetched one tile ahead (named
             // barrier 1 synchronises the 128 epilogue threads only)
@@ -226,7 +286,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float *ynt = yn_s + ybuf * BN;
                 mbar_wait(&t_full[buf], (g >> 1) & 1);
                 tc_fence_after();
-                float t1 = INFINITY, t2 = INFINITY;
+                float t1 = INFINITY, t2 = INFINITY, tsum = 0.0f;
                 const int live = int(P.k - c0 < BN ? P.k - c0 : BN);
                 const uint32_t tbase = tmem + lane_base + uint32_t(buf * BN);
                 // software-pipelined TMEM drain: chunk ch+1 in flight while ch is screened
@@ -241,7 +301,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         for (int e = 0; e < 32; ++e)  // static indices: va stays in registers
                             if (ch * 32 + e < live)
                                 P.raw[grow * P.k + c0 + ch * 32 + e] = __uint_as_float(va[e]);
-                    screen_chunk(va, ynt + ch * 32, ch * 32, live - ch * 32, IDX_MASK, t1, t2);
+                    if (CHK && inj_c >= int(c0) + ch * 32 && inj_c < int(c0) + ch * 32 + 32)
+                        inject_into(va, inj_c - int(c0) - ch * 32, inj_b, inj_a);
+                    screen_chunk<CHK>(va, ynt + ch * 32, ch * 32, live - ch * 32, IDX_MASK, t1, t2,
+                                      tsum);
                     if (ch + 1 < BN / 32) {
                         tmem_ld_wait(vb);
                         if (ch + 2 < BN / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
@@ -251,8 +314,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                 if ((ch + 1) * 32 + e < live)
                                     P.raw[grow * P.k + c0 + (ch + 1) * 32 + e] =
                                         __uint_as_float(vb[e]);
-                        screen_chunk(vb, ynt + (ch + 1) * 32, (ch + 1) * 32, live - (ch + 1) * 32,
-                                     IDX_MASK, t1, t2);
+                        if (CHK && inj_c >= int(c0) + (ch + 1) * 32 &&
+                            inj_c < int(c0) + (ch + 1) * 32 + 32)
+                            inject_into(vb, inj_c - int(c0) - (ch + 1) * 32, inj_b, inj_a);
+                        screen_chunk<CHK>(vb, ynt + (ch + 1) * 32, (ch + 1) * 32,
+                                          live - (ch + 1) * 32, IDX_MASK, t1, t2, tsum);
                         if (ch + 2 < BN / 32) tmem_ld_wait(va);
                     }
                 }
@@ -265,6 +331,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int q = 0; q < (BN + 127) / 128; ++q)
                     if (et + q * 128 < BN) yn_s[(ybuf ^ 1) * BN + et + q * 128] = yn_next[q];
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (CHK) rsum += double(tsum);
+                if (CHK && t == P.ntiles - 1 && grow < P.m && !(P.dbg & 1)) {
+                    // ABFT: the row checksum of all K accumulators against
+                    // x~ . (sum_j c~_j), evaluated on the CUDA cores
+                    const float tau = P.tau_coef * fmaxf(1.0f, amax_i * *P.camax) + P.tau_abs;
+                    if (!(fabs(rsum - rref) <= double(tau))) abft_bad = true;
+                }
                 // merge the tile's top-2 into the running top-2
                 const float hi = fmaxf(m1, t1);
                 if (t1 < m1) tile1 = t;
@@ -329,7 +402,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                              xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) +
                                              P.a_coef * xn * cm);
                 const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
-                if (m2 - m1 > gap_need && m1 < INFINITY) {
+                if (CHK && abft_bad) atomicAdd(P.abft_count, 1u);
+                if (m2 - m1 > gap_need && m1 < INFINITY && !abft_bad) {
                     P.out_idx[orow] = j;
                     P.out_val[orow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
                 } else {
@@ -375,6 +449,96 @@ __global__ void tc_prep_kernel(const float *y, const float *yn, int64_t k, int64
     if (lane == 0) {
         atomicMax(reinterpret_cast<int *>(bounds), __float_as_int(m));
         atomicMax(reinterpret_cast<int *>(bounds + 1), __float_as_int(e));
+    }
+}
+
+// FT mode: per N-tile checksum centroid sum_j tf32(c_j) (float64 sum, then
+// fp32) zero-padded to nkb*32 features, and the tile's max |c|.
+__global__ void tile_csum_kernel(const float *y, int64_t k, int64_t d, int bn, int nkb,
+                                 int trunc, float *csum, float *camax) {
+    const int64_t t = blockIdx.x;
+    const int64_t j0 = t * bn, j1 = j0 + bn < k ? j0 + bn : k;
+    float am = 0.0f;
+    for (int64_t f = threadIdx.x; f < int64_t(nkb) * 32; f += blockDim.x) {
+        double s = 0.0;
+        if (f < d)
+            for (int64_t j = j0; j < j1; ++j) {
+                const float v = y[j * d + f];
+                s += double(trunc ? tf32_trunc(v) : v);  // 3xTF32 pass: ~exact operands
+                am = fmaxf(am, fabsf(v));
+            }
+        csum[t * nkb * 32 + f] = float(s);
+    }
+    for (int off = 16; off; off >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, off));
+    __shared__ float sh[32];
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = am;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float m = 0.0f;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) m = fmaxf(m, sh[w]);
+        camax[t] = m;
+    }
+}
+
+// FT mode: scheduled flips -> per-row (column, exact before, after) so the
+// TC epilogue can corrupt exactly the accumulator the reference corrupts.
+__global__ void inj_rows_kernel(const float *x, const float *y, int64_t m, int64_t k, int64_t d,
+                                int64_t bm, int64_t bn, ftk_injection inj, int32_t *inj_col,
+                                float *inj_before, float *inj_after) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < inj.n;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t ei = inj.ei[q], ej = inj.ej[q];
+        const int64_t row = inj.bi[q] * bm + ei, col = inj.bj[q] * bn + ej;
+        if (ei >= bm || ej >= bn || row >= m || col >= k) continue;
+        float acc = 0.0f;
+        for (int64_t f = 0; f < d; ++f) acc = __fadd_rn(acc, __fmul_rn(x[row * d + f], y[col * d + f]));
+        inj_col[row] = int32_t(col);
+        inj_before[row] = acc;
+        inj_after[row] = flip_bit(acc, inj.bit[q]);
+    }
+}
+
+__global__ void remap_events_kernel(int64_t *rec, const int64_t *count, int64_t cap,
+                                    const int64_t *blocks) {
+    const int64_t n = *count < cap ? *count : cap;
+    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+         c += int64_t(gridDim.x) * blockDim.x)
+        rec[c * 7 + 1] = blocks[rec[c * 7 + 1]];
+}
+
+__global__ void remap_inj_kernel(const int64_t *bi, int64_t n, const int64_t *blk_of, int64_t nb,
+                                 int64_t *bi_out) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        int64_t pos = -1;
+        for (int64_t b = 0; b < nb; ++b)
+            if (blk_of[b] == bi[q]) pos = b;
+        bi_out[q] = pos < 0 ? int64_t(1) << 40 : pos;  // unmatched -> never applies
+    }
+}
+
+// gather rows [blocks[b]*bm, +bm) (clipped to m) into a compact buffer
+__global__ void gather_blocks_kernel(const float *x, int64_t m, int64_t d, int64_t bm,
+                                     const int64_t *blocks, int64_t nb, float *g) {
+    const int64_t n = nb * bm * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / d, f = e % d;
+        const int64_t row = blocks[r / bm] * bm + r % bm;
+        if (row < m) g[e] = x[row * d + f];
+    }
+}
+
+__global__ void scatter_blocks_kernel(const int32_t *idx, const float *val, int64_t m, int64_t bm,
+                                      const int64_t *blocks, int64_t nb, int32_t *out_idx,
+                                      float *out_val) {
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nb * bm;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t row = blocks[r / bm] * bm + r % bm;
+        if (row < m) {
+            out_idx[row] = idx[r];
+            out_val[row] = val[r];
+        }
     }
 }
 
@@ -452,7 +616,7 @@ static int make_map(CUtensorMap *map, const float *base, int64_t rows, int64_t c
     return FTK_OK;
 }
 
-template <int BN, bool SPLIT>
+template <int BN, bool SPLIT, bool CHK>
 static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &mxl,
                          const CUtensorMap &mc, const CUtensorMap &mcl, cudaStream_t st) {
     constexpr int NOP = SPLIT ? 2 : 1;
@@ -480,7 +644,7 @@ static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &m
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int64_t grid = ntm < nsm ? ntm : nsm;
-    auto kern = tc_screen_kernel<BN, SPLIT>;
+    auto kern = tc_screen_kernel<BN, SPLIT, CHK>;
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<dim3(unsigned(grid)), dim3(TC_THREADS), smem, st>>>(mx, mxl, mc, mcl, P);
     FTK_LAUNCHED("tc_screen_kernel");
@@ -490,11 +654,19 @@ static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &m
 template <bool SPLIT>
 static int screen(int bn, const TcParams &P, const CUtensorMap &mx, const CUtensorMap &mxl,
                   const CUtensorMap &mc, const CUtensorMap &mcl, cudaStream_t st) {
+    if (P.csum) {
+        switch (bn) {
+            case 32: return launch_screen<32, SPLIT, true>(P, mx, mxl, mc, mcl, st);
+            case 64: return launch_screen<64, SPLIT, true>(P, mx, mxl, mc, mcl, st);
+            case 128: return launch_screen<128, SPLIT, true>(P, mx, mxl, mc, mcl, st);
+            default: return launch_screen<256, SPLIT, true>(P, mx, mxl, mc, mcl, st);
+        }
+    }
     switch (bn) {
-        case 32: return launch_screen<32, SPLIT>(P, mx, mxl, mc, mcl, st);
-        case 64: return launch_screen<64, SPLIT>(P, mx, mxl, mc, mcl, st);
-        case 128: return launch_screen<128, SPLIT>(P, mx, mxl, mc, mcl, st);
-        default: return launch_screen<256, SPLIT>(P, mx, mxl, mc, mcl, st);
+        case 32: return launch_screen<32, SPLIT, false>(P, mx, mxl, mc, mcl, st);
+        case 64: return launch_screen<64, SPLIT, false>(P, mx, mxl, mc, mcl, st);
+        case 128: return launch_screen<128, SPLIT, false>(P, mx, mxl, mc, mcl, st);
+        default: return launch_screen<256, SPLIT, false>(P, mx, mxl, mc, mcl, st);
     }
 }
 
@@ -508,11 +680,82 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 
-static unsigned g_last_fb[3] = {0, 0, 0};  // pass-1 flagged, pass-2 flagged (diagnostics)
+static unsigned g_last_fb[3] = {0, 0, 0};  // pass-1 / pass-2 uncertified, TC ABFT flags
+
+struct TcFt {          // checksum-protected (abft) mode
+    double delta_rel, abs_tol;
+    int64_t bm, bn, bk, iteration;
+    const ftk_injection *inj;
+    ftk_events *ev;
+};
+
+// FT mode helpers: checksum centroids for a given N tiling
+static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb,
+                     int trunc, float **csum, float **camax, cudaStream_t st) {
+    const int64_t nt = 1;  // one checksum centroid over all K centroids
+    const int bn = int(k);
+    float *buf = static_cast<float *>(scratch(ctx, slot, sizeof(float) * (nt * nkb * 32 + nt + 64), st));
+    if (!buf) return FTK_ERR_CUDA;
+    *csum = buf;
+    *camax = buf + nt * nkb * 32;
+    tile_csum_kernel<<<unsigned(nt), 128, 0, st>>>(y, k, d, bn, nkb, trunc, *csum, *camax);
+    FTK_LAUNCHED("tile_csum_kernel");
+    return FTK_OK;
+}
+
+// Reference-identical handling of scheduled flips: the logical row blocks
+// that carry an injection are recomputed by the exact checked kernel (the
+// reference's detection / location / correction / events, bit for bit) and
+// overwrite the TC results for those rows.
+static int emulate_injected_blocks(ftk_ctx *ctx, const float *xf, const float *yf,
+                                   const float *ynf, int64_t m, int64_t k, int64_t d,
+                                   const TcFt &ft, int32_t *out_idx, float *outv,
+                                   cudaStream_t st) {
+    const ftk_injection &inj = *ft.inj;
+    std::vector<int64_t> bi(inj.n);
+    FTK_CUDA(cudaMemcpyAsync(bi.data(), inj.bi, sizeof(int64_t) * inj.n, cudaMemcpyDeviceToHost, st));
+    FTK_CUDA(cudaStreamSynchronize(st));
+    const int64_t nbi = (m + ft.bm - 1) / ft.bm;
+    std::vector<int64_t> blocks;
+    for (int64_t v : bi)
+        if (v >= 0 && v < nbi) blocks.push_back(v);
+    std::sort(blocks.begin(), blocks.end());
+    blocks.erase(std::unique(blocks.begin(), blocks.end()), blocks.end());
+    if (blocks.empty()) return FTK_OK;
+    // the (possibly partial) last row block must stay last in the compact set
+    const int64_t nb = int64_t(blocks.size());
+    const int64_t rows_c = (blocks.back() == nbi - 1) ? (nb - 1) * ft.bm + (m - (nbi - 1) * ft.bm)
+                                                      : nb * ft.bm;
+    const size_t need = sizeof(int64_t) * (2 * nb + 2 * inj.n + 8) +
+                        sizeof(float) * (nb * ft.bm * d + 2 * nb * ft.bm) + 256;
+    char *buf = static_cast<char *>(scratch(ctx, SLOT_INJ, need, st));
+    if (!buf) return FTK_ERR_CUDA;
+    int64_t *d_blocks = reinterpret_cast<int64_t *>(buf);
+    int64_t *d_bi = d_blocks + nb;
+    float *g = reinterpret_cast<float *>(d_bi + inj.n + 2);
+    int32_t *gi = reinterpret_cast<int32_t *>(g + nb * ft.bm * d);
+    float *gv = reinterpret_cast<float *>(gi + nb * ft.bm);
+    FTK_CUDA(cudaMemcpyAsync(d_blocks, blocks.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, st));
+    remap_inj_kernel<<<1, 256, 0, st>>>(inj.bi, inj.n, d_blocks, nb, d_bi);
+    FTK_LAUNCHED("remap_inj_kernel");
+    gather_blocks_kernel<<<148, 256, 0, st>>>(xf, m, d, ft.bm, d_blocks, nb, g);
+    FTK_LAUNCHED("gather_blocks_kernel");
+    ftk_injection rin = inj;
+    rin.bi = d_bi;
+    int rc = exact_run(ctx, FTK_F32, g, yf, ynf, rows_c, k, d, ft.bm, ft.bn, ft.bk, gi, gv, nullptr,
+                       true, ft.delta_rel, ft.abs_tol, ft.iteration, &rin, ft.ev, st);
+    if (rc) return rc;
+    remap_events_kernel<<<1, 256, 0, st>>>(ft.ev->rec, ft.ev->count, ft.ev->cap, d_blocks);
+    FTK_LAUNCHED("remap_events_kernel");
+    scatter_blocks_kernel<<<148, 256, 0, st>>>(gi, gv, m, ft.bm, d_blocks, nb, out_idx, outv);
+    FTK_LAUNCHED("scatter_blocks_kernel");
+    FTK_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
+    return FTK_OK;
+}
 
 int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn,
                   int64_t m, int64_t k, int64_t d, int32_t *out_idx, void *out_val,
-                  cudaStream_t st, float *raw, int split_only) {
+                  cudaStream_t st, float *raw, int split_only, const TcFt *ft) {
     if (!tc_supported(dtype, m, k, d)) {
         set_error("tc variant: unsupported shape/dtype");
         return FTK_ERR_UNSUPPORTED;
@@ -531,8 +774,8 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     float *c_lo = static_cast<float *>(scratch(ctx, SLOT_TC_B, sizeof(float) * k * d, st));
     if (!misc || !rows1 || !c_lo) return FTK_ERR_CUDA;
     int32_t *rows2 = rows1 + (m + 1);
-    unsigned *cnt = reinterpret_cast<unsigned *>(misc + 8);  // [0] pass-1 flagged, [1] pass-2
-    FTK_CUDA(cudaMemsetAsync(misc, 0, 64, st));  // bounds + fallback counters
+    unsigned *cnt = reinterpret_cast<unsigned *>(misc + 8);  // [0] pass-1, [1] pass-2, [2] abft
+    FTK_CUDA(cudaMemsetAsync(misc, 0, 64, st));  // bounds + counters
     tc_prep_kernel<<<unsigned((k + 7) / 8 < 296 ? (k + 7) / 8 : 296), 256, 0, st>>>(yf, ynf, k, d,
                                                                                 misc);
     FTK_LAUNCHED("tc_prep_kernel");
@@ -548,7 +791,27 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     P.out_val = outv;
     P.raw = raw;
     if (const char *e = getenv("FTK_TC_DEBUG")) P.dbg = atoi(e);  // pipeline-timing probe
-    CUtensorMap mx, mc, mcl;
+    float *csum1 = nullptr, *camax1 = nullptr, *csum2 = nullptr, *camax2 = nullptr;
+    if (ft) {
+        int rc0 = prep_csum(ctx, SLOT_TC_CSUM1, yf, k, d, P.nkb, 1, &csum1, &camax1, st);
+        if (!rc0) rc0 = prep_csum(ctx, SLOT_TC_CSUM2, yf, k, d, P.nkb, 0, &csum2, &camax2, st);
+        if (rc0) return rc0;
+        P.tau_abs = float(ft->abs_tol);
+        P.abft_count = cnt + 2;
+        if (ft->inj && ft->inj->n > 0) {
+            int32_t *ic = static_cast<int32_t *>(scratch(ctx, SLOT_TC_INJROWS, sizeof(float) * 3 * (m + 1), st));
+            if (!ic) return FTK_ERR_CUDA;
+            float *ib = reinterpret_cast<float *>(ic + (m + 1));
+            float *ia = ib + (m + 1);
+            FTK_CUDA(cudaMemsetAsync(ic, 0xFF, sizeof(int32_t) * m, st));  // -1: no flip
+            inj_rows_kernel<<<1, 128, 0, st>>>(xf, yf, m, k, d, ft->bm, ft->bn, *ft->inj, ic, ib, ia);
+            FTK_LAUNCHED("inj_rows_kernel");
+            P.inj_col = ic;
+            P.inj_before = ib;
+            P.inj_after = ia;
+        }
+    }
+    CUtensorMap mx, mc;
     int rc = make_map(&mc, yf, k, d, uint32_t(bn));
     if (rc) return rc;
     unsigned n1 = unsigned(m);
@@ -561,6 +824,11 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         P.a_coef = float(3.0 * double(d) * 0x1p-24);  // accumulation terms (tight bound)
         P.fb_rows = rows1;
         P.fb_count = cnt;
+        if (ft) {
+            P.csum = csum1;
+            P.camax = camax1;
+            P.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));
+        }
         rc = screen<false>(bn, P, mx, mx, mc, mc, st);
         if (rc) return rc;
         FTK_CUDA(cudaMemcpyAsync(&n1, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
@@ -569,71 +837,96 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     }
     g_last_fb[0] = n1;
     g_last_fb[1] = 0;
-    if (n1 == 0) return FTK_OK;
-    // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
-    float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
-    if (!g) return FTK_ERR_CUDA;
-    float *g_lo = g + size_t(n1) * d;
-    if (split_only) {
-        // identity row list for a direct 3xTF32 call (testing / forced mode)
-        std::vector<int32_t> ids(m);
-        for (int64_t i = 0; i < m; ++i) ids[i] = int32_t(i);
-        FTK_CUDA(cudaMemcpyAsync(rows1, ids.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-        FTK_CUDA(cudaMemcpyAsync(cnt, &n1, sizeof(unsigned), cudaMemcpyHostToDevice, st));
-        FTK_CUDA(cudaStreamSynchronize(st));
-        pass2_rows = rows1;
+    if (n1 > 0) {
+        // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
+        float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
+        if (!g) return FTK_ERR_CUDA;
+        float *g_lo = g + size_t(n1) * d;
+        if (split_only) {
+            // identity row list for a direct 3xTF32 call (testing / forced mode)
+            std::vector<int32_t> ids(m);
+            for (int64_t i = 0; i < m; ++i) ids[i] = int32_t(i);
+            FTK_CUDA(cudaMemcpyAsync(rows1, ids.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+            FTK_CUDA(cudaMemcpyAsync(cnt, &n1, sizeof(unsigned), cudaMemcpyHostToDevice, st));
+            FTK_CUDA(cudaStreamSynchronize(st));
+            pass2_rows = rows1;
+        }
+        gather_rows_kernel<<<148 * 8, 256, 0, st>>>(xf, d, pass2_rows, cnt, g, g_lo);
+        FTK_LAUNCHED("gather_rows_kernel");
+        split_lo_kernel<<<148 * 4, 256, 0, st>>>(yf, k * d, c_lo);
+        FTK_LAUNCHED("split_lo_kernel");
+        CUtensorMap mg, mgl, mc2, mcl2;
+        if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mgl, g_lo, n1, d, TC_BM)) ||
+            (rc = make_map(&mc2, yf, k, d, uint32_t(bn2))) ||
+            (rc = make_map(&mcl2, c_lo, k, d, uint32_t(bn2))))
+            return rc;
+        TcParams Q = P;
+        Q.x = g;
+        Q.m = n1;
+        Q.ntiles = int((k + bn2 - 1) / bn2);
+        Q.a_coef = float(2.0 * (3.0 * 0x1p-20 + 7.0 * double(d) * 0x1p-24) * (1.0 + 0x1p-10));
+        Q.rows = pass2_rows;
+        Q.fb_rows = rows2;
+        Q.fb_count = cnt + 1;
+        Q.raw = split_only ? raw : nullptr;
+        Q.inj_col = nullptr;  // pass-1 flips do not recur in the re-screen
+        if (ft) {
+            Q.csum = csum2;
+            Q.camax = camax2;
+            Q.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));
+        }
+        rc = screen<true>(bn2, Q, mg, mgl, mc2, mcl2, st);
+        unsigned n2 = 0;
+        unsigned *cnt2 = cnt + 1;
+        if (rc == FTK_ERR_UNSUPPORTED) {
+            // hi+lo X tile does not fit (large D): every pass-1 tie goes exact
+            rows2 = const_cast<int32_t *>(pass2_rows);
+            n2 = n1;
+            cnt2 = cnt;
+            rc = FTK_OK;
+        } else {
+            if (rc) return rc;
+            FTK_CUDA(cudaMemcpyAsync(&n2, cnt2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+            FTK_CUDA(cudaStreamSynchronize(st));
+        }
+        g_last_fb[1] = n2;
+        if (n2 > 0) {
+            // ---------------- exact resolution of the remaining ties (tiled SIMT kernel)
+            gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, cnt2, g, nullptr);
+            FTK_LAUNCHED("gather_rows_kernel");
+            int32_t *idx2 = reinterpret_cast<int32_t *>(g_lo);
+            float *val2 = g_lo + n2;
+            // 8-row slabs: few rows, so spread them over many CTAs
+            rc = exact_run(ctx, FTK_F32, g, yf, ynf, n2, k, d, 8, 256, 16, idx2, val2, nullptr,
+                           false, 0.0, 0.0, 0, nullptr, nullptr, st);
+            if (rc) return rc;
+            scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, cnt2, idx2, val2, out_idx, outv);
+            FTK_LAUNCHED("scatter_rows_kernel");
+        }
     }
-    gather_rows_kernel<<<148 * 8, 256, 0, st>>>(xf, d, pass2_rows, cnt, g, g_lo);
-    FTK_LAUNCHED("gather_rows_kernel");
-    split_lo_kernel<<<148 * 4, 256, 0, st>>>(yf, k * d, c_lo);
-    FTK_LAUNCHED("split_lo_kernel");
-    CUtensorMap mg, mgl, mc2, mcl2;
-    if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mgl, g_lo, n1, d, TC_BM)) ||
-        (rc = make_map(&mc2, yf, k, d, uint32_t(bn2))) ||
-        (rc = make_map(&mcl2, c_lo, k, d, uint32_t(bn2))))
-        return rc;
-    TcParams Q = P;
-    Q.x = g;
-    Q.m = n1;
-    Q.ntiles = int((k + bn2 - 1) / bn2);
-    Q.a_coef = float(2.0 * (3.0 * 0x1p-20 + 7.0 * double(d) * 0x1p-24) * (1.0 + 0x1p-10));
-    Q.rows = pass2_rows;
-    Q.fb_rows = rows2;
-    Q.fb_count = cnt + 1;
-    Q.raw = split_only ? raw : nullptr;
-    rc = screen<true>(bn2, Q, mg, mgl, mc2, mcl2, st);
-    unsigned n2 = 0;
-    if (rc == FTK_ERR_UNSUPPORTED) {
-        // hi+lo X tile does not fit (large D): every pass-1 tie goes exact
-        rows2 = const_cast<int32_t *>(pass2_rows);
-        n2 = n1;
-        rc = FTK_OK;
-    } else {
-        if (rc) return rc;
-        FTK_CUDA(cudaMemcpyAsync(&n2, cnt + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    if (ft) {
+        unsigned nab = 0;
+        FTK_CUDA(cudaMemcpyAsync(&nab, cnt + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         FTK_CUDA(cudaStreamSynchronize(st));
-        cnt += 1;
+        g_last_fb[2] = nab;
+        if (ft->inj && ft->inj->n > 0)
+            return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
     }
-    g_last_fb[1] = n2;
-    if (n2 == 0) return FTK_OK;
-    // ---------------- exact resolution of the remaining ties (tiled SIMT kernel)
-    float *g2 = g;  // reuse: n2 <= n1 rows
-    gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, cnt, g2, nullptr);
-    FTK_LAUNCHED("gather_rows_kernel");
-    int32_t *idx2 = reinterpret_cast<int32_t *>(g_lo);
-    float *val2 = g_lo + n2;
-    // 8-row slabs: few rows, so spread them over many CTAs
-    rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 8, 256, 16, idx2, val2, nullptr, false,
-                   0.0, 0.0, 0, nullptr, nullptr, st);
-    if (rc) return rc;
-    scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, cnt, idx2, val2, out_idx, outv);
-    FTK_LAUNCHED("scatter_rows_kernel");
     return FTK_OK;
+}
+
+int tc_checked_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn,
+                   int64_t m, int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk,
+                   double delta_rel, double abs_tol, int64_t iteration, int32_t *out_idx,
+                   void *out_val, const ftk_injection *inj, ftk_events *ev, cudaStream_t st) {
+    TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
+    return tc_assign_run(ctx, dtype, x, y, yn, m, k, d, out_idx, out_val, st, nullptr, 0, &ft);
 }
 
 int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t) {
     out[0] = g_last_fb[0];
     out[1] = g_last_fb[1];
+    out[2] = g_last_fb[2];
     return FTK_OK;
 }
 

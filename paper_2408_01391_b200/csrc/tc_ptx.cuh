@@ -127,6 +127,18 @@ __device__ __forceinline__ float tf32_trunc(float v) {
     return __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
 }
 
+// Scheduled flip on the TMEM-loaded accumulator of column e (0..31): the
+// screened value moves by the reference's delta (after - before of the exact
+// accumulator) or becomes the non-finite flipped value.  Static indexing only.
+__device__ __forceinline__ void inject_into(uint32_t (&v)[32], int e, float before, float after) {
+#pragma unroll
+    for (int u = 0; u < 32; ++u)
+        if (u == e) {
+            const float cur = __uint_as_float(v[u]);
+            v[u] = __float_as_uint(isfinite(after) ? cur + (after - before) : after);
+        }
+}
+
 // Running top-2 (t1 <= t2) update with two new values: 5 min/max ops per
 // pair (the compiler emits FMNMX3 for the 3-input minimum).
 __device__ __forceinline__ void top2_pair(float a, float b, float &t1, float &t2) {
@@ -144,15 +156,22 @@ __device__ __forceinline__ float pack_col(float dd, uint32_t col, uint32_t mask)
 // the low 7 mantissa bits (column within the <=128-wide tile), folded into
 // the running top-2.  yn_s points at this chunk's 32 norms in SHARED memory
 // (broadcast reads); `live` = valid columns in the chunk (<= 0: none).
+template <bool CHK = false>
 __device__ __forceinline__ void screen_chunk(const uint32_t (&v)[32], const float *yn_s,
                                              int cbase, int live, uint32_t mask, float &t1,
-                                             float &t2) {
+                                             float &t2, float &tsum) {
     if (live >= 32) {
         const float4 *yn4 = reinterpret_cast<const float4 *>(yn_s);
+        float part[2] = {0.0f, 0.0f};
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
             const float4 yv = yn4[q];
             const int e = q * 4;
+            if (CHK) {  // ABFT row checksum over the raw accumulators (shallow tree)
+                const float s01 = __uint_as_float(v[e + 0]) + __uint_as_float(v[e + 1]);
+                const float s23 = __uint_as_float(v[e + 2]) + __uint_as_float(v[e + 3]);
+                part[q & 1] += s01 + s23;
+            }
             const float p0 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 0]), yv.x), cbase + e + 0, mask);
             const float p1 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 1]), yv.y), cbase + e + 1, mask);
             const float p2 = pack_col(fmaf(-2.0f, __uint_as_float(v[e + 2]), yv.z), cbase + e + 2, mask);
@@ -160,10 +179,12 @@ __device__ __forceinline__ void screen_chunk(const uint32_t (&v)[32], const floa
             top2_pair(p0, p1, t1, t2);
             top2_pair(p2, p3, t1, t2);
         }
+        if (CHK) tsum += part[0] + part[1];
     } else {
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
             if (e < live) {
+                if (CHK) tsum += __uint_as_float(v[e]);
                 const float p =
                     pack_col(fmaf(-2.0f, __uint_as_float(v[e]), yn_s[e]), cbase + e, mask);
                 const float hi = fmaxf(t1, p);

@@ -97,3 +97,40 @@ def test_screen_error_model(split):
     assert np.array_equal(E.to_host(idx), ref_lab)
     assert E.to_host(val).tobytes() == ref_val.tobytes()
     print("max err/bound", float((err / bound).max()), "split", split)
+
+
+def test_tc_checked_matches_reference_events(golden):
+    """Checksum-protected TC path: fault-free -> same bits as the unprotected
+    reference and no TC checksum alarm; injected -> the reference's labels,
+    min_dists, events and hook records (golden fixtures)."""
+    from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook
+    from paper_2408_01391_b200.tiles import MICRO_SINGLE, make_config
+
+    rng = np.random.default_rng(5)
+    x = np.ascontiguousarray(rng.standard_normal((3000, 64)), dtype=np.float32)
+    y = np.ascontiguousarray(rng.standard_normal((300, 64)), dtype=np.float32)
+    res, rep = P.checked_assign(x, y)
+    lab, val = O.assign(x, y)
+    assert np.array_equal(res.assignments, lab) and res.min_dists.tobytes() == val.tobytes()
+    assert rep.detections == 0 and E.tc_fallback_rows()[2] == 0
+    z = golden("checked_cases.npz")
+    for n in ["a", "b", "d"]:
+        xx, yy, ent = z[f"{n}_x"], z[f"{n}_y"], z[f"{n}_ent"]
+        if xx.shape[1] % 4:
+            continue
+        blk = tuple(int(v) for v in z[f"{n}_block"])
+        cfg = None if blk[0] < 0 else make_config(blk, blk, MICRO_SINGLE)
+        entries = [FaultEntry(int(e[0]), (int(e[1]), int(e[2])), (int(e[3]), int(e[4])), int(e[5]))
+                   for e in ent]
+        h = ScheduledFaultHook(FaultSchedule(entries))
+        r2, rep2 = P.checked_assign(xx, yy, cfg=cfg, hook=h)
+        assert np.array_equal(r2.assignments, z[f"{n}_lab"]), n
+        assert r2.min_dists.tobytes() == z[f"{n}_val"].tobytes(), n
+        ev = np.array([[e.iteration, e.tile[0], e.tile[1],
+                        0 if e.kind == "detected-corrected" else 1, e.loc[0], e.loc[1]]
+                       for e in rep2.events], np.int64).reshape(-1, 6)
+        assert ev.tolist() == z[f"{n}_ev"].tolist(), n
+        inj = np.array([[d["before"], d["after"]] for d in h.injected]).reshape(-1, 2)
+        assert inj.tobytes() == z[f"{n}_inj"].tobytes(), n
+        # the tensor-core checksum itself saw the above-threshold flips
+        assert E.tc_fallback_rows()[2] >= 1, n
