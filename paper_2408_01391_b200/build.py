@@ -22,6 +22,7 @@ SOURCES = {
     "exact.cu": ["--fmad=false"],
     "update.cu": ["--fmad=false"],
     "tc.cu": [],
+    "tc_pair.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

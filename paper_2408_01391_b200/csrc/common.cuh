@@ -70,6 +70,8 @@ enum ScratchSlot {
     SLOT_TC_CSUM1 = 15,
     SLOT_TC_CSUM2 = 16,
     SLOT_TC_INJROWS = 17,
+    SLOT_PAIR_FB = 18,    // pass-1 thresholds + seeds
+    SLOT_PAIR_CAND = 19,  // pass-2 candidate list, keys, counters
 };
 
 // ------------------------------------------------------- float helpers --

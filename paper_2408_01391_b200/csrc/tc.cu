@@ -42,6 +42,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "tc_pair.cuh"
 
 namespace ftk {
 
@@ -680,7 +681,10 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 
-static unsigned g_last_fb[3] = {0, 0, 0};  // pass-1 / pass-2 uncertified, TC ABFT flags
+static unsigned g_last_fb[3] = {0, 0, 0};
+static int g_last_path = 0;  // pass-1 kernel of the last call: 0 single-CTA, 1 CTA pair
+
+  // pass-1 / pass-2 uncertified, TC ABFT flags
 
 struct TcFt {          // checksum-protected (abft) mode
     double delta_rel, abs_tol;
@@ -812,6 +816,8 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         }
     }
     CUtensorMap mx, mc;
+    float *pair_fb_thr = nullptr;
+    unsigned long long *pair_fb_seed = nullptr;
     int rc = make_map(&mc, yf, k, d, uint32_t(bn));
     if (rc) return rc;
     unsigned n1 = unsigned(m);
@@ -829,7 +835,49 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             P.camax = camax1;
             P.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));
         }
-        rc = screen<false>(bn, P, mx, mx, mc, mc, st);
+        const char *pe = getenv("FTK_TC_PAIR");
+        if (!(pe && atoi(pe) == 0) && d <= TC_MAX_D && raw == nullptr) {
+            // CTA-pair kernel (tc_pair.cu): M = 256 per cluster, half the L2 traffic
+            CUtensorMap mc128;
+            if ((rc = make_map(&mc128, yf, k, d, PAIR_BN / 2))) return rc;
+            PairParams Q{};
+            Q.y = yf; Q.yn = ynf; Q.m = m; Q.k = k; Q.d = d;
+            Q.a_coef = P.a_coef; Q.b_coef = P.b_coef; Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
+            Q.out_idx = out_idx; Q.out_val = outv; Q.fb_rows = rows1; Q.fb_count = cnt;
+            Q.csum = P.csum; Q.camax = P.camax; Q.tau_coef = P.tau_coef; Q.tau_abs = P.tau_abs;
+            Q.inj_col = P.inj_col; Q.inj_before = P.inj_before; Q.inj_after = P.inj_after;
+            Q.abft_count = P.abft_count;
+            Q.dbg = P.dbg;
+            {
+                char *fb = static_cast<char *>(scratch(ctx, SLOT_PAIR_FB, (sizeof(float) + 8) * size_t(m + 1) + 64, st));
+                if (!fb) return FTK_ERR_CUDA;
+                Q.fb_seed = reinterpret_cast<unsigned long long *>(fb);
+                Q.fb_thr = reinterpret_cast<float *>(fb + 8 * size_t(m + 1));
+                pair_fb_thr = Q.fb_thr;
+                pair_fb_seed = Q.fb_seed;
+            }
+            static long long *dclk = nullptr;  // FTK_PAIR_CLK=1: role timing printed to stderr
+            const char *ce = getenv("FTK_PAIR_CLK");
+            if (ce && atoi(ce)) {
+                if (!dclk) cudaMalloc(&dclk, 6 * sizeof(long long));
+                cudaMemsetAsync(dclk, 0, 6 * sizeof(long long), st);
+                Q.clk = dclk;
+            }
+            rc = pair_screen_launch(mx, mc128, Q, ft != nullptr, st);
+            g_last_path = 1;
+            if (Q.clk) {
+                long long h[6];
+                cudaMemcpyAsync(h, Q.clk, sizeof(h), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                fprintf(stderr, "pair clk: screen busy %.0f wait %.0f per tile (%lld tiles); "
+                        "mma wait t_empty %.0f full %.0f a_full %.0f per tile\n",
+                        double(h[0]) / h[5], double(h[1]) / h[5], h[5], 2.0 * h[2] / h[5],
+                        2.0 * h[3] / h[5], 2.0 * h[4] / h[5]);
+            }
+        } else {
+            rc = screen<false>(bn, P, mx, mx, mc, mc, st);
+            g_last_path = 0;
+        }
         if (rc) return rc;
         FTK_CUDA(cudaMemcpyAsync(&n1, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         FTK_CUDA(cudaStreamSynchronize(st));
@@ -837,7 +885,59 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     }
     g_last_fb[0] = n1;
     g_last_fb[1] = 0;
-    if (n1 > 0) {
+    if (n1 > 0 && pair_fb_thr && !split_only) {
+        // ---------------- pass 2 (CTA-pair path): 1xTF32 re-screen of the
+        // gathered uncertified rows collecting every centroid whose screened
+        // value can still beat the row's exact d1, then exact evaluation of
+        // those candidates only; rows with too many candidates go exact
+        const unsigned row_cap = 256;
+        const unsigned cap = unsigned(std::min<int64_t>(int64_t(n1) * 16 + 65536, int64_t(1) << 30));
+        const size_t gbytes = (sizeof(float) * size_t(n1) * d + 255) & ~size_t(255);
+        const size_t need = gbytes + sizeof(int2) * cap + 8 * size_t(n1) + 4 * size_t(n1) + 256;
+        char *buf = static_cast<char *>(scratch(ctx, SLOT_PAIR_CAND, need, st));
+        if (!buf) return FTK_ERR_CUDA;
+        float *g = reinterpret_cast<float *>(buf);
+        int2 *cand = reinterpret_cast<int2 *>(buf + gbytes);
+        unsigned long long *key = reinterpret_cast<unsigned long long *>(cand + cap);
+        unsigned *row_cnt = reinterpret_cast<unsigned *>(key + n1);
+        unsigned *ccount = row_cnt + n1;  // [0] candidates, [1] rows left for the exact kernel
+        FTK_CUDA(cudaMemsetAsync(row_cnt, 0, sizeof(unsigned) * (size_t(n1) + 2), st));
+        FTK_CUDA(cudaMemcpyAsync(key, pair_fb_seed, 8 * size_t(n1), cudaMemcpyDeviceToDevice, st));
+        gather_rows_kernel<<<148 * 8, 256, 0, st>>>(xf, d, rows1, cnt, g, nullptr);
+        FTK_LAUNCHED("gather_rows_kernel");
+        CUtensorMap mg, mc64;
+        if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mc64, yf, k, d, PAIR_BN / 2)))
+            return rc;
+        PairParams Q{};
+        Q.y = yf; Q.yn = ynf; Q.m = n1; Q.k = k; Q.d = d;
+        Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
+        Q.thr = pair_fb_thr;
+        Q.cand = cand;
+        Q.cand_count = ccount;
+        Q.cand_cap = cap;
+        Q.row_cnt = row_cnt;
+        if ((rc = pair_screen_launch(mg, mc64, Q, false, st))) return rc;
+        if ((rc = pair_candidates_run(g, yf, ynf, d, cand, ccount, cap, row_cnt, row_cap, key, rows1,
+                                      cnt, out_idx, outv, rows2, ccount + 1, st)))
+            return rc;
+        unsigned n2 = 0;
+        FTK_CUDA(cudaMemcpyAsync(&n2, ccount + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        FTK_CUDA(cudaStreamSynchronize(st));
+        g_last_fb[1] = n2;
+        if (n2 > 0) {
+            float *g2 = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * (size_t(n2) * (d + 2)) + 64, st));
+            if (!g2) return FTK_ERR_CUDA;
+            gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, ccount + 1, g2, nullptr);
+            FTK_LAUNCHED("gather_rows_kernel");
+            int32_t *idx2 = reinterpret_cast<int32_t *>(g2 + size_t(n2) * d);
+            float *val2 = g2 + size_t(n2) * d + n2;
+            rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 8, 256, 16, idx2, val2, nullptr,
+                           false, 0.0, 0.0, 0, nullptr, nullptr, st);
+            if (rc) return rc;
+            scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, ccount + 1, idx2, val2, out_idx, outv);
+            FTK_LAUNCHED("scatter_rows_kernel");
+        }
+    } else if (n1 > 0) {
         // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
         float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
         if (!g) return FTK_ERR_CUDA;

@@ -1,0 +1,55 @@
+// tc_pair.cuh -- parameters and launcher of the CTA-pair screen (tc_pair.cu)
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ftk {
+
+// centroids per accumulator tile (the TMEM holds 512 / PAIR_BN buffers);
+// each CTA of the pair loads PAIR_BN / 2 centroid rows per k-block
+constexpr int PAIR_BN = 256;
+
+struct PairParams {
+    const float *y, *yn;
+    int64_t m, k, d;
+    int nkb, ntiles, stages, abufs;
+    float a_coef, b_coef;
+    const float *cmax2, *ecmax2;
+    int32_t *out_idx;
+    float *out_val;
+    int32_t *fb_rows;
+    unsigned *fb_count;
+    // ABFT
+    const float *csum, *camax;
+    float tau_coef, tau_abs;
+    const int32_t *inj_col;
+    const float *inj_before, *inj_after;
+    unsigned *abft_count;
+    // pass 1: per uncertified row, the pass-2 threshold and the (d1, j1) seed key
+    float *fb_thr;
+    unsigned long long *fb_seed;
+    // pass 2 (COLLECT mode, thr != null): rows are the gathered uncertified
+    // rows; every column with s_j <= thr[row] is appended to cand
+    const float *thr;
+    int2 *cand;
+    unsigned *cand_count;
+    unsigned cand_cap;
+    unsigned *row_cnt;
+    long long *clk;  // debug: per-role clock64 sums (screen busy/wait, MMA waits), or null
+    int dbg;  // bit 0: skip the screen math, bit 1: skip the refine (pipeline timing only)
+};
+
+int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams P, bool chk,
+                       cudaStream_t st);
+
+}  // namespace ftk
+
+namespace ftk {
+int pair_candidates_run(const float *g, const float *y, const float *yn, int64_t d,
+                        const int2 *cand, const unsigned *count, unsigned cap,
+                        const unsigned *row_cnt, unsigned row_cap, unsigned long long *key,
+                        const int32_t *rows, const unsigned *n_rows, int32_t *out_idx,
+                        float *out_val, int32_t *rows2, unsigned *n2, cudaStream_t st);
+}  // namespace ftk

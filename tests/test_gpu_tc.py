@@ -56,7 +56,7 @@ def test_tc_blobs(d, k):
     assert fb[1] < 0.01 * 20000, fb  # the 3xTF32 re-screen certifies nearly every tie
 
 
-def test_tc_ties_go_to_exact():
+def test_tc_ties_resolved_exactly():
     rng = np.random.default_rng(3)
     y = np.ascontiguousarray(rng.standard_normal((40, 32)), dtype=np.float32)
     y[7] = y[3]  # exact duplicate centroid: every row nearest to it is a tie
@@ -66,7 +66,9 @@ def test_tc_ties_go_to_exact():
     ref_lab, ref_val = O.assign(x, y)
     assert np.array_equal(lab, ref_lab) and set(lab.tolist()) == {3}
     assert val.tobytes() == ref_val.tobytes()
-    assert fb[1] >= 50
+    # no screen can certify an exact tie: every row takes the exact path
+    # (the candidate evaluation of the CTA-pair pass 2, or the exact kernel)
+    assert fb[0] >= 50
 
 
 def _tf32(a):
