@@ -18,6 +18,7 @@
 
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <functional>
 #include <map>
 #include <mutex>
@@ -178,11 +179,15 @@ __global__ void seg_count_kernel(const int64_t *counts, int64_t k, int64_t *nseg
         nseg[c] = (counts[c] + SEG - 1) / SEG;
 }
 
-template <typename T, bool DMR>
+// Per segment and feature: the float64 partial sum of the segment's members
+// (in member order), max |v| and min (|v| bits - 1) -- the smallest nonzero
+// magnitude, whose exponent bounds the ulp exponent of every value.  Two
+// features per thread with 8-byte loads; ~8 instructions per element.
+template <bool DMR>
 __global__ void __launch_bounds__(128) seg_partials_kernel(
-    const T *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
+    const float *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
     int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
-    __shared__ int32_t rows[SEG];
+    __shared__ int64_t rowoff[SEG];
     __shared__ int64_t info[3];
     const int64_t s = blockIdx.x;
     if (threadIdx.x == 0) {
@@ -204,36 +209,119 @@ __global__ void __launch_bounds__(128) seg_partials_kernel(
     if (info[0] < 0) return;
     const int64_t beg = info[1];
     const int n = int(info[2]);
-    for (int t = threadIdx.x; t < n; t += blockDim.x) rows[t] = perm[beg + t];
+    for (int t = threadIdx.x; t < n; t += blockDim.x) rowoff[t] = int64_t(perm[beg + t]) * d;
     __syncthreads();
-    for (int64_t f = threadIdx.x; f < d; f += blockDim.x) {
-        double a = 0.0, b = 0.0, ab = 0.0;
-        int q = INT_MAX;
-        constexpr int U = 16;
+    const bool pairs = (d & 1) == 0;
+    const int64_t nf = pairs ? d / 2 : d;
+    for (int64_t f = threadIdx.x; f < nf; f += blockDim.x) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+        uint32_t mx0 = 0, mx1 = 0, mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
+        constexpr int U = 8;
         int t = 0;
-        for (; t + U <= n; t += U) {
-            double v[U];
+        if (pairs) {
+            const float *xb = x + 2 * f;
+            for (; t < n; t += U) {
+                float2 v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = double(x[int64_t(rows[t + u]) * d + f]);
+                for (int u = 0; u < U; ++u)
+                    v[u] = (t + u < n) ? *reinterpret_cast<const float2 *>(xb + rowoff[t + u])
+                                       : make_float2(0.f, 0.f);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                a = __dadd_rn(a, v[u]);
-                if (DMR) b = __dadd_rn(b, v[u]);
-                ab = __dadd_rn(ab, fabs(v[u]));
-                if (v[u] != 0.0) q = min(q, ulp_exp<T>(T(v[u])));
+                for (int u = 0; u < U; ++u) {
+                    a0 = __dadd_rn(a0, double(v[u].x));
+                    a1 = __dadd_rn(a1, double(v[u].y));
+                    if (DMR) {
+                        b0 = __dadd_rn(b0, double(v[u].x));
+                        b1 = __dadd_rn(b1, double(v[u].y));
+                    }
+                    const uint32_t u0 = __float_as_uint(v[u].x) & 0x7FFFFFFFu;
+                    const uint32_t u1 = __float_as_uint(v[u].y) & 0x7FFFFFFFu;
+                    mx0 = max(mx0, u0);
+                    mx1 = max(mx1, u1);
+                    mn0 = min(mn0, u0 - 1u);  // zeros wrap to 0xFFFFFFFF: ignored
+                    mn1 = min(mn1, u1 - 1u);
+                }
+            }
+        } else {
+            for (; t < n; ++t) {
+                const float v = x[rowoff[t] + f];
+                a0 = __dadd_rn(a0, double(v));
+                if (DMR) b0 = __dadd_rn(b0, double(v));
+                const uint32_t u0 = __float_as_uint(v) & 0x7FFFFFFFu;
+                mx0 = max(mx0, u0);
+                mn0 = min(mn0, u0 - 1u);
             }
         }
-        for (; t < n; ++t) {
-            const double v = double(x[int64_t(rows[t]) * d + f]);
-            a = __dadd_rn(a, v);
-            if (DMR) b = __dadd_rn(b, v);
-            ab = __dadd_rn(ab, fabs(v));
-            if (v != 0.0) q = min(q, ulp_exp<T>(T(v)));
+        // q = exponent of the ulp of the smallest nonzero magnitude (a lower
+        // bound of every value's ulp exponent); bound = n * max|v|
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !pairs) break;
+            const int64_t ff = pairs ? 2 * f + h : f;
+            const uint32_t mn = h ? mn1 : mn0, mx = h ? mx1 : mx0;
+            int q = INT_MAX;
+            if (mn != 0xFFFFFFFFu) {
+                const int e = int((mn + 1u) >> 23);
+                q = (e == 0 ? 1 : e) - 150;
+            }
+            ps_a[s * d + ff] = h ? a1 : a0;
+            if (DMR) ps_b[s * d + ff] = h ? b1 : b0;
+            ps_abs[s * d + ff] = double(n) * double(__uint_as_float(mx));
+            ps_q[s * d + ff] = q;
         }
-        ps_a[s * d + f] = a;
-        if (DMR) ps_b[s * d + f] = b;
-        ps_abs[s * d + f] = ab;
-        ps_q[s * d + f] = q;
+    }
+}
+
+// Fold one (cluster, feature) chain.  If every value of the chain is a
+// multiple of 2^q and sum |v| < 2^(53+q), every partial sum of the
+// reference's sequential chain is an exact float64 number, so the segment
+// partials combined in any order give the reference's bits.  Chains that
+// fail (values of tiny magnitude next to large sums) are queued for
+// seg_replay_kernel, which recomputes them in member order.
+template <bool DMR>
+__global__ void seg_fold_kernel(const int64_t *seg_base, int64_t k, int64_t d,
+                                const double *ps_a, const double *ps_b, const double *ps_abs,
+                                const int32_t *ps_q, double *sums_a, double *sums_b,
+                                int64_t *fail_list, unsigned *fail_count) {
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < k * d;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c = e / d, f = e % d;
+        const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+        double a = 0.0, b = 0.0, bnd = 0.0;
+        int q = INT_MAX;
+        int64_t s = s0;
+        constexpr int U = 4;
+        for (; s + U <= s1; s += U) {
+            double pa[U], pb[U], pn[U];
+            int pq[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                pa[u] = ps_a[(s + u) * d + f];
+                if (DMR) pb[u] = ps_b[(s + u) * d + f];
+                pn[u] = ps_abs[(s + u) * d + f];
+                pq[u] = ps_q[(s + u) * d + f];
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                a = __dadd_rn(a, pa[u]);
+                if (DMR) b = __dadd_rn(b, pb[u]);
+                bnd = __dadd_rn(bnd, pn[u]);
+                q = min(q, pq[u]);
+            }
+        }
+        for (; s < s1; ++s) {
+            a = __dadd_rn(a, ps_a[s * d + f]);
+            if (DMR) b = __dadd_rn(b, ps_b[s * d + f]);
+            bnd = __dadd_rn(bnd, ps_abs[s * d + f]);
+            q = min(q, ps_q[s * d + f]);
+        }
+        const bool exact = q == INT_MAX || (q > -1000 && bnd * (1.0 + 0x1p-20) < ldexp(1.0, 53 + q));
+        if (exact) {
+            sums_a[e] = a;
+            if (DMR) sums_b[e] = b;
+        } else {
+            fail_list[atomicAdd(fail_count, 1u)] = e;
+        }
     }
 }
 
@@ -247,60 +335,67 @@ __device__ __forceinline__ int lowbit_exp(double s) {
     return int(ef == 0 ? 1 : ef) - 1075 + __ffsll((long long)mant) - 1;
 }
 
-// Fold the segments of one (cluster, feature) chain in member order.  A
-// segment whose values, joined to the running sum s, satisfy the exactness
-// certificate (|s| + sum|v| < 2^(53+q), q = min ulp exponent of s and of the
-// segment's values) contributes its precomputed partial exactly; a segment
-// that fails is re-walked member by member from s -- the reference's chain.
-template <typename T, bool DMR>
-__global__ void seg_fold_kernel(const T *x, int64_t d, const int32_t *perm,
-                                const int64_t *offsets, const int64_t *seg_base, int64_t k,
-                                const double *ps_a, const double *ps_b, const double *ps_abs,
-                                const int32_t *ps_q, double *sums_a, double *sums_b) {
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < k * d;
-         e += int64_t(gridDim.x) * blockDim.x) {
+// One block per failing chain.  The leading segments whose partial sums
+// provably join the running sum exactly (per-segment certificate against the
+// running sum's lowest set bit) are folded directly; from the first segment
+// that fails on, the block stages member values in shared memory and one
+// thread runs the reference's sequential float64 chain.
+template <bool DMR>
+__global__ void __launch_bounds__(256) seg_replay_kernel(
+    const float *x, int64_t d, const int32_t *perm, const int64_t *offsets,
+    const int64_t *seg_base, const double *ps_a, const double *ps_b, const double *ps_abs,
+    const int32_t *ps_q, const int64_t *fail_list, const unsigned *fail_count, double *sums_a,
+    double *sums_b) {
+    constexpr int TILE = 2048;
+    __shared__ float vals[TILE];
+    __shared__ double run[2];
+    __shared__ int64_t start;
+    const unsigned nfail = *fail_count;
+    for (unsigned w = blockIdx.x; w < nfail; w += gridDim.x) {
+        const int64_t e = fail_list[w];
         const int64_t c = e / d, f = e % d;
-        const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
-        double a = 0.0, b = 0.0;
-        for (int64_t s = s0; s < s1; ++s) {
-            const int qseg = ps_q[s * d + f];
-            if (qseg == INT_MAX) continue;                 // all-zero segment: s + 0 == s
-            if (s == s0) {                                  // chain from 0 == the partial itself
-                a = ps_a[s * d + f];
-                if (DMR) b = ps_b[s * d + f];
-                continue;
-            }
-            const int qa = lowbit_exp(a);
-            const int q = qa < qseg ? qa : qseg;
-            const double bound = fabs(a) + ps_abs[s * d + f] * (1.0 + 0x1p-20);
-            const bool exact = q == INT_MAX || (q > -1000 && bound < ldexp(1.0, 53 + q));
-            if (exact && (!DMR || a == b)) {
+        if (threadIdx.x == 0) {
+            const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+            double a = 0.0, b = 0.0;
+            int64_t s = s0;
+            for (; s < s1; ++s) {
+                const int qseg = ps_q[s * d + f];
+                if (qseg == INT_MAX) continue;  // all-zero segment
+                const int qa = lowbit_exp(a);
+                const int q = qa < qseg ? qa : qseg;
+                const double bound = fabs(a) + ps_abs[s * d + f] * (1.0 + 0x1p-20);
+                if (!(q > -1000 && bound < ldexp(1.0, 53 + q)) || (DMR && a != b)) break;
                 a = __dadd_rn(a, ps_a[s * d + f]);
                 if (DMR) b = __dadd_rn(b, ps_b[s * d + f]);
-            } else {
-                const int64_t lo = offsets[c] + (s - s0) * SEG;
-                const int64_t hi = lo + SEG < offsets[c + 1] ? lo + SEG : offsets[c + 1];
-                constexpr int U = 16;
-                int64_t t = lo;
-                for (; t + U <= hi; t += U) {
-                    double v[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) v[u] = double(x[int64_t(perm[t + u]) * d + f]);
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        a = __dadd_rn(a, v[u]);
-                        if (DMR) b = __dadd_rn(b, v[u]);
-                    }
-                }
-                for (; t < hi; ++t) {
-                    const double v = double(x[int64_t(perm[t]) * d + f]);
+            }
+            run[0] = a;
+            run[1] = b;
+            start = offsets[c] + (s - s0) * SEG;
+        }
+        __syncthreads();
+        const int64_t hi = offsets[c + 1];
+        for (int64_t t0 = start; t0 < hi; t0 += TILE) {
+            const int n = int(hi - t0 < TILE ? hi - t0 : TILE);
+            for (int t = threadIdx.x; t < n; t += blockDim.x)
+                vals[t] = x[int64_t(perm[t0 + t]) * d + f];
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double a = run[0], b = run[1];
+                for (int t = 0; t < n; ++t) {
+                    const double v = double(vals[t]);
                     a = __dadd_rn(a, v);
                     if (DMR) b = __dadd_rn(b, v);
                 }
+                run[0] = a;
+                run[1] = b;
             }
+            __syncthreads();
         }
-        sums_a[e] = a;
-        if (DMR) sums_b[e] = b;
+        if (threadIdx.x == 0) {
+            sums_a[e] = run[0];
+            if (DMR) sums_b[e] = run[1];
+        }
+        __syncthreads();
     }
 }
 
@@ -688,21 +783,33 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(nseg, k, seg_base);
         FTK_LAUNCHED("exclusive_scan_small_kernel");
         auto xx = static_cast<const float *>(x);
+        int64_t *fail_list = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_FB, sizeof(int64_t) * (k * d + 2), st));
+        if (!fail_list) return FTK_ERR_CUDA;
+        unsigned *fail_count = reinterpret_cast<unsigned *>(fail_list + k * d);
+        FTK_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(unsigned), st));
+        const unsigned rgrid = unsigned(std::min<int64_t>(k * d, 148 * 8));
         if (dmr) {
-            seg_partials_kernel<float, true><<<unsigned(max_seg), 128, 0, st>>>(
+            seg_partials_kernel<true><<<unsigned(max_seg), 128, 0, st>>>(
                 xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<float, true><<<grid_for(k * d, 128), 128, 0, st>>>(
-                xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b);
+            seg_fold_kernel<true><<<grid_for(k * d, 128), 128, 0, st>>>(
+                seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count);
+            FTK_LAUNCHED("seg_fold_kernel");
+            seg_replay_kernel<true><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
+                                                          ps_b, ps_abs, ps_q, fail_list, fail_count,
+                                                          sums_a, sums_b);
         } else {
-            seg_partials_kernel<float, false><<<unsigned(max_seg), 128, 0, st>>>(
+            seg_partials_kernel<false><<<unsigned(max_seg), 128, 0, st>>>(
                 xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<float, false><<<grid_for(k * d, 128), 128, 0, st>>>(
-                xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q, sums_a,
-                nullptr);
+            seg_fold_kernel<false><<<grid_for(k * d, 128), 128, 0, st>>>(
+                seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count);
+            FTK_LAUNCHED("seg_fold_kernel");
+            seg_replay_kernel<false><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
+                                                           nullptr, ps_abs, ps_q, fail_list,
+                                                           fail_count, sums_a, nullptr);
         }
-        FTK_LAUNCHED("seg_fold_kernel");
+        FTK_LAUNCHED("seg_replay_kernel");
         return FTK_OK;
     }
     if (dtype == FTK_F32) {
