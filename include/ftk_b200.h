@@ -79,6 +79,18 @@ int64_t ftk_launch_count(void);
 ftk_ctx *ftk_ctx_create(int device);
 void ftk_ctx_destroy(ftk_ctx *ctx);
 
+/* Per-row screening bounds of an fp32 matrix, info: m x 4 floats per row
+ * (sum x^2, sum (x - tf32(x))^2, max |x|, 0), any summation order (they only
+ * feed upper bounds).  Used by the tensor-core assignment certificate. */
+int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info, void *stream);
+
+/* Register precomputed row bounds (ftk_row_info) for the data matrix x of a
+ * fit: assignment calls with exactly this (x, m, d) read them instead of
+ * recomputing them from x every call.  The caller guarantees x is not
+ * modified while registered; pass x = NULL to unregister.  The reference has
+ * no counterpart (its kernels recompute nothing across calls). */
+int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info);
+
 /* out[i] = left-to-right sum of x[i,j]^2 in the data dtype. */
 int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,
                      void *stream);

@@ -10,6 +10,7 @@ import numpy as np
 from . import _native as N
 
 _CTX = {}
+_ROWS_OWNER = {}  # device -> id of the RowInfo registered on its context
 _VARIANT = {"auto": N.VARIANT_AUTO, "exact": N.VARIANT_EXACT, "tc": N.VARIANT_TC}
 
 
@@ -164,6 +165,39 @@ def row_sq_norms_dev(x_t):
     N.check(N.load().ftk_row_sq_norms(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), x_t.shape[0],
                                       x_t.shape[1], ptr(out), stream()), "ftk_row_sq_norms")
     return out
+
+
+class RowInfo:
+    """Per-fit screening bounds of an fp32 data matrix (ftk_row_info),
+    registered on the context for the lifetime of a fit (ftk_ctx_set_rows);
+    ``close`` unregisters them before the data can be freed or modified."""
+
+    def __init__(self, x_t):
+        t = _torch()
+        self.x_t = x_t
+        self.info = None
+        if x_t.dtype != t.float32 or x_t.shape[0] == 0:
+            return
+        m, d = x_t.shape
+        self.info = t.empty((m, 4), dtype=t.float32, device=x_t.device)
+        lib = N.load()
+        N.check(lib.ftk_row_info(ctx(), ptr(x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
+        N.check(lib.ftk_ctx_set_rows(ctx(), ptr(x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
+        _ROWS_OWNER[x_t.device.index] = id(self)
+
+    def close(self):
+        if self.info is not None:
+            dev = self.x_t.device.index
+            if _ROWS_OWNER.get(dev) == id(self):  # a later fit may own the slot now
+                N.load().ftk_ctx_set_rows(ctx(), None, 0, 0, None)
+                _ROWS_OWNER.pop(dev, None)
+            self.info = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def row_sq_norms(x):

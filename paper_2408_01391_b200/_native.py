@@ -38,6 +38,8 @@ PROTOTYPES = {
     "ftk_ctx_create": (_p, [_int]),
     "ftk_ctx_destroy": (None, [_p]),
     "ftk_row_sq_norms": (_int, [_p, _int, _p, _i64, _i64, _p, _p]),
+    "ftk_row_info": (_int, [_p, _p, _i64, _i64, _p, _p]),
+    "ftk_ctx_set_rows": (_int, [_p, _p, _i64, _i64, _p]),
     "ftk_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p,
                           _p, _p]),
     "ftk_checked_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,

@@ -44,6 +44,7 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 int row_sq_norms_run(int, const void *, int64_t, int64_t, void *, cudaStream_t);
+int row_info_run(const float *, int64_t, int64_t, float *, cudaStream_t);
 int update_sums_run(ftk_ctx *, int, const void *, const int32_t *, int64_t, int64_t, int64_t,
                     double *, int64_t *, double *, int64_t *, cudaStream_t);
 int dmr_compare_run(const double *, const int64_t *, const double *, const int64_t *, int64_t,
@@ -98,6 +99,20 @@ void ftk_ctx_destroy(ftk_ctx *ctx) {
     for (auto &s : ctx->slots)
         if (s.ptr) cudaFree(s.ptr);
     delete ctx;
+}
+
+int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info, void *stream) {
+    if (!ctx || d < 1 || m < 0) { set_error("bad ctx/shape"); return FTK_ERR_ARG; }
+    return row_info_run(x, m, d, info, as_stream(stream));
+}
+
+int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info) {
+    if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    ctx->rows_x = x;
+    ctx->rows_m = x ? m : 0;
+    ctx->rows_d = x ? d : 0;
+    ctx->rows_info = x ? info : nullptr;
+    return FTK_OK;
 }
 
 int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,

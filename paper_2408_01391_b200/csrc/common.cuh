@@ -45,6 +45,10 @@ struct Scratch {
 struct ftk_ctx {
     int device = 0;
     ftk::Scratch slots[24];
+    // per-fit row bounds registered by ftk_ctx_set_rows (X constant for the fit)
+    const void *rows_x = nullptr;
+    int64_t rows_m = 0, rows_d = 0;
+    const float *rows_info = nullptr;  // m x 4: |x|^2, |x - tf32(x)|^2, max|x|, 0
 };
 
 namespace ftk {

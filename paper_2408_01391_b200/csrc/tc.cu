@@ -426,6 +426,37 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // --------------------------------------------------------- small kernels --
+// Per-row bounds for the screen certificate (one warp per row, any order).
+__global__ void row_info_kernel(const float *x, int64_t m, int64_t d, float4 *info) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = w0; i < m; i += nw) {
+        float xx = 0.0f, ee = 0.0f, am = 0.0f;
+        for (int64_t f = lane; f < d; f += 32) {
+            const float v = x[i * d + f];
+            const float r = v - tf32_trunc(v);
+            xx = fmaf(v, v, xx);
+            ee = fmaf(r, r, ee);
+            am = fmaxf(am, fabsf(v));
+        }
+        for (int off = 16; off; off >>= 1) {
+            xx += __shfl_xor_sync(0xffffffffu, xx, off);
+            ee += __shfl_xor_sync(0xffffffffu, ee, off);
+            am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, off));
+        }
+        if (lane == 0) info[i] = make_float4(xx, ee, am, 0.0f);
+    }
+}
+
+int row_info_run(const float *x, int64_t m, int64_t d, float *info, cudaStream_t st) {
+    if (m == 0) return FTK_OK;
+    const int64_t blocks = std::min<int64_t>((m + 7) / 8, 148 * 16);
+    row_info_kernel<<<unsigned(blocks), 256, 0, st>>>(x, m, d, reinterpret_cast<float4 *>(info));
+    FTK_LAUNCHED("row_info_kernel");
+    return FTK_OK;
+}
+
 // Upper bounds of max_j ||c_j||^2 (from the exact fp32 norms) and of
 // max_j ||c_j - tf32(c_j)||^2: one warp per centroid row, float maxima via
 // integer atomicMax (non-negative floats order like their bit patterns).
@@ -453,31 +484,52 @@ __global__ void tc_prep_kernel(const float *y, const float *yn, int64_t k, int64
     }
 }
 
-// FT mode: per N-tile checksum centroid sum_j tf32(c_j) (float64 sum, then
-// fp32) zero-padded to nkb*32 features, and the tile's max |c|.
-__global__ void tile_csum_kernel(const float *y, int64_t k, int64_t d, int bn, int nkb,
-                                 int trunc, float *csum, float *camax) {
-    const int64_t t = blockIdx.x;
-    const int64_t j0 = t * bn, j1 = j0 + bn < k ? j0 + bn : k;
+// FT mode: checksum centroid sum_j tf32(c_j) (float64 sum in a fixed tree
+// order, then fp32) zero-padded to nkb*32 features, and max |c| (one block
+// per feature; the last block to finish folds the per-feature maxima).
+__global__ void tile_csum_kernel(const float *y, int64_t k, int64_t d, int nkb, int trunc,
+                                 float *csum, float *camax, float *fmax, unsigned *done) {
+    const int64_t f = blockIdx.x;  // 0 .. nkb*32-1
+    double s = 0.0;
     float am = 0.0f;
-    for (int64_t f = threadIdx.x; f < int64_t(nkb) * 32; f += blockDim.x) {
-        double s = 0.0;
-        if (f < d)
-            for (int64_t j = j0; j < j1; ++j) {
-                const float v = y[j * d + f];
-                s += double(trunc ? tf32_trunc(v) : v);  // 3xTF32 pass: ~exact operands
-                am = fmaxf(am, fabsf(v));
-            }
-        csum[t * nkb * 32 + f] = float(s);
+    if (f < d)
+        for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+            const float v = y[j * d + f];
+            s += double(trunc ? tf32_trunc(v) : v);  // 3xTF32 pass: ~exact operands
+            am = fmaxf(am, fabsf(v));
+        }
+    __shared__ double sh[32];
+    __shared__ float shm[32];
+    for (int off = 16; off; off >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, off);
+        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, off));
     }
-    for (int off = 16; off; off >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, off));
-    __shared__ float sh[32];
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = am;
+    if ((threadIdx.x & 31) == 0) {
+        sh[threadIdx.x >> 5] = s;
+        shm[threadIdx.x >> 5] = am;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
+        double t = 0.0;
         float m = 0.0f;
-        for (int w = 0; w < int(blockDim.x / 32); ++w) m = fmaxf(m, sh[w]);
-        camax[t] = m;
+        for (int w = 0; w < int(blockDim.x / 32); ++w) {
+            t += sh[w];
+            m = fmaxf(m, shm[w]);
+        }
+        csum[f] = float(t);
+        fmax[f] = m;
+        __threadfence();
+        if (atomicAdd(done, 1u) == gridDim.x - 1) {  // last block: global max
+            __threadfence();
+            float g = 0.0f, n2 = 0.0f;
+            for (int64_t q = 0; q < gridDim.x; ++q) {
+                g = fmaxf(g, fmax[q]);
+                n2 = fmaf(csum[q], csum[q], n2);
+            }
+            camax[0] = g;
+            camax[2] = n2;  // |csum|^2 (bounds the fp32 reference error)
+            *done = 0;
+        }
     }
 }
 
@@ -696,13 +748,15 @@ struct TcFt {          // checksum-protected (abft) mode
 // FT mode helpers: checksum centroids for a given N tiling
 static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb,
                      int trunc, float **csum, float **camax, cudaStream_t st) {
-    const int64_t nt = 1;  // one checksum centroid over all K centroids
-    const int bn = int(k);
-    float *buf = static_cast<float *>(scratch(ctx, slot, sizeof(float) * (nt * nkb * 32 + nt + 64), st));
+    const int64_t nf = int64_t(nkb) * 32;
+    float *buf = static_cast<float *>(scratch(ctx, slot, sizeof(float) * (2 * nf + 64), st));
     if (!buf) return FTK_ERR_CUDA;
     *csum = buf;
-    *camax = buf + nt * nkb * 32;
-    tile_csum_kernel<<<unsigned(nt), 128, 0, st>>>(y, k, d, bn, nkb, trunc, *csum, *camax);
+    *camax = buf + nf;
+    float *fmax = buf + nf + 32;
+    unsigned *done = reinterpret_cast<unsigned *>(buf + nf + 1);
+    FTK_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
+    tile_csum_kernel<<<unsigned(nf), 256, 0, st>>>(y, k, d, nkb, trunc, *csum, *camax, fmax, done);
     FTK_LAUNCHED("tile_csum_kernel");
     return FTK_OK;
 }
@@ -841,13 +895,15 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             CUtensorMap mc128;
             if ((rc = make_map(&mc128, yf, k, d, PAIR_BN / 2))) return rc;
             PairParams Q{};
-            Q.y = yf; Q.yn = ynf; Q.m = m; Q.k = k; Q.d = d;
+            Q.x = xf; Q.y = yf; Q.yn = ynf; Q.m = m; Q.k = k; Q.d = d;
             Q.a_coef = P.a_coef; Q.b_coef = P.b_coef; Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
             Q.out_idx = out_idx; Q.out_val = outv; Q.fb_rows = rows1; Q.fb_count = cnt;
             Q.csum = P.csum; Q.camax = P.camax; Q.tau_coef = P.tau_coef; Q.tau_abs = P.tau_abs;
             Q.inj_col = P.inj_col; Q.inj_before = P.inj_before; Q.inj_after = P.inj_after;
             Q.abft_count = P.abft_count;
             Q.dbg = P.dbg;
+            if (ctx->rows_info && ctx->rows_x == x && ctx->rows_m == m && ctx->rows_d == d)
+                Q.rowinfo = reinterpret_cast<const float4 *>(ctx->rows_info);
             {
                 char *fb = static_cast<char *>(scratch(ctx, SLOT_PAIR_FB, (sizeof(float) + 8) * size_t(m + 1) + 64, st));
                 if (!fb) return FTK_ERR_CUDA;
@@ -859,20 +915,23 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             static long long *dclk = nullptr;  // FTK_PAIR_CLK=1: role timing printed to stderr
             const char *ce = getenv("FTK_PAIR_CLK");
             if (ce && atoi(ce)) {
-                if (!dclk) cudaMalloc(&dclk, 6 * sizeof(long long));
-                cudaMemsetAsync(dclk, 0, 6 * sizeof(long long), st);
+                if (!dclk) cudaMalloc(&dclk, 10 * sizeof(long long));
+                cudaMemsetAsync(dclk, 0, 10 * sizeof(long long), st);
                 Q.clk = dclk;
             }
             rc = pair_screen_launch(mx, mc128, Q, ft != nullptr, st);
             g_last_path = 1;
             if (Q.clk) {
-                long long h[6];
+                long long h[10];
                 cudaMemcpyAsync(h, Q.clk, sizeof(h), cudaMemcpyDeviceToHost, st);
                 cudaStreamSynchronize(st);
                 fprintf(stderr, "pair clk: screen busy %.0f wait %.0f per tile (%lld tiles); "
                         "mma wait t_empty %.0f full %.0f a_full %.0f per tile\n",
                         double(h[0]) / h[5], double(h[1]) / h[5], h[5], 2.0 * h[2] / h[5],
                         2.0 * h[3] / h[5], 2.0 * h[4] / h[5]);
+                const double nrt = double(h[5]) / (P.ntiles > 0 ? double((k + 255) / 256) : 1.0);
+                fprintf(stderr, "pair clk per row tile: refine wait %.0f busy %.0f; X prod wait %.0f, "
+                        "peer X load %.0f\n", h[6] / nrt, h[7] / nrt, h[8] / nrt, 2.0 * h[9] / nrt);
             }
         } else {
             rc = screen<false>(bn, P, mx, mx, mc, mc, st);
@@ -909,7 +968,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mc64, yf, k, d, PAIR_BN / 2)))
             return rc;
         PairParams Q{};
-        Q.y = yf; Q.yn = ynf; Q.m = n1; Q.k = k; Q.d = d;
+        Q.x = g; Q.y = yf; Q.yn = ynf; Q.m = n1; Q.k = k; Q.d = d;
         Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
         Q.thr = pair_fb_thr;
         Q.cand = cand;

@@ -89,7 +89,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
-    long long clk[6] = {0, 0, 0, 0, 0, 0};  // debug timing (P.clk)
+    long long clk[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // debug timing (P.clk)
     const int64_t npt = (P.m + 2 * PR_BM - 1) / (2 * PR_BM);  // row pair-tiles
     const int64_t pt0 = cluster_id_x(), pstride = ncluster_x();
 
@@ -102,7 +102,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&a_full[a], rank == 0 ? 2 : 1);  // leader: own TMA + peer's forward
-            mbar_init(&a_empty[a], 4);
+            mbar_init(&a_empty[a], 4);  // refine warps, done with the X half
             mbar_init(&p_full[a], 8);
             mbar_init(&p_empty[a], 4);
         }
@@ -180,7 +180,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const uint32_t lead = mapa_shared(smem_u32(&a_full[0]), 0);
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
                 const int ab = it % NA;
+                const long long xw0_ = clock64();
                 mbar_wait(&a_empty[ab], (uint32_t(it / NA) & 1) ^ 1);
+                const long long xw1_ = clock64();
+                clk[8] += xw1_ - xw0_;
                 unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
                 mbar_expect_tx(&a_full[ab], A_BYTES);
@@ -188,6 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     tma_load_2d(a_dst + size_t(kb) * PR_A_KB, &tmX, &a_full[ab], kb * PR_KB, row0);
                 if (rank == 1) {  // the leader's MMA reads this half too
                     mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);
+                    clk[9] += clock64() - xw1_;
                     mbar_arrive_remote(lead + uint32_t(ab) * 8u);
                 }
             }
@@ -334,7 +338,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
             const int ab = it % NA;
+            const long long rw0_ = clock64();
             mbar_wait(&p_full[pb], uint32_t(it >> 1) & 1);
+            const long long rw1_ = clock64();
+            clk[6] += rw1_ - rw0_;
             const PairPart q0 = part[(pb * 2 + 0) * PR_BM + r];
             const PairPart q1 = part[(pb * 2 + 1) * PR_BM + r];
             double rsum = 0.0;
@@ -347,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const float m2 = fminf(fminf(q0.m2, q1.m2), fmaxf(q0.m1, q1.m1));
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
             mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // own X half resident + visible
-            const unsigned char *sAt = sA + size_t(ab) * A_BYTES;
+            const unsigned char *sAt = sA + size_t(ab) * A_BYTES + uint32_t(r) * 128;
             bool ok = false;
             float dval = 0.0f;
             float thr_out = INFINITY;          // pass-2 candidate threshold
@@ -355,47 +362,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             if (!COLLECT && grow < P.m && m1 < INFINITY && !(P.dbg & 2)) {
                 const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(j) * P.d);
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
-                double rref = 0.0;
+                float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
                 const float4 *cs4 = CHK ? reinterpret_cast<const float4 *>(P.csum) : nullptr;
-                for (int kb = 0; kb < nkb; ++kb) {
-                    const int k0 = kb * PR_KB;
-                    float4 cv[8];
+                const bool have_info = P.rowinfo != nullptr;
+                if (have_info) {
+                    const float4 ri = __ldg(P.rowinfo + grow);
+                    xx = ri.x;
+                    ee = ri.y;
+                    amax = ri.z;
+                }
+                // centroid row in 32-float batches, the next batch in flight
+                // (two statically indexed register buffers: no local memory)
+                auto load_c = [&](float4 (&cv)[8], int kb) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
-                        cv[q] = (k0 + 4 * q < P.d) ? __ldg(cj4 + (k0 >> 2) + q)
-                                                   : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const unsigned char *rowp = sAt + uint32_t(kb) * PR_A_KB + uint32_t(r) * 128;
+                        cv[q] = (kb * PR_KB + 4 * q < P.d) ? __ldg(cj4 + kb * 8 + q)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                };
+                auto consume = [&](const float4 (&cv)[8], int kb) {
+                    const int k0 = kb * PR_KB;
+                    const unsigned char *rowp = sAt + uint32_t(kb) * PR_A_KB;
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         if (k0 + 4 * q < P.d) {
                             const float4 xv =
                                 *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.x, cv[q].x));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.y, cv[q].y));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.z, cv[q].z));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.w, cv[q].w));
-                            xx = fmaf(xv.x, xv.x, xx);
-                            xx = fmaf(xv.y, xv.y, xx);
-                            xx = fmaf(xv.z, xv.z, xx);
-                            xx = fmaf(xv.w, xv.w, xx);
-                            const float r0 = xv.x - tf32_trunc(xv.x);
-                            const float r1 = xv.y - tf32_trunc(xv.y);
-                            const float r2 = xv.z - tf32_trunc(xv.z);
-                            const float r3 = xv.w - tf32_trunc(xv.w);
-                            ee = fmaf(r0, r0, ee);
-                            ee = fmaf(r1, r1, ee);
-                            ee = fmaf(r2, r2, ee);
-                            ee = fmaf(r3, r3, ee);
+                            const float4 c4 = cv[q];
+                            acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.z, c4.z));
+                            acc = __fadd_rn(acc, __fmul_rn(xv.w, c4.w));
+                            if (!have_info) {
+                                xx = fmaf(xv.x, xv.x, xx);
+                                xx = fmaf(xv.y, xv.y, xx);
+                                xx = fmaf(xv.z, xv.z, xx);
+                                xx = fmaf(xv.w, xv.w, xx);
+                                const float r0 = xv.x - tf32_trunc(xv.x);
+                                const float r1 = xv.y - tf32_trunc(xv.y);
+                                const float r2 = xv.z - tf32_trunc(xv.z);
+                                const float r3 = xv.w - tf32_trunc(xv.w);
+                                ee = fmaf(r0, r0, ee);
+                                ee = fmaf(r1, r1, ee);
+                                ee = fmaf(r2, r2, ee);
+                                ee = fmaf(r3, r3, ee);
+                                if (CHK)
+                                    amax = fmaxf(amax, fmaxf(fmaxf(fabsf(xv.x), fabsf(xv.y)),
+                                                             fmaxf(fabsf(xv.z), fabsf(xv.w))));
+                            }
                             if (CHK) {
-                                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(xv.x), fabsf(xv.y)),
-                                                         fmaxf(fabsf(xv.z), fabsf(xv.w))));
                                 const float4 sv = __ldg(cs4 + kb * 8 + q);
-                                rref = fma(double(tf32_trunc(xv.x)), double(sv.x), rref);
-                                rref = fma(double(tf32_trunc(xv.y)), double(sv.y), rref);
-                                rref = fma(double(tf32_trunc(xv.z)), double(sv.z), rref);
-                                rref = fma(double(tf32_trunc(xv.w)), double(sv.w), rref);
+                                rr[0] = fmaf(tf32_trunc(xv.x), sv.x, rr[0]);
+                                rr[1] = fmaf(tf32_trunc(xv.y), sv.y, rr[1]);
+                                rr[2] = fmaf(tf32_trunc(xv.z), sv.z, rr[2]);
+                                rr[3] = fmaf(tf32_trunc(xv.w), sv.w, rr[3]);
                             }
                         }
+                    }
+                };
+                float4 cA[8], cB[8];
+                load_c(cA, 0);
+                for (int kb = 0; kb < nkb; kb += 2) {
+                    if (kb + 1 < nkb) load_c(cB, kb + 1);
+                    consume(cA, kb);
+                    if (kb + 1 < nkb) {
+                        if (kb + 2 < nkb) load_c(cA, kb + 2);
+                        consume(cB, kb + 1);
                     }
                 }
                 const float xn = sqrtf(xx * (1.0f + 0x1p-10f));
@@ -404,9 +435,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                 (sqrtf(ee * (1.0f + 0x1p-10f)) * cm +
                                  xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) + P.a_coef * xn * cm);
                 dval = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
+                const double rref = (rr[0] + rr[1]) + (rr[2] + rr[3]);
                 bool abft_bad = false;
                 if (CHK) {
-                    const float tau = P.tau_coef * fmaxf(1.0f, amax * *P.camax) + P.tau_abs;
+                    // reference tolerance + the fp32 evaluation error of the
+                    // checksum reference, |x~ . csum| rounding <= 34 u |x| |csum|
+                    const float tau = P.tau_coef * fmaxf(1.0f, amax * *P.camax) + P.tau_abs +
+                                      34.0f * 0x1p-24f * sqrtf(xx * (1.0f + 0x1p-10f)) *
+                                          sqrtf(P.camax[2] * (1.0f + 0x1p-10f));
                     abft_bad = !(fabs(rsum - rref) <= double(tau));
                     if (abft_bad) atomicAdd(P.abft_count, 1u);
                 }
@@ -445,12 +481,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&a_empty[ab]);
+            if (lane == 0) mbar_arrive(&a_empty[ab]);  // X half no longer read
+            clk[7] += clock64() - rw1_;
         }
     }
 
-    if (P.clk && lane == 0 && (warp == 0 || warp == W_MMA))
-        for (int q = 0; q < 6; ++q) atomicAdd(reinterpret_cast<unsigned long long *>(P.clk) + q,
+    if (P.clk && lane == 0 && (warp == 0 || warp == W_MMA || warp == W_REFINE0 || warp == W_XPROD))
+        for (int q = 0; q < 10; ++q) atomicAdd(reinterpret_cast<unsigned long long *>(P.clk) + q,
                                               (unsigned long long)clk[q]);
     tc_fence_before();
     __syncthreads();

@@ -12,6 +12,7 @@ namespace ftk {
 constexpr int PAIR_BN = 256;
 
 struct PairParams {
+    const float *x;  // rows (global, read by the refine warps)
     const float *y, *yn;
     int64_t m, k, d;
     int nkb, ntiles, stages, abufs;
@@ -37,6 +38,7 @@ struct PairParams {
     unsigned *cand_count;
     unsigned cand_cap;
     unsigned *row_cnt;
+    const float4 *rowinfo;  // per-fit row bounds (|x|^2, |x - tf32 x|^2, max|x|) or null
     long long *clk;  // debug: per-role clock64 sums (screen busy/wait, MMA waits), or null
     int dbg;  // bit 0: skip the screen math, bit 1: skip the refine (pipeline timing only)
 };

@@ -279,6 +279,7 @@ class LloydEngine:
         m = x_t.shape[0]
         dev = x_t.device
         self.xsq = E.row_sq_norms_dev(x_t).to(t.float64)
+        self.rows = E.RowInfo(x_t)  # per-fit screening bounds (X is constant)
         self.sq = t.empty(m, dtype=t.float64, device=dev)
         self.ctl_f64 = t.zeros(4, dtype=t.float64, device=dev)   # inertia, moved
         self.ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)     # equal, n_empty, dmr flag
@@ -333,6 +334,10 @@ class LloydEngine:
         self.slot = 1 - self.slot
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
 
+    def close(self):
+        """Unregister the per-fit row bounds (X may be freed afterwards)."""
+        self.rows.close()
+
     def final(self, iteration):
         """Final assignment against the current centroids -> (labels, inertia)."""
         A = self.A
@@ -374,17 +379,20 @@ def lloyd(x, config, fault_spec=None):
     history = []
     converged = False
     iters = 0
-    for it in range(config.max_iters):
-        inertia, unchanged, moved = eng.step(it)
-        timings["assign_ns"] += int(eng.assign_ms * 1e6)
-        timings["update_ns"] += int(eng.update_ms * 1e6)
-        history.append(inertia)
-        iters = it + 1
-        if unchanged or moved < config.tol:
-            converged = True
-            break
-    labels, inertia = eng.final(iters)
-    centroids = E.to_host(eng.cent)
+    try:
+        for it in range(config.max_iters):
+            inertia, unchanged, moved = eng.step(it)
+            timings["assign_ns"] += int(eng.assign_ms * 1e6)
+            timings["update_ns"] += int(eng.update_ms * 1e6)
+            history.append(inertia)
+            iters = it + 1
+            if unchanged or moved < config.tol:
+                converged = True
+                break
+        labels, inertia = eng.final(iters)
+        centroids = E.to_host(eng.cent)
+    finally:
+        eng.close()
     timings["total_ns"] = time.perf_counter_ns() - t_total
     return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,
                         converged=converged, report=eng.report, timings=timings,

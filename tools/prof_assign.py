@@ -15,6 +15,7 @@ ap.add_argument("--d", type=int, default=128)
 ap.add_argument("--k", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--iters", type=int, default=0, help="Lloyd iterations to converge centroids first")
+ap.add_argument("--checked", action="store_true", help="ABFT (checksum-protected) assignment")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -37,7 +38,12 @@ yn = E.row_sq_norms_dev(y_t)
 for r in range(a.reps):
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
-    E.assign_dev(x_t, y_t, yn, (32, 256, 16), variant=a.variant)
+    if a.checked:
+        ev = E.DevEvents(64)
+        E.assign_dev(x_t, y_t, yn, (32, 256, 16), variant=a.variant, checked=True, delta_rel=1e-4,
+                     abs_tol=0.0, events=ev)
+    else:
+        E.assign_dev(x_t, y_t, yn, (32, 256, 16), variant=a.variant)
     en.record()
     torch.cuda.synchronize()
     fb = E.tc_fallback_rows() if a.variant == "tc" else (-1, -1)
