@@ -23,6 +23,7 @@ SOURCES = {
     "update.cu": ["--fmad=false"],
     "tc.cu": [],
     "tc_pair.cu": [],
+    "dscreen.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

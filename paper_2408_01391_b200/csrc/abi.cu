@@ -3,6 +3,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "tc_pair.cuh"
 
 namespace ftk {
 
@@ -69,6 +70,8 @@ int tc_checked_run(ftk_ctx *, int, const void *, const void *, const void *, int
                    int64_t, int64_t, int64_t, int64_t, double, double, int64_t, int32_t *, void *,
                    const ftk_injection *, ftk_events *, cudaStream_t);
 int tc_supported(int dtype, int64_t m, int64_t k, int64_t d);
+int dscreen_run(ftk_ctx *, const double *, const double *, const double *, int64_t, int64_t,
+                int64_t, int32_t *, double *, const TcFt *, cudaStream_t);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
@@ -129,6 +132,13 @@ int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *
     if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
     cudaStream_t st = as_stream(stream);
     bool has_inj = inj && inj->n > 0;
+    if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && !has_inj) {
+        // float64: DFMA screen + certified exact refine (dscreen.cu)
+        int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
+                             static_cast<const double *>(ynorms), m, k, d, out_idx,
+                             static_cast<double *>(out_val), nullptr, st);
+        if (rc != FTK_ERR_UNSUPPORTED) return rc;
+    }
     if (variant == FTK_VARIANT_TC || (variant == FTK_VARIANT_AUTO && !has_inj)) {
         int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st, nullptr, 0,
                                nullptr);
@@ -145,6 +155,13 @@ int ftk_checked_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, cons
                        const ftk_injection *inj, ftk_events *ev, void *stream) {
     if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
     cudaStream_t st = as_stream(stream);
+    if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && bn >= 1 && bm >= 1) {
+        TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
+        int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
+                             static_cast<const double *>(ynorms), m, k, d, out_idx,
+                             static_cast<double *>(out_val), &ft, st);
+        if (rc != FTK_ERR_UNSUPPORTED) return rc;
+    }
     // TC path: screened assignment with per-tile row checksums; flagged rows
     // and the logical blocks carrying scheduled flips are resolved exactly
     if ((variant == FTK_VARIANT_TC || variant == FTK_VARIANT_AUTO) &&

@@ -76,6 +76,8 @@ enum ScratchSlot {
     SLOT_TC_INJROWS = 17,
     SLOT_PAIR_FB = 18,    // pass-1 thresholds + seeds
     SLOT_PAIR_CAND = 19,  // pass-2 candidate list, keys, counters
+    SLOT_DS = 20,         // float64 screen: bounds, counters, fallback rows
+    SLOT_DS_G = 21,       // float64 screen: gathered fallback rows
 };
 
 // ------------------------------------------------------- float helpers --

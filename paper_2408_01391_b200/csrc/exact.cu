@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
             }
             const T *xr = Xs + r * TM;
             const T *cr = Cs + jl * (KC + 1);
-            for (int kk = 0; kk < kc; ++kk) {
+            for (int kk = 0; kk < (real_row_group ? kc : 0); ++kk) {  // padding threads: no reads
                 const T cv = cr[kk];
                 const T *xk = xr + kk * bm;
 #pragma unroll

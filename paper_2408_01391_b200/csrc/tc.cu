@@ -571,8 +571,9 @@ __global__ void remap_inj_kernel(const int64_t *bi, int64_t n, const int64_t *bl
 }
 
 // gather rows [blocks[b]*bm, +bm) (clipped to m) into a compact buffer
-__global__ void gather_blocks_kernel(const float *x, int64_t m, int64_t d, int64_t bm,
-                                     const int64_t *blocks, int64_t nb, float *g) {
+template <typename T>
+__global__ void gather_blocks_kernel(const T *x, int64_t m, int64_t d, int64_t bm,
+                                     const int64_t *blocks, int64_t nb, T *g) {
     const int64_t n = nb * bm * d;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
          e += int64_t(gridDim.x) * blockDim.x) {
@@ -582,9 +583,10 @@ __global__ void gather_blocks_kernel(const float *x, int64_t m, int64_t d, int64
     }
 }
 
-__global__ void scatter_blocks_kernel(const int32_t *idx, const float *val, int64_t m, int64_t bm,
+template <typename T>
+__global__ void scatter_blocks_kernel(const int32_t *idx, const T *val, int64_t m, int64_t bm,
                                       const int64_t *blocks, int64_t nb, int32_t *out_idx,
-                                      float *out_val) {
+                                      T *out_val) {
     for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nb * bm;
          r += int64_t(gridDim.x) * blockDim.x) {
         const int64_t row = blocks[r / bm] * bm + r % bm;
@@ -738,12 +740,6 @@ static int g_last_path = 0;  // pass-1 kernel of the last call: 0 single-CTA, 1 
 
   // pass-1 / pass-2 uncertified, TC ABFT flags
 
-struct TcFt {          // checksum-protected (abft) mode
-    double delta_rel, abs_tol;
-    int64_t bm, bn, bk, iteration;
-    const ftk_injection *inj;
-    ftk_events *ev;
-};
 
 // FT mode helpers: checksum centroids for a given N tiling
 static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb,
@@ -765,10 +761,10 @@ static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t 
 // that carry an injection are recomputed by the exact checked kernel (the
 // reference's detection / location / correction / events, bit for bit) and
 // overwrite the TC results for those rows.
-static int emulate_injected_blocks(ftk_ctx *ctx, const float *xf, const float *yf,
-                                   const float *ynf, int64_t m, int64_t k, int64_t d,
-                                   const TcFt &ft, int32_t *out_idx, float *outv,
-                                   cudaStream_t st) {
+template <typename T>
+int emulate_injected_blocks(ftk_ctx *ctx, const T *xf, const T *yf, const T *ynf, int64_t m,
+                            int64_t k, int64_t d, const TcFt &ft, int32_t *out_idx, T *outv,
+                            cudaStream_t st) {
     const ftk_injection &inj = *ft.inj;
     std::vector<int64_t> bi(inj.n);
     FTK_CUDA(cudaMemcpyAsync(bi.data(), inj.bi, sizeof(int64_t) * inj.n, cudaMemcpyDeviceToHost, st));
@@ -785,27 +781,28 @@ static int emulate_injected_blocks(ftk_ctx *ctx, const float *xf, const float *y
     const int64_t rows_c = (blocks.back() == nbi - 1) ? (nb - 1) * ft.bm + (m - (nbi - 1) * ft.bm)
                                                       : nb * ft.bm;
     const size_t need = sizeof(int64_t) * (2 * nb + 2 * inj.n + 8) +
-                        sizeof(float) * (nb * ft.bm * d + 2 * nb * ft.bm) + 256;
+                        sizeof(T) * (nb * ft.bm * d + 2 * nb * ft.bm) + 256;
     char *buf = static_cast<char *>(scratch(ctx, SLOT_INJ, need, st));
     if (!buf) return FTK_ERR_CUDA;
     int64_t *d_blocks = reinterpret_cast<int64_t *>(buf);
     int64_t *d_bi = d_blocks + nb;
-    float *g = reinterpret_cast<float *>(d_bi + inj.n + 2);
-    int32_t *gi = reinterpret_cast<int32_t *>(g + nb * ft.bm * d);
-    float *gv = reinterpret_cast<float *>(gi + nb * ft.bm);
+    T *g = reinterpret_cast<T *>(d_bi + inj.n + 2);
+    T *gv = g + nb * ft.bm * d;
+    int32_t *gi = reinterpret_cast<int32_t *>(gv + nb * ft.bm);
     FTK_CUDA(cudaMemcpyAsync(d_blocks, blocks.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, st));
     remap_inj_kernel<<<1, 256, 0, st>>>(inj.bi, inj.n, d_blocks, nb, d_bi);
     FTK_LAUNCHED("remap_inj_kernel");
-    gather_blocks_kernel<<<148, 256, 0, st>>>(xf, m, d, ft.bm, d_blocks, nb, g);
+    gather_blocks_kernel<T><<<148, 256, 0, st>>>(xf, m, d, ft.bm, d_blocks, nb, g);
     FTK_LAUNCHED("gather_blocks_kernel");
     ftk_injection rin = inj;
     rin.bi = d_bi;
-    int rc = exact_run(ctx, FTK_F32, g, yf, ynf, rows_c, k, d, ft.bm, ft.bn, ft.bk, gi, gv, nullptr,
+    int rc = exact_run(ctx, sizeof(T) == 4 ? FTK_F32 : FTK_F64, g, yf, ynf, rows_c, k, d, ft.bm,
+                       ft.bn, ft.bk, gi, gv, nullptr,
                        true, ft.delta_rel, ft.abs_tol, ft.iteration, &rin, ft.ev, st);
     if (rc) return rc;
     remap_events_kernel<<<1, 256, 0, st>>>(ft.ev->rec, ft.ev->count, ft.ev->cap, d_blocks);
     FTK_LAUNCHED("remap_events_kernel");
-    scatter_blocks_kernel<<<148, 256, 0, st>>>(gi, gv, m, ft.bm, d_blocks, nb, out_idx, outv);
+    scatter_blocks_kernel<T><<<148, 256, 0, st>>>(gi, gv, m, ft.bm, d_blocks, nb, out_idx, outv);
     FTK_LAUNCHED("scatter_blocks_kernel");
     FTK_CUDA(cudaStreamSynchronize(st));  // host vectors go out of scope
     return FTK_OK;
@@ -1081,6 +1078,10 @@ int tc_checked_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const 
     TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
     return tc_assign_run(ctx, dtype, x, y, yn, m, k, d, out_idx, out_val, st, nullptr, 0, &ft);
 }
+
+template int emulate_injected_blocks<double>(ftk_ctx *, const double *, const double *,
+                                             const double *, int64_t, int64_t, int64_t,
+                                             const TcFt &, int32_t *, double *, cudaStream_t);
 
 int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t) {
     out[0] = g_last_fb[0];

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/ftk_b200.h"
+
 namespace ftk {
 
 // centroids per accumulator tile (the TMEM holds 512 / PAIR_BN buffers);
@@ -54,4 +56,21 @@ int pair_candidates_run(const float *g, const float *y, const float *yn, int64_t
                         const unsigned *row_cnt, unsigned row_cap, unsigned long long *key,
                         const int32_t *rows, const unsigned *n_rows, int32_t *out_idx,
                         float *out_val, int32_t *rows2, unsigned *n2, cudaStream_t st);
+}  // namespace ftk
+
+namespace ftk {
+struct TcFt {  // checksum-protected (abft) mode of a screened assignment
+    double delta_rel, abs_tol;
+    int64_t bm, bn, bk, iteration;
+    const ftk_injection *inj;
+    ftk_events *ev;
+};
+
+// The logical row blocks that carry scheduled flips are recomputed by the
+// exact checked kernel (the reference's detection, location, correction and
+// event record, bit for bit) and overwrite the screened results of those rows.
+template <typename T>
+int emulate_injected_blocks(ftk_ctx *ctx, const T *xf, const T *yf, const T *ynf, int64_t m,
+                            int64_t k, int64_t d, const TcFt &ft, int32_t *out_idx, T *outv,
+                            cudaStream_t st);
 }  // namespace ftk
