@@ -153,6 +153,110 @@ __global__ void __launch_bounds__(256) chain_sums_kernel(const T *x, int64_t d,
     }
 }
 
+// ------------------------------------------------ pipelined ordered chains --
+// The reference's chain verbatim (one float64 accumulator per (cluster,
+// feature), members in ascending sample order), latency-hidden: each warp
+// owns (cluster, 32-feature group) and streams member rows through a shared
+// memory ring with cp.async (CH_RING rows in flight, CH_GROUP rows per
+// commit group), so the chain runs at DADD latency instead of load latency.
+// Used when the chains are long and few (K * D/32 fits one wave): small K or
+// float64 data, where certified segment folding rarely applies.
+constexpr int CH_RING = 256, CH_GROUP = 32, CH_WARPS = 1;
+
+__device__ __forceinline__ void cp_async_8(void *dst, const void *src, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                 "@p cp.async.ca.shared.global [%0], [%1], 8;\n\t}" ::"r"(s),
+                 "l"(src), "r"(int(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_4(void *dst, const void *src, bool pred) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %2, 0;\n\t"
+                 "@p cp.async.ca.shared.global [%0], [%1], 4;\n\t}" ::"r"(s),
+                 "l"(src), "r"(int(pred))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename T, bool DMR>
+__global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
+    const T *x, int64_t d, const int32_t *perm, const int64_t *offsets, int64_t k,
+    double *sums_a, double *sums_b) {
+    extern __shared__ __align__(16) unsigned char ch_smem[];
+    T(*ring)[CH_RING][32] = reinterpret_cast<T(*)[CH_RING][32]>(ch_smem);  // [CH_WARPS]
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ngroups = (d + 31) / 32;
+    const int64_t wid = int64_t(blockIdx.x) * CH_WARPS + w;
+    if (wid >= k * ngroups) return;
+    const int64_t c = wid / ngroups;
+    const int64_t f = (wid % ngroups) * 32 + lane;
+    const bool live = f < d;
+    const int64_t lo = offsets[c], hi = offsets[c + 1];
+    const int64_t n = hi - lo;
+    T(*rb)[32] = ring[w];
+    // issue the copies of members [t, t + CH_GROUP) into their ring slots;
+    // `rows` holds those members' sample indices (lanes 0..CH_GROUP-1),
+    // loaded one group ahead so the shuffles never wait on global memory
+    auto load_rows = [&](int64_t t) -> int32_t {
+        const int64_t idx = t + lane;
+        return (lane < CH_GROUP && idx < n) ? __ldg(perm + lo + idx) : 0;
+    };
+    auto issue = [&](int64_t t, int32_t rows) {
+#pragma unroll
+        for (int u = 0; u < CH_GROUP; ++u) {
+            const int32_t row = __shfl_sync(0xffffffffu, rows, u);
+            const bool p = live && (t + u < n);
+            T *dst = &rb[(t + u) % CH_RING][lane];
+            if (sizeof(T) == 8) cp_async_8(dst, x + int64_t(row) * d + f, p);
+            else cp_async_4(dst, x + int64_t(row) * d + f, p);
+        }
+        cp_async_commit();
+    };
+    constexpr int NG = CH_RING / CH_GROUP;
+    // sample indices run three groups ahead of the copies that need them
+    int32_t r0 = load_rows(0), r1 = load_rows(CH_GROUP), r2 = load_rows(2 * CH_GROUP);
+#pragma unroll
+    for (int g = 0; g < NG - 1; ++g) {
+        issue(int64_t(g) * CH_GROUP, r0);
+        r0 = r1;
+        r1 = r2;
+        r2 = load_rows(int64_t(g + 3) * CH_GROUP);
+    }
+    double acc_a = 0.0, acc_b = 0.0;
+    for (int64_t t = 0; t < n; t += CH_GROUP) {
+        const int64_t ti = t + int64_t(NG - 1) * CH_GROUP;
+        issue(ti, r0);  // may be empty: keeps the group count uniform
+        r0 = r1;
+        r1 = r2;
+        r2 = load_rows(ti + 3 * CH_GROUP);
+        cp_async_wait<NG - 1>();  // group of rows [t, t + CH_GROUP) landed
+        __syncwarp();
+        const int cnt = int(n - t < CH_GROUP ? n - t : CH_GROUP);
+        double v[CH_GROUP];
+#pragma unroll
+        for (int u = 0; u < CH_GROUP; ++u)
+            v[u] = (live && u < cnt) ? double(rb[(t + u) % CH_RING][lane]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < CH_GROUP; ++u) {
+            if (u < cnt) {
+                acc_a = __dadd_rn(acc_a, v[u]);
+                if (DMR) acc_b = __dadd_rn(acc_b, v[u]);
+            }
+        }
+        __syncwarp();  // slots of this group are refilled next iteration
+    }
+    cp_async_wait<0>();
+    if (live) {
+        sums_a[c * d + f] = acc_a;
+        if (DMR) sums_b[c * d + f] = acc_b;
+    }
+}
+
 // ------------------------------------------------ certified segmented sums --
 // The reference's float64 chain is order-dependent only if some partial sum
 // rounds.  For a (cluster, feature) chain whose values are all multiples of
@@ -764,6 +868,28 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     const int block = 256;
     const unsigned grid = unsigned((warps * 32 + block - 1) / block);
     const bool dmr = sums_b != nullptr;
+    const int64_t nwarps = k * ((d + 31) / 32);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const bool pipe_chains = m > 0 && (dtype == FTK_F64 || nwarps <= int64_t(nsm) * 12);
+    if (pipe_chains) {
+        // few long chains: the reference's ordered chain, latency-hidden
+        const unsigned g = unsigned((nwarps + CH_WARPS - 1) / CH_WARPS);
+        const size_t sm = size_t(CH_WARPS) * CH_RING * 32 * (dtype == FTK_F32 ? 4 : 8);
+        if (dtype == FTK_F32) {
+            auto xx = static_cast<const float *>(x);
+            auto kern = dmr ? chain_pipe_kernel<float, true> : chain_pipe_kernel<float, false>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            kern<<<g, 32 * CH_WARPS, sm, st>>>(xx, d, vals_out, offsets, k, sums_a, dmr ? sums_b : nullptr);
+        } else {
+            auto xx = static_cast<const double *>(x);
+            auto kern = dmr ? chain_pipe_kernel<double, true> : chain_pipe_kernel<double, false>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+            kern<<<g, 32 * CH_WARPS, sm, st>>>(xx, d, vals_out, offsets, k, sums_a, dmr ? sums_b : nullptr);
+        }
+        FTK_LAUNCHED("chain_pipe_kernel");
+        return FTK_OK;
+    }
     if (dtype == FTK_F32 && m > 0) {
         // certified segmented sums (float32 data): segments fold exactly
         // unless their certificate fails, in which case only that segment is
