@@ -180,6 +180,11 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
  * certify (resolved by the exact kernel). */
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream);
 
+/* Diagnostics: device time (CUDA events on the launching stream) of the
+ * last tensor-core screen launch (the CTA-pair pass-1 kernel), in ms; -1 if
+ * the last TC assignment did not use it. */
+int ftk_tc_last_kernel_ms(ftk_ctx *ctx, float *ms);
+
 /* Validation hook for the screening error model: runs the TC assignment
  * (split = 0: 1xTF32 pass then 3xTF32 on ties; split = 1: 3xTF32 on every
  * row) and also materialises the raw tensor-core dot products of the screen

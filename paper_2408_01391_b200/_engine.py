@@ -334,6 +334,15 @@ def tc_fallback_rows():
     return int(v[0]), int(v[1]), int(v[2])
 
 
+def tc_last_kernel_ms():
+    """Device time of the last tensor-core screen launch (ms, -1 if none)."""
+    import ctypes
+
+    v = ctypes.c_float(-1.0)
+    N.check(N.load().ftk_tc_last_kernel_ms(ctx(), ctypes.byref(v)), "ftk_tc_last_kernel_ms")
+    return float(v.value)
+
+
 def tc_raw_dots(x_t, y_t, yn_t, split=False):
     """Raw tensor-core screened dot products (m x k) + the assignment."""
     t = _torch()

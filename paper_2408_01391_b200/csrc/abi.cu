@@ -73,6 +73,7 @@ int tc_supported(int dtype, int64_t m, int64_t k, int64_t d);
 int dscreen_run(ftk_ctx *, const double *, const double *, const double *, int64_t, int64_t,
                 int64_t, int32_t *, double *, const TcFt *, cudaStream_t);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
+float tc_last_pass1_ms();
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
 
@@ -254,6 +255,12 @@ int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
     out[1] = int64_t(v[1]);
     out[2] = int64_t(v[2]);
     return rc;
+}
+
+int ftk_tc_last_kernel_ms(ftk_ctx *ctx, float *ms) {
+    if (!ctx || !ms) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    *ms = tc_last_pass1_ms();
+    return FTK_OK;
 }
 
 int ftk_tc_raw_dots(ftk_ctx *ctx, int split, const float *x, const float *y, const float *ynorms,

@@ -737,6 +737,7 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
 
 static unsigned g_last_fb[3] = {0, 0, 0};
 static int g_last_path = 0;  // pass-1 kernel of the last call: 0 single-CTA, 1 CTA pair
+static cudaEvent_t g_time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
 
   // pass-1 / pass-2 uncertified, TC ABFT flags
 
@@ -916,7 +917,16 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                 cudaMemsetAsync(dclk, 0, 10 * sizeof(long long), st);
                 Q.clk = dclk;
             }
+            static cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // pass-1 kernel timing
+            if (!ev0) {
+                cudaEventCreate(&ev0);
+                cudaEventCreate(&ev1);
+            }
+            cudaEventRecord(ev0, st);
             rc = pair_screen_launch(mx, mc128, Q, ft != nullptr, st);
+            cudaEventRecord(ev1, st);
+            g_time_ev[0] = ev0;
+            g_time_ev[1] = ev1;
             g_last_path = 1;
             if (Q.clk) {
                 long long h[10];
@@ -1082,6 +1092,15 @@ int tc_checked_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const 
 template int emulate_injected_blocks<double>(ftk_ctx *, const double *, const double *,
                                              const double *, int64_t, int64_t, int64_t,
                                              const TcFt &, int32_t *, double *, cudaStream_t);
+
+// Device time of the last CTA-pair pass-1 launch (ms), -1 if none.
+float tc_last_pass1_ms() {
+    if (!g_time_ev[0] || g_last_path != 1) return -1.0f;
+    float ms = -1.0f;
+    if (cudaEventSynchronize(g_time_ev[1]) != cudaSuccess) return -1.0f;
+    cudaEventElapsedTime(&ms, g_time_ev[0], g_time_ev[1]);
+    return ms;
+}
 
 int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t) {
     out[0] = g_last_fb[0];
