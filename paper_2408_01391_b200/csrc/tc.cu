@@ -937,8 +937,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                         double(h[0]) / h[5], double(h[1]) / h[5], h[5], 2.0 * h[2] / h[5],
                         2.0 * h[3] / h[5], 2.0 * h[4] / h[5]);
                 const double nrt = double(h[5]) / (P.ntiles > 0 ? double((k + 255) / 256) : 1.0);
-                fprintf(stderr, "pair clk per row tile: refine wait %.0f busy %.0f; X prod wait %.0f, "
-                        "peer X load %.0f\n", h[6] / nrt, h[7] / nrt, h[8] / nrt, 2.0 * h[9] / nrt);
+                fprintf(stderr, "pair clk per row tile: refine wait %.0f busy %.0f (loop %.0f, post %.0f)\n", h[6] / nrt, h[7] / nrt, h[8] / nrt, h[9] / nrt);
             }
         } else {
             rc = screen<false>(bn, P, mx, mx, mc, mc, st);

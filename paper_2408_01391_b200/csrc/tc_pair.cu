@@ -80,7 +80,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * PR_B_HALF);  // [2][2][128]
     double *psum = reinterpret_cast<double *>(part + 2 * 2 * PR_BM);           // [2][2][128]
     float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(yns + 2 * PR_BN);
+    float4 *stg = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // [4 refine warps][32 rows][8]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * 32 * 8);
     uint64_t *full = bars, *empty = bars + S;
     uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
     uint64_t *t_full = a_full + 4, *t_empty = t_full + PR_NBUF;
@@ -183,7 +184,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const long long xw0_ = clock64();
                 mbar_wait(&a_empty[ab], (uint32_t(it / NA) & 1) ^ 1);
                 const long long xw1_ = clock64();
-                clk[8] += xw1_ - xw0_;
                 unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
                 mbar_expect_tx(&a_full[ab], A_BYTES);
@@ -191,7 +191,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     tma_load_2d(a_dst + size_t(kb) * PR_A_KB, &tmX, &a_full[ab], kb * PR_KB, row0);
                 if (rank == 1) {  // the leader's MMA reads this half too
                     mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);
-                    clk[9] += clock64() - xw1_;
                     mbar_arrive_remote(lead + uint32_t(ab) * 8u);
                 }
             }
@@ -359,8 +358,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             float dval = 0.0f;
             float thr_out = INFINITY;          // pass-2 candidate threshold
             unsigned long long seed_out = ~0ull;  // (ordered d1, j1) key
-            if (!COLLECT && grow < P.m && m1 < INFINITY && !(P.dbg & 2)) {
-                const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(j) * P.d);
+            const bool active = !COLLECT && grow < P.m && m1 < INFINITY && !(P.dbg & 2);
+            if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
                 const float4 *cs4 = CHK ? reinterpret_cast<const float4 *>(P.csum) : nullptr;
@@ -371,15 +370,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     ee = ri.y;
                     amax = ri.z;
                 }
-                // centroid row in 32-float batches, the next batch in flight
-                // (two statically indexed register buffers: no local memory)
-                auto load_c = [&](float4 (&cv)[8], int kb) {
+                // centroid rows of the warp's 32 winners, one 32-float k-block at
+                // a time: loaded cooperatively (a warp instruction covers 4 rows,
+                // 8 lanes x 16 B each -> 4 L1 wavefronts instead of 32 for
+                // per-thread row gathers), staged in shared memory (XOR-swizzled
+                // by row) and read back by the owning thread; the next k-block is
+                // held in registers while the current one is consumed
+                float4 *wst = stg + (warp - W_REFINE0) * (32 * 8);
+                float4 nxt[8];
+                auto gather = [&](int kb) {
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        cv[q] = (kb * PR_KB + 4 * q < P.d) ? __ldg(cj4 + kb * 8 + q)
-                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int i = 0; i < 8; ++i) {
+                        const int rr = i * 4 + (lane >> 3), q = lane & 7;
+                        const int jr = __shfl_sync(0xffffffffu, j, rr);
+                        const bool okr = __shfl_sync(0xffffffffu, int(active), rr) != 0;
+                        const int f = kb * PR_KB + 4 * q;
+                        nxt[i] = (okr && f < P.d)
+                                     ? __ldg(reinterpret_cast<const float4 *>(P.y + int64_t(jr) * P.d + f))
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
                 };
-                auto consume = [&](const float4 (&cv)[8], int kb) {
+                auto stash = [&]() {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int rr = i * 4 + (lane >> 3), q = lane & 7;
+                        wst[rr * 8 + (q ^ (rr & 7))] = nxt[i];
+                    }
+                };
+                const long long lp0_ = clock64();
+                gather(0);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    __syncwarp();
+                    stash();
+                    __syncwarp();
+                    if (kb + 1 < nkb) gather(kb + 1);
                     const int k0 = kb * PR_KB;
                     const unsigned char *rowp = sAt + uint32_t(kb) * PR_A_KB;
 #pragma unroll
@@ -387,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         if (k0 + 4 * q < P.d) {
                             const float4 xv =
                                 *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
-                            const float4 c4 = cv[q];
+                            const float4 c4 = wst[lane * 8 + (q ^ (lane & 7))];
                             acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
                             acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
                             acc = __fadd_rn(acc, __fmul_rn(xv.z, c4.z));
@@ -418,17 +442,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             }
                         }
                     }
-                };
-                float4 cA[8], cB[8];
-                load_c(cA, 0);
-                for (int kb = 0; kb < nkb; kb += 2) {
-                    if (kb + 1 < nkb) load_c(cB, kb + 1);
-                    consume(cA, kb);
-                    if (kb + 1 < nkb) {
-                        if (kb + 2 < nkb) load_c(cA, kb + 2);
-                        consume(cB, kb + 1);
-                    }
                 }
+                const long long lp1_ = clock64();
+                clk[8] += lp1_ - lp0_;
+              if (active) {  // lanes without a live row only helped with the loads
                 const float xn = sqrtf(xx * (1.0f + 0x1p-10f));
                 const float cm = sqrtf(*P.cmax2 * (1.0f + 0x1p-10f));
                 const float A = 2.0f * (1.0f + 0x1p-10f) *
@@ -456,6 +473,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
                 ok = !abft_bad && sane &&
                      (m2 - A - P.b_coef * fabsf(m2) - 0x1p-21f * (fabsf(m1) + fabsf(m2)) > dval);
+              }
+                clk[9] += clock64() - lp1_;
             }
             if (!COLLECT && grow < P.m) {
                 if (ok) {
@@ -502,7 +521,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 size_t pair_smem_bytes(int nkb, int abufs, int stages) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * PR_B_HALF +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
-           (8 + 2 * PR_NBUF) * 8 + 64;
+           4 * 32 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
 }
 
 int pair_plan(int64_t d, int *abufs, int *stages) {
