@@ -81,7 +81,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     double *psum = reinterpret_cast<double *>(part + 2 * 2 * PR_BM);           // [2][2][128]
     float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
     float4 *stg = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // [4 refine warps][32 rows][8]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stg + 4 * 32 * 8);
+    float4 *css = stg + 4 * 32 * 8;                             // ABFT checksum centroid [nkb * 8]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
     uint64_t *full = bars, *empty = bars + S;
     uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
     uint64_t *t_full = a_full + 4, *t_empty = t_full + PR_NBUF;
@@ -333,6 +334,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         // ----------------------------------------------------- refine --
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
+        if (CHK) {
+            const int t = (warp - W_REFINE0) * 32 + lane;  // 0..127
+            if (t < nkb * 8) css[t] = __ldg(reinterpret_cast<const float4 *>(P.csum) + t);
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+        }
         int it = 0;
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
@@ -362,7 +368,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
-                const float4 *cs4 = CHK ? reinterpret_cast<const float4 *>(P.csum) : nullptr;
+                const float4 *cs4 = css;  // staged once per CTA (ABFT)
                 const bool have_info = P.rowinfo != nullptr;
                 if (have_info) {
                     const float4 ri = __ldg(P.rowinfo + grow);
@@ -434,7 +440,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                                              fmaxf(fabsf(xv.z), fabsf(xv.w))));
                             }
                             if (CHK) {
-                                const float4 sv = __ldg(cs4 + kb * 8 + q);
+                                const float4 sv = cs4[kb * 8 + q];
                                 rr[0] = fmaf(tf32_trunc(xv.x), sv.x, rr[0]);
                                 rr[1] = fmaf(tf32_trunc(xv.y), sv.y, rr[1]);
                                 rr[2] = fmaf(tf32_trunc(xv.z), sv.z, rr[2]);
@@ -521,7 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 size_t pair_smem_bytes(int nkb, int abufs, int stages) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * PR_B_HALF +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
-           4 * 32 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
+           4 * 32 * 8 * sizeof(float4) + 8 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
 }
 
 int pair_plan(int64_t d, int *abufs, int *stages) {

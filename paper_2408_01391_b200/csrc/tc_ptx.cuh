@@ -440,14 +440,24 @@ __device__ __forceinline__ void screen32t(const uint32_t (&v)[32], const float *
     const float4 *yn4 = reinterpret_cast<const float4 *>(yn_s);
     const uint32_t base4 = cbase * 0x01010101u + 0x03020100u;
     float p[32];
+    if (CHK) {
+        // row-sum of the raw accumulators: a pairwise tree (FADD2), not a chain
+        float t[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            fadd2v(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                   __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]), t[2 * i], t[2 * i + 1]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fadd2v(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3], t[2 * i], t[2 * i + 1]);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) fadd2v(t[4 * i], t[4 * i + 1], t[4 * i + 2], t[4 * i + 3], t[2 * i], t[2 * i + 1]);
+        fadd2v(t[0], t[1], t[2], t[3], t[0], t[1]);
+        fadd2(s0, s1, t[0], t[1]);
+    }
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
         const float4 yv = yn4[q];
         const int e = q * 4;
-        if (CHK) {
-            fadd2(s0, s1, __uint_as_float(v[e + 0]), __uint_as_float(v[e + 1]));
-            fadd2(s0, s1, __uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]));
-        }
         float d0, d1, d2, d3;
         ffma2_m2(__uint_as_float(v[e + 0]), __uint_as_float(v[e + 1]), yv.x, yv.y, d0, d1);
         ffma2_m2(__uint_as_float(v[e + 2]), __uint_as_float(v[e + 3]), yv.z, yv.w, d2, d3);
