@@ -288,11 +288,17 @@ __global__ void seg_count_kernel(const int64_t *counts, int64_t k, int64_t *nseg
 // magnitude, whose exponent bounds the ulp exponent of every value.  Two
 // features per thread with 8-byte loads; ~8 instructions per element.
 template <bool DMR>
-__global__ void __launch_bounds__(128) seg_partials_kernel(
+__global__ void __launch_bounds__(256) seg_partials_kernel(
     const float *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
     int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
+    // The segment partial is only used when the whole chain is certified
+    // exact (then any association gives the reference's bits), so the
+    // members of a segment are split across `nph` thread phases and the
+    // phase partials are combined through shared memory.
     __shared__ int64_t rowoff[SEG];
     __shared__ int64_t info[3];
+    __shared__ double red_a[256 * 2], red_b[256 * 2];
+    __shared__ uint32_t red_mx[256 * 2], red_mn[256 * 2];
     const int64_t s = blockIdx.x;
     if (threadIdx.x == 0) {
         // cluster owning segment s: largest c with seg_base[c] <= s
@@ -317,43 +323,80 @@ __global__ void __launch_bounds__(128) seg_partials_kernel(
     __syncthreads();
     const bool pairs = (d & 1) == 0;
     const int64_t nf = pairs ? d / 2 : d;
-    for (int64_t f = threadIdx.x; f < nf; f += blockDim.x) {
+    const int nph = nf >= int64_t(blockDim.x) ? 1 : int(blockDim.x / nf);
+    const int ph = nph > 1 ? int(threadIdx.x / nf) : 0;
+    for (int64_t f = nph > 1 ? int64_t(threadIdx.x % nf) : int64_t(threadIdx.x); f < nf;
+         f += (nph > 1 ? nf : int64_t(blockDim.x))) {
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
         uint32_t mx0 = 0, mx1 = 0, mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
-        constexpr int U = 8;
-        int t = 0;
-        if (pairs) {
-            const float *xb = x + 2 * f;
-            for (; t < n; t += U) {
-                float2 v[U];
+        if (ph < nph) {
+            constexpr int U = 8;
+            if (pairs) {
+                const float *xb = x + 2 * f;
+                for (int t = ph; t < n; t += U * nph) {
+                    float2 v[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u)
-                    v[u] = (t + u < n) ? *reinterpret_cast<const float2 *>(xb + rowoff[t + u])
-                                       : make_float2(0.f, 0.f);
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    a0 = __dadd_rn(a0, double(v[u].x));
-                    a1 = __dadd_rn(a1, double(v[u].y));
-                    if (DMR) {
-                        b0 = __dadd_rn(b0, double(v[u].x));
-                        b1 = __dadd_rn(b1, double(v[u].y));
+                    for (int u = 0; u < U; ++u) {
+                        const int tt = t + u * nph;
+                        v[u] = tt < n ? *reinterpret_cast<const float2 *>(xb + rowoff[tt])
+                                      : make_float2(0.f, 0.f);
                     }
-                    const uint32_t u0 = __float_as_uint(v[u].x) & 0x7FFFFFFFu;
-                    const uint32_t u1 = __float_as_uint(v[u].y) & 0x7FFFFFFFu;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        a0 = __dadd_rn(a0, double(v[u].x));
+                        a1 = __dadd_rn(a1, double(v[u].y));
+                        if (DMR) {
+                            b0 = __dadd_rn(b0, double(v[u].x));
+                            b1 = __dadd_rn(b1, double(v[u].y));
+                        }
+                        const uint32_t u0 = __float_as_uint(v[u].x) & 0x7FFFFFFFu;
+                        const uint32_t u1 = __float_as_uint(v[u].y) & 0x7FFFFFFFu;
+                        mx0 = max(mx0, u0);
+                        mx1 = max(mx1, u1);
+                        mn0 = min(mn0, u0 - 1u);  // zeros wrap to 0xFFFFFFFF: ignored
+                        mn1 = min(mn1, u1 - 1u);
+                    }
+                }
+            } else {
+                for (int t = ph; t < n; t += nph) {
+                    const float v = x[rowoff[t] + f];
+                    a0 = __dadd_rn(a0, double(v));
+                    if (DMR) b0 = __dadd_rn(b0, double(v));
+                    const uint32_t u0 = __float_as_uint(v) & 0x7FFFFFFFu;
                     mx0 = max(mx0, u0);
-                    mx1 = max(mx1, u1);
-                    mn0 = min(mn0, u0 - 1u);  // zeros wrap to 0xFFFFFFFF: ignored
-                    mn1 = min(mn1, u1 - 1u);
+                    mn0 = min(mn0, u0 - 1u);
                 }
             }
-        } else {
-            for (; t < n; ++t) {
-                const float v = x[rowoff[t] + f];
-                a0 = __dadd_rn(a0, double(v));
-                if (DMR) b0 = __dadd_rn(b0, double(v));
-                const uint32_t u0 = __float_as_uint(v) & 0x7FFFFFFFu;
-                mx0 = max(mx0, u0);
-                mn0 = min(mn0, u0 - 1u);
+        }
+        if (nph > 1) {
+            // combine the phases of feature (pair) f
+            const int slot = ph * int(nf) + int(f);
+            red_a[2 * slot] = a0;
+            red_a[2 * slot + 1] = a1;
+            if (DMR) {
+                red_b[2 * slot] = b0;
+                red_b[2 * slot + 1] = b1;
+            }
+            red_mx[2 * slot] = mx0;
+            red_mx[2 * slot + 1] = mx1;
+            red_mn[2 * slot] = mn0;
+            red_mn[2 * slot + 1] = mn1;
+            __syncthreads();  // nph > 1: every thread runs exactly one f iteration
+        }
+        if (nph > 1) {
+            if (ph != 0) continue;
+            for (int q = 1; q < nph; ++q) {
+                const int slot = q * int(nf) + int(f);
+                a0 = __dadd_rn(a0, red_a[2 * slot]);
+                a1 = __dadd_rn(a1, red_a[2 * slot + 1]);
+                if (DMR) {
+                    b0 = __dadd_rn(b0, red_b[2 * slot]);
+                    b1 = __dadd_rn(b1, red_b[2 * slot + 1]);
+                }
+                mx0 = max(mx0, red_mx[2 * slot]);
+                mx1 = max(mx1, red_mx[2 * slot + 1]);
+                mn0 = min(mn0, red_mn[2 * slot]);
+                mn1 = min(mn1, red_mn[2 * slot + 1]);
             }
         }
         // q = exponent of the ulp of the smallest nonzero magnitude (a lower
@@ -915,7 +958,7 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         FTK_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(unsigned), st));
         const unsigned rgrid = unsigned(std::min<int64_t>(k * d, 148 * 8));
         if (dmr) {
-            seg_partials_kernel<true><<<unsigned(max_seg), 128, 0, st>>>(
+            seg_partials_kernel<true><<<unsigned(max_seg), 256, 0, st>>>(
                 xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
             seg_fold_kernel<true><<<grid_for(k * d, 128), 128, 0, st>>>(
@@ -925,7 +968,7 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
                                                           ps_b, ps_abs, ps_q, fail_list, fail_count,
                                                           sums_a, sums_b);
         } else {
-            seg_partials_kernel<false><<<unsigned(max_seg), 128, 0, st>>>(
+            seg_partials_kernel<false><<<unsigned(max_seg), 256, 0, st>>>(
                 xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
             seg_fold_kernel<false><<<grid_for(k * d, 128), 128, 0, st>>>(
