@@ -93,6 +93,27 @@ def make_data(seed=0):
     return x
 
 
+def _campaign_schedule(p, iters, m, k, seed, bm=32, bn=256):
+    """Per-tile-probability campaign drawn vectorised (same distribution as
+    faults.plan_faults' per-tile-prob mode with uniform bits, not its draw
+    order -- plan_faults walks every (iteration, tile) in Python, far too slow
+    for a ~1 s campaign over 125k tiles)."""
+    from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule
+
+    rng = np.random.default_rng(seed)
+    nbi, nbj = (m + bm - 1) // bm, (k + bn - 1) // bn
+    n_hit = rng.binomial(iters * nbi * nbj, p)
+    flat = np.unique(rng.integers(0, iters * nbi * nbj, size=n_hit))
+    out = []
+    for f in flat.tolist():
+        it, t = divmod(f, nbi * nbj)
+        bi, bj = divmod(t, nbj)
+        mi, nj = min(bm, m - bi * bm), min(bn, k - bj * bn)
+        out.append(FaultEntry(it, (bi, bj), (int(rng.integers(0, mi)), int(rng.integers(0, nj))),
+                              int(rng.integers(0, 32))))
+    return FaultSchedule(out)
+
+
 # ------------------------------------------------------------- reference --
 def cpu_reference(x, threads=None, sample_rows=50_000, iters=2):
     """Times the oracle's Lloyd iteration (assign + update; C, all host
@@ -210,6 +231,33 @@ def run_ours(args, rank, world):
     injected = len(hook.injected)
     rep = eng.report
 
+    # fault campaign long enough (~1 s of iterations) for tens of injected
+    # errors at ~50/s: FT-on iterations under injection vs the FT-off step time
+    campaign = None
+    if args.campaign_s > 0:
+        c_iters = max(50, int(args.campaign_s / max(ms_ft * 1e-3, 1e-6)))
+        c_sched = _campaign_schedule(p, c_iters + 1, hi - lo, K, seed=2)
+        c_hook = ScheduledFaultHook(c_sched)
+        c_eng = engine("abft", c_hook)
+        c_eng.step(0)
+        torch.cuda.synchronize()
+        cst, cen = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cst.record()
+        for it in range(1, c_iters + 1):
+            c_eng.step(it)
+        cen.record()
+        torch.cuda.synchronize()
+        c_ms = cst.elapsed_time(cen)
+        c_eng.close()
+        c_rep = c_eng.report
+        c_inj = sum(1 for e in c_hook.injected if e["iteration"] >= 1)
+        campaign = {"iters": c_iters, "device_s": c_ms * 1e-3, "ms_per_step": c_ms / c_iters,
+                    "injected": c_inj, "injected_per_s": c_inj / (c_ms * 1e-3),
+                    "detections": c_rep.detections, "corrections": c_rep.corrections,
+                    "uncorrectable": c_rep.uncorrectable,
+                    "overhead_vs_ft_off_pct": 100.0 * ((c_ms / c_iters) / ms_off - 1.0),
+                    "p_tile": p}
+
     flops = 2.0 * N_ROWS * DIM * K / world
     hbm, bf16, src = _peaks()
     tf32_peak = bf16 / 2.0
@@ -266,6 +314,7 @@ def run_ours(args, rank, world):
         "faults": {"injected": injected, "per_s": injected / (ms_ft * 1e-3 * horizon),
                    "detections": rep.detections, "corrections": rep.corrections,
                    "uncorrectable": rep.uncorrectable, "p_tile": p},
+        "ft_campaign": campaign,
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,
@@ -281,6 +330,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--variant", default=None)
+    ap.add_argument("--campaign-s", type=float, default=1.0,
+                    help="seconds of ABFT iterations under ~50 injected errors/s (0: skip)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
