@@ -64,7 +64,7 @@ class ClockSampler:
                     self.rows.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self._t.start()
@@ -242,11 +242,13 @@ def run_ours(args, rank, world):
         c_eng.step(0)
         torch.cuda.synchronize()
         cst, cen = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        cst.record()
-        for it in range(1, c_iters + 1):
-            c_eng.step(it)
-        cen.record()
-        torch.cuda.synchronize()
+        with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as ccs:
+            cst.record()
+            for it in range(1, c_iters + 1):
+                c_eng.step(it)
+            cen.record()
+            torch.cuda.synchronize()
+        c_clocks = ccs.summary()
         c_ms = cst.elapsed_time(cen)
         c_eng.close()
         c_rep = c_eng.report
@@ -256,7 +258,7 @@ def run_ours(args, rank, world):
                     "detections": c_rep.detections, "corrections": c_rep.corrections,
                     "uncorrectable": c_rep.uncorrectable,
                     "overhead_vs_ft_off_pct": 100.0 * ((c_ms / c_iters) / ms_off - 1.0),
-                    "p_tile": p}
+                    "p_tile": p, "clocks": c_clocks}
 
     flops = 2.0 * N_ROWS * DIM * K / world
     hbm, bf16, src = _peaks()
