@@ -147,9 +147,10 @@ class DevEvents:
     def reset(self):
         self.count.zero_()
 
-    def read(self):
-        """-> (overflowed, [(rec7..., delta)])"""
-        n = int(self.count.item())
+    def read(self, n=None):
+        """-> (overflowed, [(rec7..., delta)]); `n` = the count if the caller
+        already copied it to the host (saves a synchronisation)."""
+        n = int(self.count.item()) if n is None else int(n)
         m = min(n, self.cap)
         if m == 0:
             return n > self.cap, []

@@ -738,6 +738,7 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
 static unsigned g_last_fb[3] = {0, 0, 0};
 static int g_last_path = 0;  // pass-1 kernel of the last call: 0 single-CTA, 1 CTA pair
 static cudaEvent_t g_time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
+static const unsigned *g_stat_dev[3] = {nullptr, nullptr, nullptr};  // lazily read counters
 
   // pass-1 / pass-2 uncertified, TC ABFT flags
 
@@ -944,65 +945,61 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             g_last_path = 0;
         }
         if (rc) return rc;
+        if (g_last_path == 1) {
+            // ---------------- pass 2, device-driven (no host synchronisation):
+            // the rows pass 1 left uncertified (device count) are gathered and
+            // re-screened by the CTA-pair kernel in COLLECT mode; every
+            // centroid whose screened value can still beat the row's exact d1
+            // is evaluated exactly; rows with too many candidates (or beyond
+            // the pass-2 capacity) are resolved by exact_rows_kernel
+            const unsigned cap_rows = unsigned(std::min<int64_t>(m, std::max<int64_t>(65536, m / 8)));
+            const unsigned row_cap = 256;
+            const unsigned cap = unsigned(std::min<int64_t>(int64_t(cap_rows) * 16 + 65536, int64_t(1) << 30));
+            const size_t gbytes = (sizeof(float) * size_t(cap_rows) * d + 255) & ~size_t(255);
+            const size_t need = gbytes + sizeof(int2) * cap + 8 * size_t(cap_rows) + 4 * size_t(cap_rows) + 256;
+            char *buf = static_cast<char *>(scratch(ctx, SLOT_PAIR_CAND, need, st));
+            if (!buf) return FTK_ERR_CUDA;
+            float *g = reinterpret_cast<float *>(buf);
+            int2 *cand = reinterpret_cast<int2 *>(buf + gbytes);
+            unsigned long long *key = reinterpret_cast<unsigned long long *>(cand + cap);
+            unsigned *row_cnt = reinterpret_cast<unsigned *>(key + cap_rows);
+            unsigned *ccount = row_cnt + cap_rows;  // [0] candidates, [1] rows for the exact kernel
+            FTK_CUDA(cudaMemsetAsync(ccount, 0, 2 * sizeof(unsigned), st));
+            if ((rc = pass2_gather_run(xf, d, rows1, cnt, cap_rows, pair_fb_seed, g, key, row_cnt, st)))
+                return rc;
+            CUtensorMap mg, mc64;
+            if ((rc = make_map(&mg, g, cap_rows, d, TC_BM)) ||
+                (rc = make_map(&mc64, yf, k, d, PAIR_BN / 2)))
+                return rc;
+            PairParams Q{};
+            Q.x = g; Q.y = yf; Q.yn = ynf; Q.m = cap_rows; Q.k = k; Q.d = d;
+            Q.m_dev = cnt;
+            Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
+            Q.thr = pair_fb_thr;
+            Q.cand = cand;
+            Q.cand_count = ccount;
+            Q.cand_cap = cap;
+            Q.row_cnt = row_cnt;
+            if ((rc = pair_screen_launch(mg, mc64, Q, false, st))) return rc;
+            if ((rc = pair_candidates_run(g, yf, ynf, d, cand, ccount, cap, row_cnt, row_cap, key,
+                                          rows1, cnt, cap_rows, out_idx, outv, rows2, ccount + 1, st)))
+                return rc;
+            if ((rc = exact_rows_run(xf, yf, ynf, k, d, rows2, ccount + 1, out_idx, outv, st))) return rc;
+            g_stat_dev[0] = cnt;          // read lazily by tc_last_fallback
+            g_stat_dev[1] = ccount + 1;
+            g_stat_dev[2] = ft ? cnt + 2 : nullptr;
+            if (ft && ft->inj && ft->inj->n > 0)
+                return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
+            return FTK_OK;
+        }
         FTK_CUDA(cudaMemcpyAsync(&n1, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         FTK_CUDA(cudaStreamSynchronize(st));
         pass2_rows = rows1;
     }
+    g_stat_dev[0] = g_stat_dev[1] = g_stat_dev[2] = nullptr;
     g_last_fb[0] = n1;
     g_last_fb[1] = 0;
-    if (n1 > 0 && pair_fb_thr && !split_only) {
-        // ---------------- pass 2 (CTA-pair path): 1xTF32 re-screen of the
-        // gathered uncertified rows collecting every centroid whose screened
-        // value can still beat the row's exact d1, then exact evaluation of
-        // those candidates only; rows with too many candidates go exact
-        const unsigned row_cap = 256;
-        const unsigned cap = unsigned(std::min<int64_t>(int64_t(n1) * 16 + 65536, int64_t(1) << 30));
-        const size_t gbytes = (sizeof(float) * size_t(n1) * d + 255) & ~size_t(255);
-        const size_t need = gbytes + sizeof(int2) * cap + 8 * size_t(n1) + 4 * size_t(n1) + 256;
-        char *buf = static_cast<char *>(scratch(ctx, SLOT_PAIR_CAND, need, st));
-        if (!buf) return FTK_ERR_CUDA;
-        float *g = reinterpret_cast<float *>(buf);
-        int2 *cand = reinterpret_cast<int2 *>(buf + gbytes);
-        unsigned long long *key = reinterpret_cast<unsigned long long *>(cand + cap);
-        unsigned *row_cnt = reinterpret_cast<unsigned *>(key + n1);
-        unsigned *ccount = row_cnt + n1;  // [0] candidates, [1] rows left for the exact kernel
-        FTK_CUDA(cudaMemsetAsync(row_cnt, 0, sizeof(unsigned) * (size_t(n1) + 2), st));
-        FTK_CUDA(cudaMemcpyAsync(key, pair_fb_seed, 8 * size_t(n1), cudaMemcpyDeviceToDevice, st));
-        gather_rows_kernel<<<148 * 8, 256, 0, st>>>(xf, d, rows1, cnt, g, nullptr);
-        FTK_LAUNCHED("gather_rows_kernel");
-        CUtensorMap mg, mc64;
-        if ((rc = make_map(&mg, g, n1, d, TC_BM)) || (rc = make_map(&mc64, yf, k, d, PAIR_BN / 2)))
-            return rc;
-        PairParams Q{};
-        Q.x = g; Q.y = yf; Q.yn = ynf; Q.m = n1; Q.k = k; Q.d = d;
-        Q.cmax2 = P.cmax2; Q.ecmax2 = P.ecmax2;
-        Q.thr = pair_fb_thr;
-        Q.cand = cand;
-        Q.cand_count = ccount;
-        Q.cand_cap = cap;
-        Q.row_cnt = row_cnt;
-        if ((rc = pair_screen_launch(mg, mc64, Q, false, st))) return rc;
-        if ((rc = pair_candidates_run(g, yf, ynf, d, cand, ccount, cap, row_cnt, row_cap, key, rows1,
-                                      cnt, out_idx, outv, rows2, ccount + 1, st)))
-            return rc;
-        unsigned n2 = 0;
-        FTK_CUDA(cudaMemcpyAsync(&n2, ccount + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-        FTK_CUDA(cudaStreamSynchronize(st));
-        g_last_fb[1] = n2;
-        if (n2 > 0) {
-            float *g2 = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * (size_t(n2) * (d + 2)) + 64, st));
-            if (!g2) return FTK_ERR_CUDA;
-            gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, ccount + 1, g2, nullptr);
-            FTK_LAUNCHED("gather_rows_kernel");
-            int32_t *idx2 = reinterpret_cast<int32_t *>(g2 + size_t(n2) * d);
-            float *val2 = g2 + size_t(n2) * d + n2;
-            rc = exact_run(ctx, FTK_F32, g2, yf, ynf, n2, k, d, 8, 256, 16, idx2, val2, nullptr,
-                           false, 0.0, 0.0, 0, nullptr, nullptr, st);
-            if (rc) return rc;
-            scatter_rows_kernel<float><<<148, 256, 0, st>>>(rows2, ccount + 1, idx2, val2, out_idx, outv);
-            FTK_LAUNCHED("scatter_rows_kernel");
-        }
-    } else if (n1 > 0) {
+    if (n1 > 0) {
         // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
         float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
         if (!g) return FTK_ERR_CUDA;
@@ -1101,7 +1098,15 @@ float tc_last_pass1_ms() {
     return ms;
 }
 
-int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t) {
+int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t st) {
+    if (g_stat_dev[0]) {  // device-driven pass 2: counters still on the device
+        FTK_CUDA(cudaStreamSynchronize(st));
+        for (int q = 0; q < 3; ++q) {
+            g_last_fb[q] = 0;
+            if (g_stat_dev[q])
+                FTK_CUDA(cudaMemcpy(&g_last_fb[q], g_stat_dev[q], sizeof(unsigned), cudaMemcpyDeviceToHost));
+        }
+    }
     out[0] = g_last_fb[0];
     out[1] = g_last_fb[1];
     out[2] = g_last_fb[2];

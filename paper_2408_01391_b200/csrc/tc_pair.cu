@@ -92,7 +92,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     long long clk[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // debug timing (P.clk)
-    const int64_t npt = (P.m + 2 * PR_BM - 1) / (2 * PR_BM);  // row pair-tiles
+    // rows of this launch: a device-side count when the caller does not know it
+    // on the host (pass 2 over the rows pass 1 left uncertified)
+    const int64_t M = P.m_dev ? (int64_t(*P.m_dev) < P.m ? int64_t(*P.m_dev) : P.m) : P.m;
+    const int64_t npt = (M + 2 * PR_BM - 1) / (2 * PR_BM);  // row pair-tiles
     const int64_t pt0 = cluster_id_x(), pstride = ncluster_x();
 
     if (warp == W_PROD && lane == 0) {
@@ -223,8 +226,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             double rsum = 0.0;
             int inj_c = -1;
             float inj_b = 0.0f, inj_a = 0.0f;
-            const float thr = (COLLECT && grow < P.m) ? P.thr[grow] : -INFINITY;
-            if (CHK && P.inj_col && grow < P.m) {
+            const float thr = (COLLECT && grow < M) ? P.thr[grow] : -INFINITY;
+            if (CHK && P.inj_col && grow < M) {
                 inj_c = P.inj_col[grow];
                 if (inj_c >= 0) {
                     inj_b = P.inj_before[grow];
@@ -364,7 +367,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             float dval = 0.0f;
             float thr_out = INFINITY;          // pass-2 candidate threshold
             unsigned long long seed_out = ~0ull;  // (ordered d1, j1) key
-            const bool active = !COLLECT && grow < P.m && m1 < INFINITY && !(P.dbg & 2);
+            const bool active = !COLLECT && grow < M && m1 < INFINITY && !(P.dbg & 2);
             if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
@@ -482,7 +485,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
               }
                 clk[9] += clock64() - lp1_;
             }
-            if (!COLLECT && grow < P.m) {
+            if (!COLLECT && grow < M) {
                 if (ok) {
                     P.out_idx[grow] = j;
                     P.out_val[grow] = dval;
@@ -490,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             // warp-aggregated append of the uncertified rows, with what pass 2
             // needs: the candidate threshold and the seed (exact d1, j1)
-            const bool need = !COLLECT && grow < P.m && !ok;
+            const bool need = !COLLECT && grow < M && !ok;
             const unsigned bal = __ballot_sync(0xffffffffu, need);
             if (bal) {
                 unsigned base = 0;
@@ -610,9 +613,10 @@ __global__ void cand_exact_kernel(const float *g, const float *y, const float *y
     }
 }
 
-// Resolved rows write their outputs; rows whose candidate set overflowed
-// (or the whole pass when the global list did) go to the exact kernel.
-__global__ void cand_finalize_kernel(const int32_t *rows, const unsigned *n_rows,
+// Resolved rows write their outputs; rows whose candidate set overflowed,
+// rows beyond the pass-2 capacity (or the whole pass when the global list
+// did) go to the exact kernel.
+__global__ void cand_finalize_kernel(const int32_t *rows, const unsigned *n_rows, unsigned row_cap_n,
                                      const unsigned long long *key, const unsigned *row_cnt,
                                      unsigned row_cap, const unsigned *count, unsigned cap,
                                      int32_t *out_idx, float *out_val, int32_t *rows2,
@@ -621,7 +625,7 @@ __global__ void cand_finalize_kernel(const int32_t *rows, const unsigned *n_rows
     const bool global_over = *count > cap;
     for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
         const int32_t row = rows[q];
-        if (global_over || row_cnt[q] > row_cap) {
+        if (q >= row_cap_n || global_over || row_cnt[q] > row_cap) {
             rows2[atomicAdd(n2, 1u)] = row;
             continue;
         }
@@ -637,15 +641,91 @@ __global__ void cand_finalize_kernel(const int32_t *rows, const unsigned *n_rows
     }
 }
 
+// Gather the pass-1 uncertified rows (device count, clamped to the pass-2
+// capacity) and initialise their candidate keys (the pass-1 seed) and counts.
+__global__ void pass2_gather_kernel(const float *x, int64_t d, const int32_t *rows,
+                                    const unsigned *count, unsigned cap_rows,
+                                    const unsigned long long *seed, float *g,
+                                    unsigned long long *key, unsigned *row_cnt) {
+    const unsigned n = min(*count, cap_rows);
+    const int64_t tot = int64_t(n) * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = e / d, f = e % d;
+        g[e] = x[int64_t(rows[q]) * d + f];
+        if (f == 0) {
+            key[q] = seed[q];
+            row_cnt[q] = 0u;
+        }
+    }
+}
+
+// Exact resolution of the (rare) rows no screen resolved: one warp per row,
+// lanes take centroids j = lane, lane + 32, ...; each distance is the
+// reference's sequential chain, the winner the first strict minimum.
+__global__ void exact_rows_kernel(const float *x, const float *y, const float *yn, int64_t k,
+                                  int64_t d, const int32_t *rows, const unsigned *count,
+                                  int32_t *out_idx, float *out_val) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const unsigned n = *count;
+    for (int64_t q = w0; q < n; q += nw) {
+        const int32_t row = rows[q];
+        const float *xr = x + int64_t(row) * d;
+        float bv = INFINITY;
+        int32_t bj = 0;
+        for (int64_t j = lane; j < k; j += 32) {
+            const float *cr = y + j * d;
+            float acc = 0.0f;
+            for (int64_t f = 0; f < d; ++f) acc = __fadd_rn(acc, __fmul_rn(__ldg(xr + f), __ldg(cr + f)));
+            const float v = __fsub_rn(__ldg(yn + j), __fadd_rn(acc, acc));
+            if (v < bv) {
+                bv = v;
+                bj = int32_t(j);
+            }
+        }
+        for (int off = 16; off; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, off);
+            if (ov < bv || (ov == bv && oj < bj)) {
+                bv = ov;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            out_idx[row] = bj;
+            out_val[row] = bv;
+        }
+    }
+}
+
+int pass2_gather_run(const float *x, int64_t d, const int32_t *rows, const unsigned *count,
+                     unsigned cap_rows, const unsigned long long *seed, float *g,
+                     unsigned long long *key, unsigned *row_cnt, cudaStream_t st) {
+    pass2_gather_kernel<<<148 * 8, 256, 0, st>>>(x, d, rows, count, cap_rows, seed, g, key, row_cnt);
+    FTK_LAUNCHED("pass2_gather_kernel");
+    return FTK_OK;
+}
+
+int exact_rows_run(const float *x, const float *y, const float *yn, int64_t k, int64_t d,
+                   const int32_t *rows, const unsigned *count, int32_t *out_idx, float *out_val,
+                   cudaStream_t st) {
+    exact_rows_kernel<<<148 * 2, 256, 0, st>>>(x, y, yn, k, d, rows, count, out_idx, out_val);
+    FTK_LAUNCHED("exact_rows_kernel");
+    return FTK_OK;
+}
+
 int pair_candidates_run(const float *g, const float *y, const float *yn, int64_t d,
                         const int2 *cand, const unsigned *count, unsigned cap,
                         const unsigned *row_cnt, unsigned row_cap, unsigned long long *key,
-                        const int32_t *rows, const unsigned *n_rows, int32_t *out_idx,
-                        float *out_val, int32_t *rows2, unsigned *n2, cudaStream_t st) {
+                        const int32_t *rows, const unsigned *n_rows, unsigned row_cap_n,
+                        int32_t *out_idx, float *out_val, int32_t *rows2, unsigned *n2,
+                        cudaStream_t st) {
     cand_exact_kernel<<<148 * 8, 256, 0, st>>>(g, y, yn, d, cand, count, cap, row_cnt, row_cap, key);
     FTK_LAUNCHED("cand_exact_kernel");
-    cand_finalize_kernel<<<148, 256, 0, st>>>(rows, n_rows, key, row_cnt, row_cap, count, cap,
-                                              out_idx, out_val, rows2, n2);
+    cand_finalize_kernel<<<148, 256, 0, st>>>(rows, n_rows, row_cap_n, key, row_cnt, row_cap,
+                                              count, cap, out_idx, out_val, rows2, n2);
     FTK_LAUNCHED("cand_finalize_kernel");
     return FTK_OK;
 }

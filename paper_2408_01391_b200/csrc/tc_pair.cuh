@@ -40,6 +40,7 @@ struct PairParams {
     unsigned *cand_count;
     unsigned cand_cap;
     unsigned *row_cnt;
+    const unsigned *m_dev;  // device-side row count (<= m) or null
     const float4 *rowinfo;  // per-fit row bounds (|x|^2, |x - tf32 x|^2, max|x|) or null
     long long *clk;  // debug: per-role clock64 sums (screen busy/wait, MMA waits), or null
     int dbg;  // bit 0: skip the screen math, bit 1: skip the refine (pipeline timing only)
@@ -54,8 +55,15 @@ namespace ftk {
 int pair_candidates_run(const float *g, const float *y, const float *yn, int64_t d,
                         const int2 *cand, const unsigned *count, unsigned cap,
                         const unsigned *row_cnt, unsigned row_cap, unsigned long long *key,
-                        const int32_t *rows, const unsigned *n_rows, int32_t *out_idx,
-                        float *out_val, int32_t *rows2, unsigned *n2, cudaStream_t st);
+                        const int32_t *rows, const unsigned *n_rows, unsigned row_cap_n,
+                        int32_t *out_idx, float *out_val, int32_t *rows2, unsigned *n2,
+                        cudaStream_t st);
+int pass2_gather_run(const float *x, int64_t d, const int32_t *rows, const unsigned *count,
+                     unsigned cap_rows, const unsigned long long *seed, float *g,
+                     unsigned long long *key, unsigned *row_cnt, cudaStream_t st);
+int exact_rows_run(const float *x, const float *y, const float *yn, int64_t k, int64_t d,
+                   const int32_t *rows, const unsigned *count, int32_t *out_idx, float *out_val,
+                   cudaStream_t st);
 }  // namespace ftk
 
 namespace ftk {

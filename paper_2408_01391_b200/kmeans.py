@@ -242,11 +242,11 @@ class _DeviceAssign:
                      out_val=self.md)
         return inj
 
-    def finish(self, hook, iteration, inj):
+    def finish(self, hook, iteration, inj, n_events=None):
         """Host side of the pass: events -> report, applied flips -> hook."""
         report = None
         if self.checked:
-            overflow, raw = self.events.read()
+            overflow, raw = self.events.read(n_events)
             if overflow:
                 raise RuntimeError("detection event buffer overflow; threshold likely "
                                    "miscalibrated")
@@ -285,6 +285,7 @@ class LloydEngine:
         self.ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)     # equal, n_empty, dmr flag
         self.ctl_host = t.zeros(4, dtype=t.float64).pin_memory()
         self.ctl_i32_host = t.zeros(8, dtype=t.int32).pin_memory()
+        self.evc_host = t.zeros(1, dtype=t.int64).pin_memory()  # detection-event count
         self.cent = E.to_dev(c0) if not _is_torch(c0) else c0.to(dev).contiguous()
         self.eps = float(np.finfo(self.dtype).eps)
         self.A = _DeviceAssign(x_t, m, k, self.dtype, cfg, ft_mode,
@@ -306,9 +307,14 @@ class LloydEngine:
         E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
         if it > 0:
             E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
-        rep = A.finish(self.gemm_hook, it, inj)
-        if rep is not None:
-            self.report.merge(rep)
+        if inj is not None or (A.checked and self.dist is not None):
+            # scheduled flips: the hook needs the applied/before/after arrays
+            rep = A.finish(self.gemm_hook, it, inj)
+            if rep is not None:
+                self.report.merge(rep)
+            pending = None
+        else:
+            pending = A  # events read after the single control readback
         sums, counts, ev_upd = _update_dev(self.x_t, A.labels[self.slot], self.k, self.dtype,
                                           self.ft_mode, self.update_hook, it, self.ctl_i32)
         if self.dist is not None:
@@ -318,7 +324,14 @@ class LloydEngine:
         ev[2].record()
         self.ctl_host.copy_(self.ctl_f64, non_blocking=True)
         self.ctl_i32_host.copy_(self.ctl_i32, non_blocking=True)
+        if pending is not None and A.checked:
+            self.evc_host.copy_(A.events.count, non_blocking=True)
         t.cuda.current_stream().synchronize()
+        if pending is not None:
+            rep = A.finish(self.gemm_hook, it, None,
+                           n_events=int(self.evc_host[0]) if A.checked else None)
+            if rep is not None:
+                self.report.merge(rep)
         if int(self.ctl_i32_host[1]):
             if self.dist is not None:
                 self.dist.reseed(self.x_t, counts, self.sq, new_cent)
