@@ -540,9 +540,10 @@ __global__ void block_absmax_kernel(const T *y, int64_t k, int64_t d, int64_t bn
 // _row_sq_norms: s = x0*x0; s += xj*xj, left to right in dtype
 template <typename T>
 __global__ void row_sq_norms_kernel(const T *x, int64_t m, int64_t n, T *out) {
-    // 128 rows per block; columns staged 32 at a time through shared memory
-    // with coalesced loads, each thread then folds its row left to right
-    constexpr int R = 128, C = 32;
+    // 32 rows per block; columns staged 32 at a time through shared memory
+    // (128 threads, 8 independent coalesced loads each), then each row is
+    // folded left to right by its own thread: s = x0*x0; s += xj*xj
+    constexpr int R = 32, C = 32;
     __shared__ T tile[R][C + 1];
     const int64_t r0 = int64_t(blockIdx.x) * R;
     const int64_t rows = m - r0 < R ? m - r0 : R;
@@ -550,15 +551,22 @@ __global__ void row_sq_norms_kernel(const T *x, int64_t m, int64_t n, T *out) {
     for (int64_t c0 = 0; c0 < n; c0 += C) {
         const int cols = int(n - c0 < C ? n - c0 : C);
         __syncthreads();
-        for (int e = threadIdx.x; e < R * C; e += blockDim.x) {
-            const int rr = e / C, cc = e % C;
-            if (rr < rows && cc < cols) tile[rr][cc] = x[(r0 + rr) * n + c0 + cc];
+        T v[R * C / 128];
+#pragma unroll
+        for (int q = 0; q < R * C / 128; ++q) {
+            const int e = threadIdx.x + q * 128, rr = e / C, cc = e % C;
+            v[q] = (rr < rows && cc < cols) ? x[(r0 + rr) * n + c0 + cc] : T(0);
+        }
+#pragma unroll
+        for (int q = 0; q < R * C / 128; ++q) {
+            const int e = threadIdx.x + q * 128;
+            tile[e / C][e % C] = v[q];
         }
         __syncthreads();
         if (threadIdx.x < rows) {
             for (int cc = 0; cc < cols; ++cc) {
-                const T v = tile[threadIdx.x][cc];
-                s = (c0 == 0 && cc == 0) ? mul_rn(v, v) : add_rn(s, mul_rn(v, v));
+                const T w = tile[threadIdx.x][cc];
+                s = (c0 == 0 && cc == 0) ? mul_rn(w, w) : add_rn(s, mul_rn(w, w));
             }
         }
     }
@@ -670,7 +678,7 @@ int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void 
 
 int row_sq_norms_run(int dtype, const void *x, int64_t m, int64_t n, void *out, cudaStream_t st) {
     if (m <= 0) return FTK_OK;
-    unsigned grid = unsigned((m + 127) / 128);
+    unsigned grid = unsigned((m + 31) / 32);
     if (dtype == FTK_F32)
         row_sq_norms_kernel<float><<<grid, 128, 0, st>>>(static_cast<const float *>(x), m, n,
                                                          static_cast<float *>(out));

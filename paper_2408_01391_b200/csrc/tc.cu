@@ -851,8 +851,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     float *csum1 = nullptr, *camax1 = nullptr, *csum2 = nullptr, *camax2 = nullptr;
     if (ft) {
         int rc0 = prep_csum(ctx, SLOT_TC_CSUM1, yf, k, d, P.nkb, 1, &csum1, &camax1, st);
-        if (!rc0) rc0 = prep_csum(ctx, SLOT_TC_CSUM2, yf, k, d, P.nkb, 0, &csum2, &camax2, st);
-        if (rc0) return rc0;
+        if (rc0) return rc0;  // the 3xTF32 checksum centroid is built by the single-CTA pass 2
         P.tau_abs = float(ft->abs_tol);
         P.abft_count = cnt + 2;
         if (ft->inj && ft->inj->n > 0) {
@@ -1033,6 +1032,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         Q.raw = split_only ? raw : nullptr;
         Q.inj_col = nullptr;  // pass-1 flips do not recur in the re-screen
         if (ft) {
+            if ((rc = prep_csum(ctx, SLOT_TC_CSUM2, yf, k, d, P.nkb, 0, &csum2, &camax2, st))) return rc;
             Q.csum = csum2;
             Q.camax = camax2;
             Q.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));

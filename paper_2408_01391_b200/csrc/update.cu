@@ -866,15 +866,17 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
                     int64_t d, int64_t k, double *sums_a, int64_t *counts_a, double *sums_b,
                     int64_t *counts_b, cudaStream_t st) {
     if (k <= 0) return FTK_OK;
-    // counts (privatised histogram when k fits in shared memory)
+    // counts: from the segment boundaries of the sorted labels (below); the
+    // DMR duplicate (counts_b) comes from an independent histogram
     FTK_CUDA(cudaMemsetAsync(counts_a, 0, sizeof(int64_t) * k, st));
-    if (m > 0) {
+    if (m > 0 && counts_b) {
+        FTK_CUDA(cudaMemsetAsync(counts_b, 0, sizeof(int64_t) * k, st));
         if (k <= 12 * 1024) {
             histogram_kernel<<<grid_for(m, 512), 512, sizeof(unsigned) * k, st>>>(
-                labels, m, k, reinterpret_cast<unsigned long long *>(counts_a));
+                labels, m, k, reinterpret_cast<unsigned long long *>(counts_b));
         } else {
             histogram_global_kernel<<<grid_for(m, 512), 512, 0, st>>>(
-                labels, m, reinterpret_cast<unsigned long long *>(counts_a));
+                labels, m, reinterpret_cast<unsigned long long *>(counts_b));
         }
         FTK_LAUNCHED("histogram_kernel");
     }
@@ -897,16 +899,12 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         FTK_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, labels, keys_out, vals_in,
                                                  vals_out, int(m), 0, bits, st));
         count_launch((bits + 7) / 8 * 3);
+        boundary_count_kernel<<<grid_for(m, 256), 256, 0, st>>>(
+            keys_out, m, k, reinterpret_cast<unsigned long long *>(counts_a));
+        FTK_LAUNCHED("boundary_count_kernel");
     }
     exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets);
     FTK_LAUNCHED("exclusive_scan_small_kernel");
-    if (counts_b) {
-        FTK_CUDA(cudaMemsetAsync(counts_b, 0, sizeof(int64_t) * k, st));
-        if (m > 0) {
-            boundary_count_kernel<<<grid_for(m, 256), 256, 0, st>>>(keys_out, m, k, reinterpret_cast<unsigned long long *>(counts_b));
-            FTK_LAUNCHED("boundary_count_kernel");
-        }
-    }
     const int64_t warps = k * ((d + 31) / 32);
     const int block = 256;
     const unsigned grid = unsigned((warps * 32 + block - 1) / block);
