@@ -76,7 +76,28 @@ __device__ __forceinline__ void ds_refine_row(const DsParams &P, int64_t row, do
             const double *xr = P.x + row * P.d;
             const double *cr = P.y + int64_t(j) * P.d;
             double acc = 0.0, xx = 0.0, rref = 0.0, amax = 0.0;
-            for (int64_t f = 0; f < P.d; ++f) {
+            // 8 features per step: the loads of a step are issued together,
+            // then folded in the reference's order
+            int64_t f = 0;
+            for (; f + 8 <= P.d; f += 8) {
+                double xv[8], cv[8], sv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    xv[u] = __ldg(xr + f + u);
+                    cv[u] = __ldg(cr + f + u);
+                    if (CHK) sv[u] = __ldg(P.csum + f + u);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __dadd_rn(acc, __dmul_rn(xv[u], cv[u]));
+                    xx = fma(xv[u], xv[u], xx);
+                    if (CHK) {
+                        rref = fma(xv[u], sv[u], rref);
+                        amax = fmax(amax, fabs(xv[u]));
+                    }
+                }
+            }
+            for (; f < P.d; ++f) {
                 const double xv = __ldg(xr + f);
                 acc = __dadd_rn(acc, __dmul_rn(xv, __ldg(cr + f)));
                 xx = fma(xv, xv, xx);
@@ -244,7 +265,7 @@ __global__ void __launch_bounds__(DS_THREADS, 1) dscreen_kernel(DsParams P) {
 // row tig, column gid; accumulators: rows gid / gid + 8, columns 2 tig, +1.
 // The DMMA accumulates each product into the sum without intermediate
 // rounding of the product (like DFMA), so the DFMA error bound holds.
-constexpr int DM_BM = 128, DM_BN = 128, DM_KC = 8, DM_STAGES = 4;
+constexpr int DM_BM = 128, DM_BN = 128, DM_KC = 16, DM_STAGES = 4;
 constexpr int DM_PA = DM_BM + 4, DM_PB = DM_BN + 4;  // padded k-rows: conflict-free fragments
 
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
@@ -303,14 +324,14 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
                 if (kc < nkc) {
 #pragma unroll
                     for (int q = 0; q < DM_BM * DM_KC / 256; ++q) {
-                        const int e = tid + q * 256, rr = e >> 3, kk = e & 7;
+                        const int e = tid + q * 256, rr = e / DM_KC, kk = e % DM_KC;
                         const int64_t row = r0 + rr, kcol = k0 + kk;
                         const bool ok = row < P.m && kcol < P.d;
                         cp_async8_zfill(&As[buf][kk][rr], ok ? P.x + row * P.d + kcol : P.x, ok);
                     }
 #pragma unroll
                     for (int q = 0; q < DM_BN * DM_KC / 256; ++q) {
-                        const int e = tid + q * 256, cc = e >> 3, kk = e & 7;
+                        const int e = tid + q * 256, cc = e / DM_KC, kk = e % DM_KC;
                         const int64_t col = c0 + cc, kcol = k0 + kk;
                         const bool ok = col < P.k && kcol < P.d;
                         cp_async8_zfill(&Bs[buf][kk][cc], ok ? P.y + col * P.d + kcol : P.y, ok);
