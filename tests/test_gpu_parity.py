@@ -323,3 +323,43 @@ def test_native_library_is_the_one_loaded():
     import os
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert "libftkb200.so" in maps
+
+
+@pytest.mark.parametrize("m,d,k,dt,tiny", [
+    (60000, 32, 2048, np.float32, False),   # segment partials + certified fold (K*D/32 > one wave)
+    (60000, 32, 2048, np.float32, True),    # + tiny values: uncertified chains replayed in order
+    (40000, 96, 5, np.float32, True),       # few long chains: pipelined ordered chains
+    (30000, 24, 7, np.float64, False),      # float64 data: pipelined ordered chains
+])
+def test_update_paths_bit_exact(m, d, k, dt, tiny):
+    """Every update path (segment partials with the exactness certificate,
+    the ordered replay of uncertified chains, the pipelined chain kernel)
+    reproduces numpy.bincount's float64 sums bit for bit."""
+    rng = np.random.default_rng(m + d + k)
+    x = rng.standard_normal((m, d)) * 3.0
+    if tiny:  # magnitudes ~1e-9 next to O(1e3) sums force roundings in the reference chain
+        x[rng.integers(0, m, 200), rng.integers(0, d, 200)] = 1e-9
+    x = np.ascontiguousarray(x, dtype=dt)
+    lab = rng.integers(0, k, m).astype(np.int64)
+    lab[:m // 3] = 0  # one long chain
+    c, counts, _ = P.update_step(x, lab, k)
+    ref, ref_counts = O.update_step(x, lab, k)
+    assert counts.tolist() == ref_counts.tolist()
+    assert c.tobytes() == ref.tobytes()
+
+
+def test_candidate_overflow_rows_go_exact():
+    """Rows whose pass-2 candidate set exceeds its cap (300 identical
+    centroids tie for every row) are resolved by the exact row kernel."""
+    rng = np.random.default_rng(12)
+    base = rng.standard_normal((1, 64)).astype(np.float32)
+    y = np.ascontiguousarray(np.vstack([np.repeat(base, 300, axis=0),
+                                        rng.standard_normal((20, 64)).astype(np.float32) * 5]))
+    x = np.ascontiguousarray(base + 1e-3 * rng.standard_normal((700, 64)).astype(np.float32))
+    res = P.fused_assign(x, y)
+    from paper_2408_01391_b200 import _engine as E
+
+    assert E.tc_fallback_rows()[1] > 0  # the exact row kernel ran
+    ref_lab, ref_val = O.assign(x, y)
+    assert np.array_equal(res.assignments, ref_lab)
+    assert res.min_dists.tobytes() == ref_val.tobytes()
