@@ -91,6 +91,13 @@ int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info
  * no counterpart (its kernels recompute nothing across calls). */
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info);
 
+/* k-means++ seeding step (kmeans.py:95-103): d2[i] = sum_f (x[i,f] - x[pick,f])^2 in
+ * float64 with numpy's pairwise association (a single leaf: d <= 128), then
+ * np.minimum with the previous d2 unless `first`.  The host keeps the
+ * reference's Generator draws and its cumsum/searchsorted. */
+int ftk_kpp_d2(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t pick,
+               int first, double *d2, void *stream);
+
 /* out[i] = left-to-right sum of x[i,j]^2 in the data dtype. */
 int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,
                      void *stream);

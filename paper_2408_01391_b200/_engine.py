@@ -201,6 +201,14 @@ class RowInfo:
             pass
 
 
+def kpp_d2_dev(x_t, pick, first, d2):
+    """k-means++ D^2 update on the device (ftk_kpp_d2)."""
+    m, d = x_t.shape
+    N.check(N.load().ftk_kpp_d2(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), m, d, int(pick),
+                                int(bool(first)), ptr(d2), stream()), "ftk_kpp_d2")
+    return d2
+
+
 def row_sq_norms(x):
     if x.shape[0] == 0:
         return np.empty(0, dtype=x.dtype)

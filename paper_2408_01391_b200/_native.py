@@ -39,6 +39,7 @@ PROTOTYPES = {
     "ftk_ctx_destroy": (None, [_p]),
     "ftk_row_sq_norms": (_int, [_p, _int, _p, _i64, _i64, _p, _p]),
     "ftk_row_info": (_int, [_p, _p, _i64, _i64, _p, _p]),
+    "ftk_kpp_d2": (_int, [_p, _int, _p, _i64, _i64, _i64, _int, _p, _p]),
     "ftk_ctx_set_rows": (_int, [_p, _p, _i64, _i64, _p]),
     "ftk_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p,
                           _p, _p]),

@@ -46,6 +46,7 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 int row_sq_norms_run(int, const void *, int64_t, int64_t, void *, cudaStream_t);
 int row_info_run(const float *, int64_t, int64_t, float *, cudaStream_t);
+int kpp_d2_run(int, const void *, int64_t, int64_t, int64_t, int, double *, cudaStream_t);
 int update_sums_run(ftk_ctx *, int, const void *, const int32_t *, int64_t, int64_t, int64_t,
                     double *, int64_t *, double *, int64_t *, cudaStream_t);
 int dmr_compare_run(const double *, const int64_t *, const double *, const int64_t *, int64_t,
@@ -108,6 +109,12 @@ void ftk_ctx_destroy(ftk_ctx *ctx) {
 int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info, void *stream) {
     if (!ctx || d < 1 || m < 0) { set_error("bad ctx/shape"); return FTK_ERR_ARG; }
     return row_info_run(x, m, d, info, as_stream(stream));
+}
+
+int ftk_kpp_d2(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t pick,
+               int first, double *d2, void *stream) {
+    if (!ctx || !dtype_ok(dtype) || pick < 0 || pick >= m) { set_error("bad ctx/dtype/pick"); return FTK_ERR_ARG; }
+    return kpp_d2_run(dtype, x, m, d, pick, first, d2, as_stream(stream));
 }
 
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info) {

@@ -92,6 +92,8 @@ def init_centroids(x, k, seed=0, method="kmeanspp"):
     rng = np.random.default_rng(seed)
     if method == "random-sample":
         return np.ascontiguousarray(x[rng.choice(m, size=k, replace=False)])
+    if x.shape[1] <= 128 and m > 0:
+        return _kmeanspp_dev(x, k, rng)
     x64 = x.astype(np.float64)
     cs = np.empty((k, x.shape[1]), dtype=np.float64)
     cs[0] = x64[int(rng.integers(0, m))]
@@ -106,6 +108,38 @@ def init_centroids(x, k, seed=0, method="kmeanspp"):
         cs[c] = x64[pick]
         d2 = np.minimum(d2, ((x64 - cs[c]) ** 2).sum(axis=1))
     return np.ascontiguousarray(cs, dtype=x.dtype)
+
+
+def _kmeanspp_dev(x, k, rng):
+    """k-means++ D^2 seeding with the reference's draws (kmeans.py:86-103).
+    The O(N K D) distance updates run on the device (ftk_kpp_d2: float64,
+    numpy's pairwise row reduce, np.minimum); d2.sum() is the device pairwise
+    sum; the reference's own numpy cumsum/searchsorted run on a pinned host
+    copy of d2, so every pick is the reference's."""
+    t = E._torch()
+    m = x.shape[0]
+    x_t = E.to_dev(x)
+    d2 = t.empty(m, dtype=t.float64, device=x_t.device)
+    tot = t.empty(1, dtype=t.float64, device=x_t.device)
+    host = t.empty(m, dtype=t.float64).pin_memory()
+    tot_h = t.empty(1, dtype=t.float64).pin_memory()
+    picks = [int(rng.integers(0, m))]
+    E.kpp_d2_dev(x_t, picks[0], True, d2)
+    h = host.numpy()
+    for _ in range(1, k):
+        E.pairwise_sum_dev(d2, tot)
+        tot_h.copy_(tot, non_blocking=True)
+        host.copy_(d2, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        total = float(tot_h[0])
+        if total <= 0:
+            pick = int(rng.integers(0, m))
+        else:
+            r = rng.random() * total
+            pick = min(int(np.searchsorted(np.cumsum(h), r, side="right")), m - 1)
+        picks.append(pick)
+        E.kpp_d2_dev(x_t, pick, False, d2)
+    return np.ascontiguousarray(x[np.asarray(picks, dtype=np.int64)])
 
 
 def _resolve_tile(tile, x, k, tune_table):

@@ -363,3 +363,15 @@ def test_candidate_overflow_rows_go_exact():
     ref_lab, ref_val = O.assign(x, y)
     assert np.array_equal(res.assignments, ref_lab)
     assert res.min_dists.tobytes() == ref_val.tobytes()
+
+
+@pytest.mark.parametrize("m,d,k,prec", [(20000, 32, 64, "single"), (5000, 100, 40, "double"),
+                                        (3000, 5, 17, "single")])
+def test_kmeanspp_seeding_matches_reference(m, d, k, prec):
+    """GPU D^2 seeding (float64 pairwise row reduce on the device, the
+    reference's Generator draws and cumsum/searchsorted on the host) picks
+    exactly the reference's centroids (kmeans.py:86-103)."""
+    x, _, _ = P.gaussian_mixture(m, d, k, 0.3, precision=prec, seed=5)
+    got = P.init_centroids(x, k, seed=9, method="kmeanspp")
+    ref = O.init_centroids(x, k, 9, "kmeanspp")
+    assert got.tobytes() == ref.tobytes()
