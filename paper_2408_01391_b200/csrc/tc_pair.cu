@@ -36,6 +36,16 @@
 #include "tc_ptx.cuh"
 #include "tc_pair.cuh"
 
+// Role-timing probes (clock64 sums per role, printed by FTK_PAIR_CLK=1) are
+// compiled in only with -DFTK_PAIR_PROBE: they cost registers in the hot loop.
+#ifdef FTK_PAIR_PROBE
+#define PROBE_T(v) const long long v = clock64()
+#define PROBE_ADD(i, x) (clk[i] += (x))
+#else
+#define PROBE_T(v)
+#define PROBE_ADD(i, x)
+#endif
+
 namespace ftk {
 
 constexpr int PR_BM = 128;          // rows per CTA
@@ -91,7 +101,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
+#ifdef FTK_PAIR_PROBE
     long long clk[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // debug timing (P.clk)
+#endif
     // rows of this launch: a device-side count when the caller does not know it
     // on the host (pass 2 over the rows pass 1 left uncertified)
     const int64_t M = P.m_dev ? (int64_t(*P.m_dev) < P.m ? int64_t(*P.m_dev) : P.m) : P.m;
@@ -153,16 +165,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             int it = 0;
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
                 const int ab = it % NA;
-                { const long long c0_ = clock64(); mbar_wait(&a_full[ab], uint32_t(it / NA) & 1); clk[4] += clock64() - c0_; }
+                { PROBE_T(c0_); mbar_wait(&a_full[ab], uint32_t(it / NA) & 1); PROBE_ADD(4, clock64() - c0_); }
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA) + uint32_t(ab) * A_BYTES;
                 for (int t = 0; t < P.ntiles; ++t, ++g) {
                     const int buf = g % PR_NBUF;
-                    { const long long c0_ = clock64(); mbar_wait(&t_empty[buf], ((g / PR_NBUF) & 1) ^ 1); clk[2] += clock64() - c0_; }
+                    { PROBE_T(c0_); mbar_wait(&t_empty[buf], ((g / PR_NBUF) & 1) ^ 1); PROBE_ADD(2, clock64() - c0_); }
                     tc_fence_after();
                     const uint32_t d_tmem = tmem + uint32_t(buf * PR_BN);
                     for (int kb = 0; kb < nkb; ++kb) {
-                        { const long long c0_ = clock64(); mbar_wait(&full[stage], phase); clk[3] += clock64() - c0_; }
+                        { PROBE_T(c0_); mbar_wait(&full[stage], phase); PROBE_ADD(3, clock64() - c0_); }
                         tc_fence_after();
                         const uint32_t bs = b_base + uint32_t(stage) * PR_B_HALF;
 #pragma unroll
@@ -185,9 +197,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const uint32_t lead = mapa_shared(smem_u32(&a_full[0]), 0);
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
                 const int ab = it % NA;
-                const long long xw0_ = clock64();
                 mbar_wait(&a_empty[ab], (uint32_t(it / NA) & 1) ^ 1);
-                const long long xw1_ = clock64();
                 unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
                 mbar_expect_tx(&a_full[ab], A_BYTES);
@@ -240,7 +250,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 // prefetch the next tile's norms (wrapping into the next row tile)
                 const int64_t cn = int64_t((t + 1) % P.ntiles) * PR_BN + et;
                 const float yn_next = (et < PR_BN && cn < P.k) ? __ldg(P.yn + cn) : INFINITY;
-                const long long cw_ = clock64(); mbar_wait(&t_full[buf], (g / PR_NBUF) & 1); const long long cb_ = clock64(); clk[1] += cb_ - cw_;
+                PROBE_T(cw_); mbar_wait(&t_full[buf], (g / PR_NBUF) & 1); PROBE_T(cb_); PROBE_ADD(1, cb_ - cw_);
                 tc_fence_after();
                 float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
                 float s0 = 0.0f, s1 = 0.0f;
@@ -308,7 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive_remote(t_empty_lead0 + uint32_t(buf) * 8u); clk[0] += clock64() - cb_; clk[5] += 1;
+                if (lane == 0) mbar_arrive_remote(t_empty_lead0 + uint32_t(buf) * 8u); PROBE_ADD(0, clock64() - cb_); PROBE_ADD(5, 1);
                 // merge the two chains into the tile's top-2, then the running top-2
                 const float t1 = fminf(a1, b1);  // b1 = b2 = inf: single chain
                 const float t2 = fminf(fminf(a2, b2), fmaxf(a1, b1));
@@ -346,10 +356,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
             const int ab = it % NA;
-            const long long rw0_ = clock64();
+            PROBE_T(rw0_);
             mbar_wait(&p_full[pb], uint32_t(it >> 1) & 1);
-            const long long rw1_ = clock64();
-            clk[6] += rw1_ - rw0_;
+            PROBE_T(rw1_);
+            PROBE_ADD(6, rw1_ - rw0_);
             const PairPart q0 = part[(pb * 2 + 0) * PR_BM + r];
             const PairPart q1 = part[(pb * 2 + 1) * PR_BM + r];
             double rsum = 0.0;
@@ -406,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         wst[rr * 8 + (q ^ (rr & 7))] = nxt[i];
                     }
                 };
-                const long long lp0_ = clock64();
+                PROBE_T(lp0_);
                 gather(0);
                 for (int kb = 0; kb < nkb; ++kb) {
                     __syncwarp();
@@ -452,8 +462,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         }
                     }
                 }
-                const long long lp1_ = clock64();
-                clk[8] += lp1_ - lp0_;
+                PROBE_T(lp1_);
+                PROBE_ADD(8, lp1_ - lp0_);
               if (active) {  // lanes without a live row only helped with the loads
                 const float xn = sqrtf(xx * (1.0f + 0x1p-10f));
                 const float cm = sqrtf(*P.cmax2 * (1.0f + 0x1p-10f));
@@ -483,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 ok = !abft_bad && sane &&
                      (m2 - A - P.b_coef * fabsf(m2) - 0x1p-21f * (fabsf(m1) + fabsf(m2)) > dval);
               }
-                clk[9] += clock64() - lp1_;
+                PROBE_ADD(9, clock64() - lp1_);
             }
             if (!COLLECT && grow < M) {
                 if (ok) {
@@ -510,13 +520,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_empty[ab]);  // X half no longer read
-            clk[7] += clock64() - rw1_;
+            PROBE_ADD(7, clock64() - rw1_);
         }
     }
 
+#ifdef FTK_PAIR_PROBE
     if (P.clk && lane == 0 && (warp == 0 || warp == W_MMA || warp == W_REFINE0 || warp == W_XPROD))
         for (int q = 0; q < 10; ++q) atomicAdd(reinterpret_cast<unsigned long long *>(P.clk) + q,
                                               (unsigned long long)clk[q]);
+#endif
     tc_fence_before();
     __syncthreads();
     cluster_sync_all();
