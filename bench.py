@@ -185,22 +185,23 @@ def run_ours(args, rank, world):
 
     def engine(ft_mode, hook=None):
         return LloydEngine(x_t, c0, K, np.float32, cfg, ft_mode, thr, 64,
-                           gemm_hook=hook or P.FaultHook(), dist=comm)
+                           gemm_hook=hook or P.FaultHook(), dist=comm, graph=True)
 
     def time_steps(eng, steps, warmup, sampler=None):
         for it in range(warmup):
             eng.step(it)
+        # one eager (non-graph) step: phase timings and CUDA events around the
+        # screen launch on its stream (graph replays carry no events)
+        eng.step(warmup, eager=True)
+        a_ms, k_ms = [eng.assign_ms], [E.tc_last_kernel_ms()]
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        a_ms, k_ms = [], []
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = _native.launch_count()
         st.record()
-        for it in range(warmup, warmup + steps):
+        for it in range(warmup + 1, warmup + 1 + steps):
             eng.step(it)
-            a_ms.append(eng.assign_ms)
-            k_ms.append(E.tc_last_kernel_ms())  # events around the screen launch (its stream)
         en.record()
         torch.cuda.synchronize()
         launches = _native.launch_count() - l0
@@ -218,7 +219,7 @@ def run_ours(args, rank, world):
     eng_off.close()
     n_tiles = ((hi - lo + cfg.block[0] - 1) // cfg.block[0]) * ((K + cfg.block[1] - 1) // cfg.block[1])
     p = min(1.0, ERR_PER_S * (ms_off * 1e-3) / n_tiles)
-    horizon = args.warmup + args.steps
+    horizon = args.warmup + args.steps + 1
     spec = FaultSpec(mode="per-tile-prob", prob=p, seed=1)
     sched = plan_faults(spec, horizon, ((hi - lo + 31) // 32, (K + 255) // 256), (32, 256),
                         dtype=np.float32, shape=(hi - lo, K))

@@ -75,6 +75,9 @@ const char *ftk_last_error(void);
 int ftk_version(void);
 /* Number of kernels this library launched since load (for launch accounting). */
 int64_t ftk_launch_count(void);
+/* Account n kernels replayed from a CUDA graph captured from this library's
+ * launches (the replay itself bypasses the launch sites). */
+void ftk_add_launches(int64_t n);
 
 ftk_ctx *ftk_ctx_create(int device);
 void ftk_ctx_destroy(ftk_ctx *ctx);

@@ -35,6 +35,7 @@ PROTOTYPES = {
     "ftk_last_error": (ctypes.c_char_p, []),
     "ftk_version": (_int, []),
     "ftk_launch_count": (_i64, []),
+    "ftk_add_launches": (None, [_i64]),
     "ftk_ctx_create": (_p, [_int]),
     "ftk_ctx_destroy": (None, [_p]),
     "ftk_row_sq_norms": (_int, [_p, _int, _p, _i64, _i64, _p, _p]),

@@ -264,6 +264,8 @@ int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
     return rc;
 }
 
+void ftk_add_launches(int64_t n) { count_launch(int(n)); }
+
 int ftk_tc_last_kernel_ms(ftk_ctx *ctx, float *ms) {
     if (!ctx || !ms) { set_error("bad ctx"); return FTK_ERR_ARG; }
     *ms = tc_last_pass1_ms();

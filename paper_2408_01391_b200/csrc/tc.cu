@@ -922,11 +922,16 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                 cudaEventCreate(&ev0);
                 cudaEventCreate(&ev1);
             }
-            cudaEventRecord(ev0, st);
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            cudaStreamIsCapturing(st, &cap);
+            const bool timed = cap == cudaStreamCaptureStatusNone;  // no timing inside graphs
+            if (timed) cudaEventRecord(ev0, st);
             rc = pair_screen_launch(mx, mc128, Q, ft != nullptr, st);
-            cudaEventRecord(ev1, st);
-            g_time_ev[0] = ev0;
-            g_time_ev[1] = ev1;
+            if (timed) {
+                cudaEventRecord(ev1, st);
+                g_time_ev[0] = ev0;
+                g_time_ev[1] = ev1;
+            }
             g_last_path = 1;
             if (Q.clk) {
                 long long h[10];

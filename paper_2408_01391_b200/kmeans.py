@@ -18,10 +18,11 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _engine as E
+from . import _native as N
 from .abft import DetectionEvent, DetectionReport, Threshold, checked_assign, events_from_ring
 from .abft import _scheduled_tiles
 from .errors import FaultEscalationError
-from .faults import NOOP_HOOK, FaultSpec, ScheduledFaultHook, plan_faults
+from .faults import NOOP_HOOK, FaultHook, FaultSpec, ScheduledFaultHook, plan_faults
 from .gemm import _as_operand, _dtype, _is_torch, fused_assign, get_variant, resolve_threads
 from .matrix import as_matrix
 from .tiles import TileConfig, default_config
@@ -303,7 +304,7 @@ class LloydEngine:
     rules; bench.py times exact step counts through it."""
 
     def __init__(self, x_t, c0, k, dtype, cfg, ft_mode, thr, threads, gemm_hook=NOOP_HOOK,
-                 update_hook=NOOP_HOOK, dist=None):
+                 update_hook=NOOP_HOOK, dist=None, graph=False):
         t = E._torch()
         self.t = t
         self.dist = dist  # parallel.ShardComm for row-sharded multi-GPU runs
@@ -329,9 +330,98 @@ class LloydEngine:
         self.ev = [t.cuda.Event(enable_timing=True) for _ in range(3)]
         self.assign_ms = 0.0
         self.update_ms = 0.0
+        # CUDA-graph replay of the device part of a step (one graph per label /
+        # centroid buffer parity); static centroid and count buffers carry the
+        # state across replays.  Eager steps remain for iterations with
+        # scheduled flips, DMR, update-site hooks or multi-GPU.
+        # (only the fp32 CTA-pair assignment is free of host synchronisation)
+        self.use_graph = bool(graph) and dist is None and ft_mode != "abft+dmr" and \
+            update_hook is NOOP_HOOK and self.dtype == np.float32 and \
+            8 <= x_t.shape[1] <= 256 and x_t.shape[1] % 4 == 0 and get_variant() != "exact"
+        self.graphs = [None, None]
+        self.graph_kernels = [0, 0]  # library kernels per replay (launch accounting)
+        self.cent_buf = [t.empty_like(self.cent), t.empty_like(self.cent)]
+        self.cent_buf[0].copy_(self.cent)
+        self.cent = self.cent_buf[0]
+        self.cbuf = 0
+        self.counts_buf = t.zeros(k, dtype=t.int64, device=dev)
+        self._pool = None
 
-    def step(self, it):
-        """One Lloyd iteration; returns (inertia, unchanged, moved)."""
+    def _graph_ok(self, it):
+        """Graph replay is used for steps without scheduled flips (those need
+        the hook's host round trip) once both buffer parities are warm."""
+        if not self.use_graph or it < 1:
+            return False
+        if self.gemm_hook is NOOP_HOOK or type(self.gemm_hook) is FaultHook:
+            return True  # the no-op hook never injects
+        sched = getattr(self.gemm_hook, "schedule", None)
+        return sched is not None and not sched.for_iteration(it)
+
+    def _device_part(self, it):
+        """Launches of one step with no host synchronisation (graph-capturable):
+        assign, inertia, label compare, update sums, finalize into the other
+        static centroid buffer, movement, control copies."""
+        A = self.A
+        yn = E.row_sq_norms_dev(self.cent)
+        A.run(self.cent, yn, NOOP_HOOK, it, self.slot)
+        E.sq_dists_dev(A.md, self.xsq, self.sq)
+        E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
+        E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
+        sa, ca, _, _ = E.update_sums_dev(self.x_t, A.labels[self.slot], self.k, dmr=False)
+        new_cent = self.cent_buf[1 - self.cbuf]
+        E.finalize_dev(sa, ca, self.dtype, out=new_cent, n_empty=self.ctl_i32[1:2])
+        self.counts_buf.copy_(ca)
+        E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+        self.ctl_host.copy_(self.ctl_f64, non_blocking=True)
+        self.ctl_i32_host.copy_(self.ctl_i32, non_blocking=True)
+        if A.checked:
+            self.evc_host.copy_(A.events.count, non_blocking=True)
+
+    def _graph_step(self, it):
+        t, A = self.t, self.A
+        g = self.graphs[self.slot]
+        if g is None:
+            # the step is captured, not run: replay it right after
+            g = t.cuda.CUDAGraph()
+            if self._pool is None:
+                self._pool = t.cuda.graph_pool_handle()
+            t.cuda.synchronize()
+            l0 = N.launch_count()
+            try:
+                with t.cuda.graph(g, pool=self._pool):
+                    self._device_part(it)
+            except Exception:
+                # a launch path that needs the host mid-step: stay eager
+                t.cuda.synchronize()
+                self.use_graph = False
+                N.load().ftk_add_launches(-(N.launch_count() - l0))
+                return self.step(it, eager=True)
+            self.graph_kernels[self.slot] = N.launch_count() - l0
+            N.load().ftk_add_launches(-self.graph_kernels[self.slot])  # captured, not run
+            self.graphs[self.slot] = g
+        g.replay()
+        N.load().ftk_add_launches(self.graph_kernels[self.slot])
+        t.cuda.current_stream().synchronize()
+        rep = A.finish(self.gemm_hook, it, None,
+                       n_events=int(self.evc_host[0]) if A.checked else None)
+        if rep is not None:
+            self.report.merge(rep)
+        new_cent = self.cent_buf[1 - self.cbuf]
+        if int(self.ctl_i32_host[1]):
+            E.reseed_dev(self.x_t, self.counts_buf, self.sq, new_cent)
+            E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+            self.ctl_host.copy_(self.ctl_f64)
+        unchanged = bool(int(self.ctl_i32_host[0]))
+        self.cbuf = 1 - self.cbuf
+        self.cent = self.cent_buf[self.cbuf]
+        self.slot = 1 - self.slot
+        return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
+
+    def step(self, it, eager=False):
+        """One Lloyd iteration; returns (inertia, unchanged, moved).  Eager
+        steps also record the phase timings (assign_ms / update_ms)."""
+        if not eager and self._graph_ok(it) and self.slot == self.cbuf:
+            return self._graph_step(it)
         t, A, ev = self.t, self.A, self.ev
         ev[0].record()
         yn = E.row_sq_norms_dev(self.cent)
@@ -353,7 +443,8 @@ class LloydEngine:
                                           self.ft_mode, self.update_hook, it, self.ctl_i32)
         if self.dist is not None:
             self.dist.reduce_partials(sums, counts, self.ctl_f64, self.ctl_i32, it)
-        new_cent = E.finalize_dev(sums, counts, self.dtype, n_empty=self.ctl_i32[1:2])
+        new_cent = self.cent_buf[1 - self.cbuf]
+        E.finalize_dev(sums, counts, self.dtype, out=new_cent, n_empty=self.ctl_i32[1:2])
         E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
         ev[2].record()
         self.ctl_host.copy_(self.ctl_f64, non_blocking=True)
@@ -377,7 +468,8 @@ class LloydEngine:
         self.update_ms = ev[1].elapsed_time(ev[2])
         self.report.events.extend(ev_upd)
         unchanged = it > 0 and bool(int(self.ctl_i32_host[0]))
-        self.cent = new_cent
+        self.cbuf = 1 - self.cbuf
+        self.cent = self.cent_buf[self.cbuf]
         self.slot = 1 - self.slot
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
 
@@ -422,7 +514,7 @@ def lloyd(x, config, fault_spec=None):
     timings["init_ns"] = time.perf_counter_ns() - t0
 
     eng = LloydEngine(E.to_dev(x), c0, k, dtype, cfg, config.ft_mode, thr, threads, gemm_hook,
-                      update_hook)
+                      update_hook, graph=config.max_iters >= 8)
     history = []
     converged = False
     iters = 0
