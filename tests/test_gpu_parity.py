@@ -375,3 +375,25 @@ def test_kmeanspp_seeding_matches_reference(m, d, k, prec):
     got = P.init_centroids(x, k, seed=9, method="kmeanspp")
     ref = O.init_centroids(x, k, 9, "kmeanspp")
     assert got.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("ft", ["off", "abft"])
+def test_graph_replay_equals_eager(ft):
+    """CUDA-graph replay of the Lloyd step gives the eager step's bits
+    (inertia, label-change flag, movement, centroids) every iteration."""
+    from paper_2408_01391_b200 import _engine as E
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    x, _, _ = P.gaussian_mixture(20000, 64, 96, 0.3, precision="single", seed=3)
+    x_t = E.to_dev(x)
+    c0 = P.init_centroids(x, 96, seed=1, method="random-sample")
+    runs = []
+    for graph in (False, True):
+        eng = LloydEngine(x_t, c0, 96, np.float32, P.default_config(np.float32), ft,
+                          P.Threshold.default_for(np.float32), 8, graph=graph)
+        outs = [eng.step(it) for it in range(9)]
+        runs.append((outs, E.to_host(eng.cent).copy(), eng.graphs[0] is not None))
+        eng.close()
+    assert runs[1][2], "graph mode did not capture"
+    assert runs[0][0] == runs[1][0]
+    assert runs[0][1].tobytes() == runs[1][1].tobytes()
