@@ -75,6 +75,7 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
+        self.rows = [r for r in self.rows if len(r) >= 6]  # drop nvidia-smi error lines
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
@@ -165,11 +166,14 @@ def run_ours(args, rank, world):
     from paper_2408_01391_b200.kmeans import LloydEngine
     from paper_2408_01391_b200.tiles import default_config
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    # FTK_BENCH_DEVICE pins every rank to one GPU and FTK_DIST_BACKEND=gloo
+    # lets the sharded path be exercised on a single-GPU box (test only)
+    dev_env = os.environ.get("FTK_BENCH_DEVICE")
+    torch.cuda.set_device(int(dev_env) if dev_env is not None else int(os.environ.get("LOCAL_RANK", 0)))
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("FTK_DIST_BACKEND", "nccl"))
     x = make_data()
     lo, hi = rank * N_ROWS // world, (rank + 1) * N_ROWS // world
     x_t = E.to_dev(x[lo:hi])
@@ -225,7 +229,7 @@ def run_ours(args, rank, world):
                         dtype=np.float32, shape=(hi - lo, K))
     hook = ScheduledFaultHook(sched)
     eng = engine("abft", hook)
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as cs:
+    with ClockSampler(torch.cuda.current_device()) as cs:
         ms_ft, a_ft, launches, k_ft = time_steps(eng, args.steps, args.warmup, cs)
     eng.close()
     clocks = cs.summary()
@@ -243,7 +247,7 @@ def run_ours(args, rank, world):
         c_eng.step(0)
         torch.cuda.synchronize()
         cst, cen = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as ccs:
+        with ClockSampler(torch.cuda.current_device()) as ccs:
             cst.record()
             for it in range(1, c_iters + 1):
                 c_eng.step(it)
@@ -274,6 +278,8 @@ def run_ours(args, rank, world):
     if os.path.exists(tp):
         with open(tp) as fh:
             traffic = json.load(fh).get("pair_screen_kernel_chk_c2_bytes")
+        if traffic is not None and world > 1:  # this rank's shard of the c2 rows
+            traffic = int(traffic * (hi - lo) / N_ROWS)
     # e2e: public API with host buffers (H2D of X and D2H of labels inside)
     e2e = None
     if world == 1:

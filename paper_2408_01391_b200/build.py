@@ -28,6 +28,8 @@ SOURCES = {
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
+if os.environ.get("FTK_PROBE"):  # role-timing probes in the CTA-pair kernel (diagnostics)
+    COMMON.append("-DFTK_PAIR_PROBE")
 
 
 def nvcc():
