@@ -90,8 +90,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * PR_B_HALF);  // [2][2][128]
     double *psum = reinterpret_cast<double *>(part + 2 * 2 * PR_BM);           // [2][2][128]
     float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
-    float4 *stg = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // [4 refine warps][32 rows][8]
-    float4 *css = stg + 4 * 32 * 8;                             // ABFT checksum centroid [nkb * 8]
+    float4 *css = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // ABFT checksum centroid [nkb * 8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
     uint64_t *full = bars, *empty = bars + S;
     uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
@@ -389,40 +388,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     ee = ri.y;
                     amax = ri.z;
                 }
-                // centroid rows of the warp's 32 winners, one 32-float k-block at
-                // a time: loaded cooperatively (a warp instruction covers 4 rows,
-                // 8 lanes x 16 B each -> 4 L1 wavefronts instead of 32 for
-                // per-thread row gathers), staged in shared memory (XOR-swizzled
-                // by row) and read back by the owning thread; the next k-block is
-                // held in registers while the current one is consumed
-                float4 *wst = stg + (warp - W_REFINE0) * (32 * 8);
-                float4 nxt[8];
-                auto gather = [&](int kb) {
+                // centroid row of this thread's winner in 32-float k-blocks,
+                // the next k-block in flight (two statically indexed register
+                // buffers); the X row comes from the resident tile
+                const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(active ? j : 0) * P.d);
+                auto load_c = [&](float4 (&cv)[8], int kb) {
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int rr = i * 4 + (lane >> 3), q = lane & 7;
-                        const int jr = __shfl_sync(0xffffffffu, j, rr);
-                        const bool okr = __shfl_sync(0xffffffffu, int(active), rr) != 0;
-                        const int f = kb * PR_KB + 4 * q;
-                        nxt[i] = (okr && f < P.d)
-                                     ? __ldg(reinterpret_cast<const float4 *>(P.y + int64_t(jr) * P.d + f))
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                    }
+                    for (int q = 0; q < 8; ++q)
+                        cv[q] = (active && kb * PR_KB + 4 * q < P.d) ? __ldg(cj4 + kb * 8 + q)
+                                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
                 };
-                auto stash = [&]() {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const int rr = i * 4 + (lane >> 3), q = lane & 7;
-                        wst[rr * 8 + (q ^ (rr & 7))] = nxt[i];
-                    }
-                };
-                PROBE_T(lp0_);
-                gather(0);
-                for (int kb = 0; kb < nkb; ++kb) {
-                    __syncwarp();
-                    stash();
-                    __syncwarp();
-                    if (kb + 1 < nkb) gather(kb + 1);
+                auto consume = [&](const float4 (&cv)[8], int kb) {
                     const int k0 = kb * PR_KB;
                     const unsigned char *rowp = sAt + uint32_t(kb) * PR_A_KB;
 #pragma unroll
@@ -430,7 +406,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         if (k0 + 4 * q < P.d) {
                             const float4 xv =
                                 *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
-                            const float4 c4 = wst[lane * 8 + (q ^ (lane & 7))];
+                            const float4 c4 = cv[q];
                             acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
                             acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
                             acc = __fadd_rn(acc, __fmul_rn(xv.z, c4.z));
@@ -460,6 +436,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                 rr[3] = fmaf(tf32_trunc(xv.w), sv.w, rr[3]);
                             }
                         }
+                    }
+                };
+                PROBE_T(lp0_);
+                float4 cA[8], cB[8];
+                load_c(cA, 0);
+                for (int kb = 0; kb < nkb; kb += 2) {
+                    if (kb + 1 < nkb) load_c(cB, kb + 1);
+                    consume(cA, kb);
+                    if (kb + 1 < nkb) {
+                        if (kb + 2 < nkb) load_c(cA, kb + 2);
+                        consume(cB, kb + 1);
                     }
                 }
                 PROBE_T(lp1_);
@@ -542,7 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 size_t pair_smem_bytes(int nkb, int abufs, int stages) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * PR_B_HALF +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
-           4 * 32 * 8 * sizeof(float4) + 8 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
+           8 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
 }
 
 int pair_plan(int64_t d, int *abufs, int *stages) {
