@@ -74,7 +74,7 @@ int tc_supported(int dtype, int64_t m, int64_t k, int64_t d);
 int dscreen_run(ftk_ctx *, const double *, const double *, const double *, int64_t, int64_t,
                 int64_t, int32_t *, double *, const TcFt *, cudaStream_t);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
-float tc_last_pass1_ms();
+float tc_last_pass1_ms(ftk_ctx *);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
 
@@ -103,6 +103,8 @@ void ftk_ctx_destroy(ftk_ctx *ctx) {
     cudaDeviceSynchronize();
     for (auto &s : ctx->slots)
         if (s.ptr) cudaFree(s.ptr);
+    for (auto &e : ctx->time_ev)
+        if (e) cudaEventDestroy(e);
     delete ctx;
 }
 
@@ -268,7 +270,7 @@ void ftk_add_launches(int64_t n) { count_launch(int(n)); }
 
 int ftk_tc_last_kernel_ms(ftk_ctx *ctx, float *ms) {
     if (!ctx || !ms) { set_error("bad ctx"); return FTK_ERR_ARG; }
-    *ms = tc_last_pass1_ms();
+    *ms = tc_last_pass1_ms(ctx);
     return FTK_OK;
 }
 

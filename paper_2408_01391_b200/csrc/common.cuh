@@ -49,6 +49,11 @@ struct ftk_ctx {
     const void *rows_x = nullptr;
     int64_t rows_m = 0, rows_d = 0;
     const float *rows_info = nullptr;  // m x 4: |x|^2, |x - tf32(x)|^2, max|x|, 0
+    // diagnostics of the last screened assignment on this context
+    unsigned last_fb[3] = {0, 0, 0};              // pass-1 uncertified, exact rows, ABFT flags
+    int last_path = 0;                            // pass-1 kernel: 0 single-CTA, 1 CTA pair
+    cudaEvent_t time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
+    const unsigned *stat_dev[3] = {nullptr, nullptr, nullptr};  // counters still on the device
 };
 
 namespace ftk {

@@ -735,10 +735,6 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 
-static unsigned g_last_fb[3] = {0, 0, 0};
-static int g_last_path = 0;  // pass-1 kernel of the last call: 0 single-CTA, 1 CTA pair
-static cudaEvent_t g_time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
-static const unsigned *g_stat_dev[3] = {nullptr, nullptr, nullptr};  // lazily read counters
 
   // pass-1 / pass-2 uncertified, TC ABFT flags
 
@@ -917,11 +913,11 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                 cudaMemsetAsync(dclk, 0, 10 * sizeof(long long), st);
                 Q.clk = dclk;
             }
-            static cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // pass-1 kernel timing
-            if (!ev0) {
-                cudaEventCreate(&ev0);
-                cudaEventCreate(&ev1);
+            if (!ctx->time_ev[0]) {  // pass-1 kernel timing
+                cudaEventCreate(&ctx->time_ev[0]);
+                cudaEventCreate(&ctx->time_ev[1]);
             }
+            cudaEvent_t ev0 = ctx->time_ev[0], ev1 = ctx->time_ev[1];
             cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
             cudaStreamIsCapturing(st, &cap);
             const bool timed = cap == cudaStreamCaptureStatusNone;  // no timing inside graphs
@@ -929,10 +925,8 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             rc = pair_screen_launch(mx, mc128, Q, ft != nullptr, st);
             if (timed) {
                 cudaEventRecord(ev1, st);
-                g_time_ev[0] = ev0;
-                g_time_ev[1] = ev1;
             }
-            g_last_path = 1;
+            ctx->last_path = 1;
             if (Q.clk) {
                 long long h[10];
                 cudaMemcpyAsync(h, Q.clk, sizeof(h), cudaMemcpyDeviceToHost, st);
@@ -946,10 +940,10 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             }
         } else {
             rc = screen<false>(bn, P, mx, mx, mc, mc, st);
-            g_last_path = 0;
+            ctx->last_path = 0;
         }
         if (rc) return rc;
-        if (g_last_path == 1) {
+        if (ctx->last_path == 1) {
             // ---------------- pass 2, device-driven (no host synchronisation):
             // the rows pass 1 left uncertified (device count) are gathered and
             // re-screened by the CTA-pair kernel in COLLECT mode; every
@@ -989,9 +983,9 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                                           rows1, cnt, cap_rows, out_idx, outv, rows2, ccount + 1, st)))
                 return rc;
             if ((rc = exact_rows_run(xf, yf, ynf, k, d, rows2, ccount + 1, out_idx, outv, st))) return rc;
-            g_stat_dev[0] = cnt;          // read lazily by tc_last_fallback
-            g_stat_dev[1] = ccount + 1;
-            g_stat_dev[2] = ft ? cnt + 2 : nullptr;
+            ctx->stat_dev[0] = cnt;          // read lazily by tc_last_fallback
+            ctx->stat_dev[1] = ccount + 1;
+            ctx->stat_dev[2] = ft ? cnt + 2 : nullptr;
             if (ft && ft->inj && ft->inj->n > 0)
                 return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
             return FTK_OK;
@@ -1000,9 +994,9 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         FTK_CUDA(cudaStreamSynchronize(st));
         pass2_rows = rows1;
     }
-    g_stat_dev[0] = g_stat_dev[1] = g_stat_dev[2] = nullptr;
-    g_last_fb[0] = n1;
-    g_last_fb[1] = 0;
+    ctx->stat_dev[0] = ctx->stat_dev[1] = ctx->stat_dev[2] = nullptr;
+    ctx->last_fb[0] = n1;
+    ctx->last_fb[1] = 0;
     if (n1 > 0) {
         // ---------------- pass 2: 3xTF32 over the gathered uncertified rows
         float *g = static_cast<float *>(scratch(ctx, SLOT_TC_A, sizeof(float) * 2 * size_t(n1) * d + 64, st));
@@ -1056,7 +1050,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             FTK_CUDA(cudaMemcpyAsync(&n2, cnt2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
             FTK_CUDA(cudaStreamSynchronize(st));
         }
-        g_last_fb[1] = n2;
+        ctx->last_fb[1] = n2;
         if (n2 > 0) {
             // ---------------- exact resolution of the remaining ties (tiled SIMT kernel)
             gather_rows_kernel<<<148 * 4, 256, 0, st>>>(xf, d, rows2, cnt2, g, nullptr);
@@ -1075,7 +1069,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         unsigned nab = 0;
         FTK_CUDA(cudaMemcpyAsync(&nab, cnt + 2, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
         FTK_CUDA(cudaStreamSynchronize(st));
-        g_last_fb[2] = nab;
+        ctx->last_fb[2] = nab;
         if (ft->inj && ft->inj->n > 0)
             return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
     }
@@ -1095,26 +1089,26 @@ template int emulate_injected_blocks<double>(ftk_ctx *, const double *, const do
                                              const TcFt &, int32_t *, double *, cudaStream_t);
 
 // Device time of the last CTA-pair pass-1 launch (ms), -1 if none.
-float tc_last_pass1_ms() {
-    if (!g_time_ev[0] || g_last_path != 1) return -1.0f;
+float tc_last_pass1_ms(ftk_ctx *ctx) {
+    if (!ctx->time_ev[0] || ctx->last_path != 1) return -1.0f;
     float ms = -1.0f;
-    if (cudaEventSynchronize(g_time_ev[1]) != cudaSuccess) return -1.0f;
-    cudaEventElapsedTime(&ms, g_time_ev[0], g_time_ev[1]);
+    if (cudaEventSynchronize(ctx->time_ev[1]) != cudaSuccess) return -1.0f;
+    cudaEventElapsedTime(&ms, ctx->time_ev[0], ctx->time_ev[1]);
     return ms;
 }
 
-int tc_last_fallback(ftk_ctx *, unsigned *out, cudaStream_t st) {
-    if (g_stat_dev[0]) {  // device-driven pass 2: counters still on the device
+int tc_last_fallback(ftk_ctx *ctx, unsigned *out, cudaStream_t st) {
+    if (ctx->stat_dev[0]) {  // device-driven pass 2: counters still on the device
         FTK_CUDA(cudaStreamSynchronize(st));
         for (int q = 0; q < 3; ++q) {
-            g_last_fb[q] = 0;
-            if (g_stat_dev[q])
-                FTK_CUDA(cudaMemcpy(&g_last_fb[q], g_stat_dev[q], sizeof(unsigned), cudaMemcpyDeviceToHost));
+            ctx->last_fb[q] = 0;
+            if (ctx->stat_dev[q])
+                FTK_CUDA(cudaMemcpy(&ctx->last_fb[q], ctx->stat_dev[q], sizeof(unsigned), cudaMemcpyDeviceToHost));
         }
     }
-    out[0] = g_last_fb[0];
-    out[1] = g_last_fb[1];
-    out[2] = g_last_fb[2];
+    out[0] = ctx->last_fb[0];
+    out[1] = ctx->last_fb[1];
+    out[2] = ctx->last_fb[2];
     return FTK_OK;
 }
 
