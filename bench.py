@@ -15,6 +15,7 @@ bounded sample of the same workload and reports the same metric.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -42,7 +43,9 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (clocks + throttle reasons)."""
+    """Clock + throttle-reason sampling DURING the timed region, in-process
+    through NVML (a sampling thread that forked nvidia-smi every 50 ms stalled
+    the launching thread for tens of ms); nvidia-smi only if NVML is absent."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -53,18 +56,45 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
+        self._nv = None
+        try:
+            import pynvml as nv
+            import torch
+
+            nv.nvmlInit()
+            pr = torch.cuda.get_device_properties(index)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            try:
+                self._h = nv.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            except Exception:
+                self._h = nv.nvmlDeviceGetHandleByIndex(index)
+            self._nv = nv
+        except Exception:
+            self._nv = None
+
+    def _sample_nvml(self):
+        nv, h = self._nv, self._h
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        return [str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([v.strip() for v in out.split(",")])
+                if self._nv is not None:
+                    self.rows.append(self._sample_nvml())
+                else:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                          "--query-gpu=" + self.Q, "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout.strip()
+                    if out:
+                        self.rows.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.05)
+            self._stop.wait(0.01 if self._nv is not None else 0.05)
 
     def __enter__(self):
         self._t.start()
@@ -84,7 +114,8 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4)
                           if len(r) > 2 + i and r[2 + i].lower().startswith("active")})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(sm),
+                "source": "nvml" if self._nv is not None else "nvidia-smi"}
 
 
 def make_data(seed=0):
@@ -191,7 +222,11 @@ def run_ours(args, rank, world):
         return LloydEngine(x_t, c0, K, np.float32, cfg, ft_mode, thr, 64,
                            gemm_hook=hook or P.FaultHook(), dist=comm, graph=True)
 
+    step_stats = []  # per-step device times of each timed run (min/median/max)
+
     def time_steps(eng, steps, warmup, sampler=None):
+        gc.collect()
+        gc.disable()  # a cyclic-GC pass in the timed region stalls the launching thread
         for it in range(warmup):
             eng.step(it)
         # one eager (non-graph) step: phase timings and CUDA events around the
@@ -201,20 +236,23 @@ def run_ours(args, rank, world):
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
-        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         l0 = _native.launch_count()
-        st.record()
-        for it in range(warmup + 1, warmup + 1 + steps):
+        evs[0].record()
+        for i, it in enumerate(range(warmup + 1, warmup + 1 + steps)):
             eng.step(it)
-        en.record()
+            evs[i + 1].record()
         torch.cuda.synchronize()
         launches = _native.launch_count() - l0
-        ms = st.elapsed_time(en)
+        ms = evs[0].elapsed_time(evs[-1])
+        per = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(steps))
+        step_stats.append({"p50": per[len(per) // 2], "max": per[-1], "min": per[0]})
         if world > 1:
             t = torch.tensor([ms], device="cuda")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms = float(t.item())
         kern = [v for v in k_ms if v > 0]
+        gc.enable()
         return ms / steps, statistics.median(a_ms), launches, (statistics.mean(kern) if kern else None)
 
     # FT-off reference timing and the per-iteration time used to size the campaign
@@ -245,7 +283,10 @@ def run_ours(args, rank, world):
         c_hook = ScheduledFaultHook(c_sched)
         c_eng = engine("abft", c_hook)
         c_eng.step(0)
+        c_eng.warm_graphs(1)  # capture outside the timed region
         torch.cuda.synchronize()
+        gc.collect()
+        gc.disable()
         cst, cen = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with ClockSampler(torch.cuda.current_device()) as ccs:
             cst.record()
@@ -253,6 +294,7 @@ def run_ours(args, rank, world):
                 c_eng.step(it)
             cen.record()
             torch.cuda.synchronize()
+        gc.enable()
         c_clocks = ccs.summary()
         c_ms = cst.elapsed_time(cen)
         c_eng.close()
@@ -324,6 +366,7 @@ def run_ours(args, rank, world):
                    "detections": rep.detections, "corrections": rep.corrections,
                    "uncorrectable": rep.uncorrectable, "p_tile": p},
         "ft_campaign": campaign,
+        "step_ms": {"ft_off": step_stats[0], "abft": step_stats[1]},
         "gpu_launches": launches,
         "clocks": clocks,
         "cpu_baseline": cpu,

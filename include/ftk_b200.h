@@ -57,6 +57,11 @@ typedef struct ftk_injection {
     int64_t *applied;  /* out: 1 when the flip landed on a live cell     */
     double *before;    /* out: accumulator value before the flip (f64)   */
     double *after;     /* out: after                                     */
+    /* optional: live count on the device. When set, n is the capacity of the
+     * arrays and the launches never read the count on the host, so a checked
+     * assignment with scheduled flips can be captured in a CUDA graph and
+     * replayed with a new schedule copied into the same arrays. */
+    const int64_t *n_dev;
 } ftk_injection;
 
 /* Detection-event ring (abft.py:281-294): rec is cap x 7 int64
@@ -93,6 +98,9 @@ int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info
  * modified while registered; pass x = NULL to unregister.  The reference has
  * no counterpart (its kernels recompute nothing across calls). */
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info);
+/* Number of scratch (re)allocations on this context so far: a CUDA graph
+ * captured from this context's launches is stale once it changes. */
+int64_t ftk_ctx_generation(ftk_ctx *ctx);
 
 /* k-means++ seeding step (kmeans.py:95-103): d2[i] = sum_f (x[i,f] - x[pick,f])^2 in
  * float64 with numpy's pairwise association (a single leaf: d <= 128), then

@@ -118,6 +118,72 @@ class DevInjection:
         self.host[7][:] = ba[1]
 
 
+class StaticInjection:
+    """Fixed-address injection arrays with the live count on the device
+    (ftk_injection.n_dev), for CUDA-graph replay of injected passes: `load`
+    stages one pass's schedule (pinned host -> device, stream-ordered before
+    the replay), the captured graph copies applied/before/after back into
+    pinned host memory, `finish` hands them to the hook after the step's
+    synchronisation."""
+
+    def __init__(self, cap):
+        t = _torch()
+        self.cap = int(cap)
+        self.idx = t.zeros((5, self.cap), dtype=t.int64, device=device())
+        self.n_dev = t.zeros(1, dtype=t.int64, device=device())
+        self.applied = t.zeros(self.cap, dtype=t.int64, device=device())
+        self.ba = t.zeros((2, self.cap), dtype=t.float64, device=device())
+        self.idx_h = t.zeros((5, self.cap), dtype=t.int64).pin_memory()
+        self.n_h = t.zeros(1, dtype=t.int64).pin_memory()
+        self.applied_h = t.zeros(self.cap, dtype=t.int64).pin_memory()
+        self.ba_h = t.zeros((2, self.cap), dtype=t.float64).pin_memory()
+        base = self.idx.data_ptr()
+        self.struct = N.Injection(self.cap, *(base + 8 * self.cap * c for c in range(5)),
+                                  self.applied.data_ptr(), self.ba[0].data_ptr(),
+                                  self.ba[1].data_ptr(), self.n_dev.data_ptr())
+        self.n = 0
+        self.host = None
+
+    def ref(self):
+        import ctypes
+
+        return ctypes.byref(self.struct)
+
+    def load(self, arrs):
+        """Stage the pass's schedule (None: no flips); False if over capacity."""
+        n = 0 if arrs is None else len(arrs[0])
+        if n > self.cap:
+            return False
+        self.n, self.host = n, arrs
+        if n:
+            self.idx_h[:, :n] = torch_from(np.stack([np.asarray(v, np.int64) for v in arrs[:5]]))
+        self.n_h[0] = n
+        self.idx.copy_(self.idx_h, non_blocking=True)
+        self.n_dev.copy_(self.n_h, non_blocking=True)
+        return True
+
+    def copy_back(self):
+        """Captured with the pass: device outputs -> pinned host."""
+        self.applied_h.copy_(self.applied, non_blocking=True)
+        self.ba_h.copy_(self.ba, non_blocking=True)
+
+    def finish(self):
+        if self.n == 0 or self.host is None:
+            return
+        n = self.n
+        self.host[5][:] = self.applied_h.numpy()[:n]
+        self.host[6][:] = self.ba_h.numpy()[0, :n]
+        self.host[7][:] = self.ba_h.numpy()[1, :n]
+
+
+def torch_from(a):
+    return _torch().from_numpy(np.ascontiguousarray(a))
+
+
+def ctx_generation():
+    return int(N.load().ftk_ctx_generation(ctx()))
+
+
 def injection_for(hook, iteration, dtype):
     if hook is None:
         return None
@@ -130,13 +196,30 @@ def injection_for(hook, iteration, dtype):
 class DevEvents:
     """Detection-event ring on the device (abft.py:281-294)."""
 
-    def __init__(self, cap):
+    def __init__(self, cap, storage=None):
         t = _torch()
         self.cap = int(cap)
-        self.rec = t.zeros((max(self.cap, 1), 7), dtype=t.int64, device=device())
-        self.delta = t.zeros(max(self.cap, 1), dtype=t.float64, device=device())
+        self.storage = max(self.cap, int(storage or 0), 1)
+        self.gen = 0  # bumped when the buffers move (captured CUDA graphs go stale)
+        self.rec = t.zeros((self.storage, 7), dtype=t.int64, device=device())
+        self.delta = t.zeros(self.storage, dtype=t.float64, device=device())
         self.count = t.zeros(1, dtype=t.int64, device=device())
         self.struct = N.Events(self.cap, self.rec.data_ptr(), self.delta.data_ptr(),
+                               self.count.data_ptr())
+
+    def set_cap(self, cap):
+        """Logical capacity of the next launch (the overflow rule of
+        abft.py:315-316); the buffers only move when `cap` exceeds storage."""
+        cap = int(cap)
+        if cap > self.storage:
+            t = _torch()
+            self.storage = max(cap, 2 * self.storage)
+            self.rec = t.zeros((self.storage, 7), dtype=t.int64, device=device())
+            self.delta = t.zeros(self.storage, dtype=t.float64, device=device())
+            self.count = t.zeros(1, dtype=t.int64, device=device())
+            self.gen += 1
+        self.cap = cap
+        self.struct = N.Events(cap, self.rec.data_ptr(), self.delta.data_ptr(),
                                self.count.data_ptr())
 
     def ref(self):
@@ -147,16 +230,18 @@ class DevEvents:
     def reset(self):
         self.count.zero_()
 
-    def read(self, n=None):
+    def read(self, n=None, cap=None):
         """-> (overflowed, [(rec7..., delta)]); `n` = the count if the caller
-        already copied it to the host (saves a synchronisation)."""
+        already copied it to the host (saves a synchronisation), `cap` the
+        logical capacity when the launch ran with a larger one (graphs)."""
         n = int(self.count.item()) if n is None else int(n)
-        m = min(n, self.cap)
+        cap = self.cap if cap is None else min(int(cap), self.storage)
+        m = min(n, cap)
         if m == 0:
-            return n > self.cap, []
+            return n > cap, []
         rec = to_host(self.rec[:m])
         delta = to_host(self.delta[:m])
-        return n > self.cap, [(tuple(int(v) for v in rec[i]), float(delta[i])) for i in range(m)]
+        return n > cap, [(tuple(int(v) for v in rec[i]), float(delta[i])) for i in range(m)]
 
 
 # ------------------------------------------------------------ kernels ----

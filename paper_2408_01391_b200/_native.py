@@ -12,7 +12,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libftkb200.so")
+LIB_PATH = os.environ.get("FTK_LIB_PATH") or os.path.join(HERE, "_lib", "libftkb200.so")
 
 FTK_OK, FTK_OVERFLOW = 0, 1
 FTK_F32, FTK_F64 = 0, 1
@@ -23,7 +23,7 @@ _i64, _i32, _p, _dbl, _int = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ct
 
 class Injection(ctypes.Structure):
     _fields_ = [("n", _i64), ("bi", _p), ("bj", _p), ("ei", _p), ("ej", _p), ("bit", _p),
-                ("applied", _p), ("before", _p), ("after", _p)]
+                ("applied", _p), ("before", _p), ("after", _p), ("n_dev", _p)]
 
 
 class Events(ctypes.Structure):
@@ -42,6 +42,7 @@ PROTOTYPES = {
     "ftk_row_info": (_int, [_p, _p, _i64, _i64, _p, _p]),
     "ftk_kpp_d2": (_int, [_p, _int, _p, _i64, _i64, _i64, _int, _p, _p]),
     "ftk_ctx_set_rows": (_int, [_p, _p, _i64, _i64, _p]),
+    "ftk_ctx_generation": (_i64, [_p]),
     "ftk_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p,
                           _p, _p]),
     "ftk_checked_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64,

@@ -30,6 +30,12 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-
           "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 if os.environ.get("FTK_PROBE"):  # role-timing probes in the CTA-pair kernel (diagnostics)
     COMMON.append("-DFTK_PAIR_PROBE")
+# A/B experiments: FTK_VARIANT=name FTK_DEFS="-DX=1 ..." builds _lib/var_<name>/libftkb200.so,
+# loaded with FTK_LIB_PATH=<that path>. The default build is untouched.
+if os.environ.get("FTK_VARIANT"):
+    LIBDIR = os.path.join(LIBDIR, "var_" + os.environ["FTK_VARIANT"])
+    LIB = os.path.join(LIBDIR, "libftkb200.so")
+    COMMON += os.environ.get("FTK_DEFS", "").split()
 
 
 def nvcc():

@@ -37,6 +37,7 @@ void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st) {
         return nullptr;
     }
     s.bytes = want;
+    ++ctx->generation;
     return s.ptr;
 }
 
@@ -118,6 +119,8 @@ int ftk_kpp_d2(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int
     if (!ctx || !dtype_ok(dtype) || pick < 0 || pick >= m) { set_error("bad ctx/dtype/pick"); return FTK_ERR_ARG; }
     return kpp_d2_run(dtype, x, m, d, pick, first, d2, as_stream(stream));
 }
+
+int64_t ftk_ctx_generation(ftk_ctx *ctx) { return ctx ? ctx->generation : -1; }
 
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info) {
     if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }

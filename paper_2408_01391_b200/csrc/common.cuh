@@ -54,6 +54,7 @@ struct ftk_ctx {
     int last_path = 0;                            // pass-1 kernel: 0 single-CTA, 1 CTA pair
     cudaEvent_t time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
     const unsigned *stat_dev[3] = {nullptr, nullptr, nullptr};  // counters still on the device
+    int64_t generation = 0;  // scratch (re)allocations: captured graphs go stale
 };
 
 namespace ftk {

@@ -36,6 +36,8 @@ struct ExactParams {
     const double *bmax;  // per logical column block: max |y| over its rows
     // injection (faults.py:261-277 arrays, device)
     int64_t n_inj;
+    const int64_t *n_inj_dev;  // live count on the device (n_inj = capacity), or null
+    const int64_t *m_dev;      // live rows on the device (m = capacity), or null
     const int64_t *ibi, *ibj, *iei, *iej, *ibit;
     int64_t *iapplied;
     double *ibefore, *iafter;
@@ -294,7 +296,10 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
     const bool real_row_group = r * TM < bm;
     const int64_t bi = blockIdx.x;
     const int64_t i0 = bi * bm;
-    const int mi = int(bm < P.m - i0 ? bm : P.m - i0);
+    const int64_t m_all = P.m_dev ? *P.m_dev : P.m;
+    if (i0 >= m_all) return;  // device row count: whole CTA idle (before any barrier)
+    const int mi = int(bm < m_all - i0 ? bm : m_all - i0);
+    const int64_t n_inj = P.n_inj_dev ? (*P.n_inj_dev < P.n_inj ? *P.n_inj_dev : P.n_inj) : P.n_inj;
     const int64_t nbj = (P.k + bn - 1) / bn;
     const int64_t nbk = (kdim + P.bk - 1) / P.bk;
 
@@ -378,13 +383,13 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
 
         // scheduled flips on the accumulator after the last k-interval
         // (_kernels.py:462-474 / 568-583)
-        if (P.n_inj > 0 && live_col) {
-            for (int64_t q = 0; q < P.n_inj; ++q) {
+        if (n_inj > 0 && live_col) {
+            for (int64_t q = 0; q < n_inj; ++q) {
                 if (P.ibj[q] != bj) continue;
                 int64_t ei = P.iei[q], ej = P.iej[q];
                 // logical tile (bi, bj) cell (ei, ej) -> global row; live cells only
                 int64_t grow = P.ibi[q] * lbm + ei;
-                if (ej != jl || ej >= nj || ei >= lbm || grow >= P.m) continue;
+                if (ej != jl || ej >= nj || ei >= lbm || grow >= m_all) continue;
                 int64_t lrow = grow - i0;  // row within this CTA
                 if (lrow < 0 || lrow >= mi) continue;
 #pragma unroll
@@ -626,10 +631,11 @@ static int launch_exact(ExactParams P, cudaStream_t st) {
     return FTK_ERR_ARG;
 }
 
-int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn, int64_t m,
-              int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk, int32_t *out_idx,
-              void *out_val, void *out_mat, bool checked, double delta_rel, double abs_tol,
-              int64_t iteration, const ftk_injection *inj, ftk_events *ev, cudaStream_t st) {
+int exact_run_m(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn, int64_t m,
+                int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk, int32_t *out_idx,
+                void *out_val, void *out_mat, bool checked, double delta_rel, double abs_tol,
+                int64_t iteration, const ftk_injection *inj, ftk_events *ev, cudaStream_t st,
+                const int64_t *m_dev) {
     if (m <= 0) return FTK_OK;
     if (bm < 1 || bn < 1 || bk < 1 || d < 1) {
         set_error("bad tile/shape");
@@ -644,9 +650,11 @@ int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void 
     while (pb < live) pb *= 2;
     P.pb = int(pb);
     P.out_idx = out_idx; P.out_val = out_val; P.out_mat = out_mat;
+    P.m_dev = m_dev;
     P.delta_rel = delta_rel; P.abs_tol = abs_tol; P.iteration = iteration;
     if (inj && inj->n > 0) {
         P.n_inj = inj->n;
+        P.n_inj_dev = inj->n_dev;
         P.ibi = inj->bi; P.ibj = inj->bj; P.iei = inj->ei; P.iej = inj->ej; P.ibit = inj->bit;
         P.iapplied = inj->applied; P.ibefore = inj->before; P.iafter = inj->after;
     }
@@ -674,6 +682,14 @@ int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void 
     if (dtype == FTK_F32)
         return checked ? launch_exact<float, true>(P, st) : launch_exact<float, false>(P, st);
     return checked ? launch_exact<double, true>(P, st) : launch_exact<double, false>(P, st);
+}
+
+int exact_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn, int64_t m,
+              int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk, int32_t *out_idx,
+              void *out_val, void *out_mat, bool checked, double delta_rel, double abs_tol,
+              int64_t iteration, const ftk_injection *inj, ftk_events *ev, cudaStream_t st) {
+    return exact_run_m(ctx, dtype, x, y, yn, m, k, d, bm, bn, bk, out_idx, out_val, out_mat, checked,
+                       delta_rel, abs_tol, iteration, inj, ev, st, nullptr);
 }
 
 int row_sq_norms_run(int dtype, const void *x, int64_t m, int64_t n, void *out, cudaStream_t st) {

@@ -538,7 +538,8 @@ __global__ void tile_csum_kernel(const float *y, int64_t k, int64_t d, int nkb, 
 __global__ void inj_rows_kernel(const float *x, const float *y, int64_t m, int64_t k, int64_t d,
                                 int64_t bm, int64_t bn, ftk_injection inj, int32_t *inj_col,
                                 float *inj_before, float *inj_after) {
-    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < inj.n;
+    const int64_t n = inj.n_dev ? (*inj.n_dev < inj.n ? *inj.n_dev : inj.n) : inj.n;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
          q += int64_t(gridDim.x) * blockDim.x) {
         const int64_t ei = inj.ei[q], ej = inj.ej[q];
         const int64_t row = inj.bi[q] * bm + ei, col = inj.bj[q] * bn + ej;
@@ -570,11 +571,63 @@ __global__ void remap_inj_kernel(const int64_t *bi, int64_t n, const int64_t *bl
     }
 }
 
+// Device-count injections (ftk_injection.n_dev): the sorted distinct logical
+// row blocks that carry a flip, each flip's compact block index, and
+// nb_rows = {blocks, compact rows} -- what emulate_injected_blocks derives on
+// the host, computed without a host round trip.  One CTA, O(n^2) over the
+// (small) schedule of one pass, dynamic smem 9 bytes per capacity entry.
+// Also clears the applied/before/after outputs.
+__global__ void inj_blocks_kernel(ftk_injection inj, int64_t nbi, int64_t m, int64_t bm,
+                                  int64_t *blocks, int64_t *bi_out, int64_t *nb_rows) {
+    extern __shared__ int64_t sbi[];
+    __shared__ int s_nb;
+    const int64_t n = *inj.n_dev < inj.n ? *inj.n_dev : inj.n;
+    unsigned char *first = reinterpret_cast<unsigned char *>(sbi + inj.n);
+    if (threadIdx.x == 0) s_nb = 0;
+    for (int64_t q = threadIdx.x; q < inj.n; q += blockDim.x) {
+        const int64_t v = q < n ? inj.bi[q] : -1;
+        sbi[q] = (v >= 0 && v < nbi) ? v : -1;
+        inj.applied[q] = 0;
+        inj.before[q] = 0.0;
+        inj.after[q] = 0.0;
+    }
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
+        bool f = sbi[q] >= 0;
+        for (int64_t p = 0; p < q && f; ++p) f = sbi[p] != sbi[q];
+        first[q] = f;
+    }
+    __syncthreads();
+    for (int64_t q = threadIdx.x; q < n; q += blockDim.x) {
+        const int64_t v = sbi[q];
+        if (v < 0) {
+            bi_out[q] = int64_t(1) << 40;  // never applies
+            continue;
+        }
+        int64_t rank = 0;  // distinct valid blocks below v
+        for (int64_t p = 0; p < n; ++p) rank += (first[p] && sbi[p] < v);
+        bi_out[q] = rank;
+        if (first[q]) {
+            blocks[rank] = v;
+            atomicAdd(&s_nb, 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int64_t nb = s_nb;
+        nb_rows[0] = nb;
+        // the (possibly partial) last row block sorts last in the compact set
+        nb_rows[1] = nb == 0 ? 0
+                     : (blocks[nb - 1] == nbi - 1 ? (nb - 1) * bm + (m - (nbi - 1) * bm) : nb * bm);
+    }
+}
+
 // gather rows [blocks[b]*bm, +bm) (clipped to m) into a compact buffer
 template <typename T>
 __global__ void gather_blocks_kernel(const T *x, int64_t m, int64_t d, int64_t bm,
-                                     const int64_t *blocks, int64_t nb, T *g) {
-    const int64_t n = nb * bm * d;
+                                     const int64_t *blocks, int64_t nb, T *g,
+                                     const int64_t *nb_dev = nullptr) {
+    const int64_t n = (nb_dev ? *nb_dev : nb) * bm * d;
     for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
          e += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = e / d, f = e % d;
@@ -586,7 +639,8 @@ __global__ void gather_blocks_kernel(const T *x, int64_t m, int64_t d, int64_t b
 template <typename T>
 __global__ void scatter_blocks_kernel(const int32_t *idx, const T *val, int64_t m, int64_t bm,
                                       const int64_t *blocks, int64_t nb, int32_t *out_idx,
-                                      T *out_val) {
+                                      T *out_val, const int64_t *nb_dev = nullptr) {
+    if (nb_dev) nb = *nb_dev;
     for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nb * bm;
          r += int64_t(gridDim.x) * blockDim.x) {
         const int64_t row = blocks[r / bm] * bm + r % bm;
@@ -759,11 +813,61 @@ static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t 
 // that carry an injection are recomputed by the exact checked kernel (the
 // reference's detection / location / correction / events, bit for bit) and
 // overwrite the TC results for those rows.
+int exact_run_m(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t,
+                int64_t, int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double,
+                int64_t, const ftk_injection *, ftk_events *, cudaStream_t, const int64_t *);
+
+// The same with the schedule's count on the device (ftk_injection.n_dev): no
+// host round trip, so the pass stays capturable in a CUDA graph.  Buffers are
+// sized for the capacity inj.n; the kernels read the live block / row counts.
+template <typename T>
+static int emulate_injected_blocks_dev(ftk_ctx *ctx, const T *xf, const T *yf, const T *ynf,
+                                       int64_t m, int64_t k, int64_t d, const TcFt &ft,
+                                       int32_t *out_idx, T *outv, cudaStream_t st) {
+    const ftk_injection &inj = *ft.inj;
+    const int64_t cap = inj.n;
+    if (cap > 4096) {
+        set_error("device-count injection: capacity above 4096 flips per pass");
+        return FTK_ERR_ARG;
+    }
+    const int64_t nbi = (m + ft.bm - 1) / ft.bm;
+    const int64_t nbc = cap < nbi ? cap : nbi;  // at most this many distinct row blocks
+    const size_t need = sizeof(int64_t) * (nbc + cap + 8) +
+                        sizeof(T) * (nbc * ft.bm * d + 2 * nbc * ft.bm) + 256;
+    char *buf = static_cast<char *>(scratch(ctx, SLOT_INJ, need, st));
+    if (!buf) return FTK_ERR_CUDA;
+    int64_t *d_blocks = reinterpret_cast<int64_t *>(buf);
+    int64_t *d_bi = d_blocks + nbc;
+    int64_t *nb_rows = d_bi + cap;  // {distinct blocks, compact rows}
+    T *g = reinterpret_cast<T *>(nb_rows + 8);
+    T *gv = g + nbc * ft.bm * d;
+    int32_t *gi = reinterpret_cast<int32_t *>(gv + nbc * ft.bm);
+    inj_blocks_kernel<<<1, 256, size_t(cap) * 9 + 16, st>>>(inj, nbi, m, ft.bm, d_blocks, d_bi,
+                                                            nb_rows);
+    FTK_LAUNCHED("inj_blocks_kernel");
+    gather_blocks_kernel<T><<<148, 256, 0, st>>>(xf, m, d, ft.bm, d_blocks, nbc, g, nb_rows);
+    FTK_LAUNCHED("gather_blocks_kernel");
+    ftk_injection rin = inj;
+    rin.bi = d_bi;
+    int rc = exact_run_m(ctx, sizeof(T) == 4 ? FTK_F32 : FTK_F64, g, yf, ynf, nbc * ft.bm, k, d,
+                         ft.bm, ft.bn, ft.bk, gi, gv, nullptr, true, ft.delta_rel, ft.abs_tol,
+                         ft.iteration, &rin, ft.ev, st, nb_rows + 1);
+    if (rc) return rc;
+    remap_events_kernel<<<1, 256, 0, st>>>(ft.ev->rec, ft.ev->count, ft.ev->cap, d_blocks);
+    FTK_LAUNCHED("remap_events_kernel");
+    scatter_blocks_kernel<T><<<148, 256, 0, st>>>(gi, gv, m, ft.bm, d_blocks, nbc, out_idx, outv,
+                                                  nb_rows);
+    FTK_LAUNCHED("scatter_blocks_kernel");
+    return FTK_OK;
+}
+
 template <typename T>
 int emulate_injected_blocks(ftk_ctx *ctx, const T *xf, const T *yf, const T *ynf, int64_t m,
                             int64_t k, int64_t d, const TcFt &ft, int32_t *out_idx, T *outv,
                             cudaStream_t st) {
     const ftk_injection &inj = *ft.inj;
+    if (inj.n_dev)
+        return emulate_injected_blocks_dev<T>(ctx, xf, yf, ynf, m, k, d, ft, out_idx, outv, st);
     std::vector<int64_t> bi(inj.n);
     FTK_CUDA(cudaMemcpyAsync(bi.data(), inj.bi, sizeof(int64_t) * inj.n, cudaMemcpyDeviceToHost, st));
     FTK_CUDA(cudaStreamSynchronize(st));

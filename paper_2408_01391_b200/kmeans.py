@@ -12,6 +12,7 @@ control readback per iteration for the host-side stopping decision
 from __future__ import annotations
 
 import dataclasses
+import gc
 import time
 from dataclasses import dataclass, field
 
@@ -262,14 +263,17 @@ class _DeviceAssign:
         self.threads = threads
         self.md = t.empty(m, dtype=x_t.dtype, device=x_t.device)
         self.labels = [t.empty(m, dtype=t.int32, device=x_t.device) for _ in range(2)]
-        self.events = E.DevEvents(64 * max(1, min(threads, self.nbi))) if self.checked else None
+        mult = max(1, min(threads, self.nbi))
+        # storage for a few hundred injected flips per pass, so eager injected
+        # steps do not move the ring that captured graph replays write into
+        self.events = E.DevEvents(64 * mult, storage=(64 + 256) * mult) if self.checked else None
 
-    def run(self, cent_t, yn_t, hook, iteration, slot):
-        inj = E.injection_for(hook, iteration, self.dtype)
+    def run(self, cent_t, yn_t, hook, iteration, slot, sinj=None):
+        """`sinj`: a StaticInjection (device-count schedule, graph capture)
+        used instead of the hook's arrays for this pass."""
+        inj = sinj if sinj is not None else E.injection_for(hook, iteration, self.dtype)
         if self.checked:
-            cap = ((inj.n if inj else 0) + 64) * max(1, min(self.threads, self.nbi))
-            if cap > self.events.cap:
-                self.events = E.DevEvents(cap)
+            self.events.set_cap(self.ev_cap(inj.cap if sinj is not None else (inj.n if inj else 0)))
             self.events.reset()
         E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=get_variant(), inj=inj,
                      checked=self.checked, delta_rel=self.delta_rel, abs_tol=self.abs_tol,
@@ -277,11 +281,20 @@ class _DeviceAssign:
                      out_val=self.md)
         return inj
 
-    def finish(self, hook, iteration, inj, n_events=None):
-        """Host side of the pass: events -> report, applied flips -> hook."""
+    def ev_cap(self, n_inj):
+        """Event capacity of a pass with n_inj flips: the reference gives
+        every worker n_inj + 64 (abft.py)."""
+        return (n_inj + 64) * max(1, min(self.threads, self.nbi))
+
+    def finish(self, hook, iteration, inj, n_events=None, replayed=False):
+        """Host side of the pass: events -> report, applied flips -> hook.
+        `replayed`: the pass ran from a CUDA graph, whose launch carries the
+        iteration number of its capture; the records get the real one."""
         report = None
         if self.checked:
-            overflow, raw = self.events.read(n_events)
+            overflow, raw = self.events.read(n_events, cap=self.ev_cap(inj.n if inj else 0))
+            if replayed:
+                raw = [((iteration,) + tuple(rec[1:]), d) for rec, d in raw]
             if overflow:
                 raise RuntimeError("detection event buffer overflow; threshold likely "
                                    "miscalibrated")
@@ -339,7 +352,13 @@ class LloydEngine:
             update_hook is NOOP_HOOK and self.dtype == np.float32 and \
             8 <= x_t.shape[1] <= 256 and x_t.shape[1] % 4 == 0 and get_variant() != "exact"
         self.graphs = [None, None]
-        self.graph_kernels = [0, 0]  # library kernels per replay (launch accounting)
+        # injected passes replay their own graphs, the schedule staged into
+        # fixed device arrays (count on the device) before the replay
+        self.sinj = E.StaticInjection(64) if self.use_graph and self.A.checked and \
+            getattr(gemm_hook, "schedule", None) is not None else None
+        self.inj_graphs = [None, None]
+        self.graph_gen = self.A.events.gen if self.A.checked else 0
+        self.ctx_gen = None
         self.cent_buf = [t.empty_like(self.cent), t.empty_like(self.cent)]
         self.cent_buf[0].copy_(self.cent)
         self.cent = self.cent_buf[0]
@@ -348,22 +367,28 @@ class LloydEngine:
         self._pool = None
 
     def _graph_ok(self, it):
-        """Graph replay is used for steps without scheduled flips (those need
-        the hook's host round trip) once both buffer parities are warm."""
+        """Graph replay is used from the second step on: clean steps replay
+        the step graph of their buffer parity, steps with scheduled flips
+        (up to the static capacity) the injected-pass graph."""
         if not self.use_graph or it < 1:
             return False
         if self.gemm_hook is NOOP_HOOK or type(self.gemm_hook) is FaultHook:
             return True  # the no-op hook never injects
         sched = getattr(self.gemm_hook, "schedule", None)
-        return sched is not None and not sched.for_iteration(it)
+        if sched is None:
+            return False
+        n = len(sched.for_iteration(it))
+        return n == 0 or (self.sinj is not None and n <= self.sinj.cap)
 
-    def _device_part(self, it):
+    def _device_part(self, it, sinj=None):
         """Launches of one step with no host synchronisation (graph-capturable):
         assign, inertia, label compare, update sums, finalize into the other
         static centroid buffer, movement, control copies."""
         A = self.A
         yn = E.row_sq_norms_dev(self.cent)
-        A.run(self.cent, yn, NOOP_HOOK, it, self.slot)
+        A.run(self.cent, yn, NOOP_HOOK, it, self.slot, sinj=sinj)
+        if sinj is not None:
+            sinj.copy_back()
         E.sq_dists_dev(A.md, self.xsq, self.sq)
         E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
         E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
@@ -377,33 +402,84 @@ class LloydEngine:
         if A.checked:
             self.evc_host.copy_(A.events.count, non_blocking=True)
 
+    def _capture(self, it):
+        """Capture the step graphs of BOTH buffer parities (captured, not
+        run), so an eager injected step never leaves a capture for later."""
+        t = self.t
+        if self._pool is None:
+            self._pool = t.cuda.graph_pool_handle()
+        if self.sinj is not None and self.inj_graphs[self.slot] is None:
+            # size the injected pass's scratch before capture (a capture cannot
+            # allocate): one eager pass with an empty schedule into this
+            # step's own outputs, which the replay overwrites
+            self.sinj.load(None)
+            self.A.run(self.cent, E.row_sq_norms_dev(self.cent), NOOP_HOOK, it, self.slot,
+                       sinj=self.sinj)
+        t.cuda.synchronize()
+        gen0 = E.ctx_generation()
+        state = (self.slot, self.cbuf, self.cent)
+        todo = [(self.graphs, None)] + ([(self.inj_graphs, self.sinj)] if self.sinj else [])
+        for store, sinj in todo:
+            for par in (self.slot, 1 - self.slot):
+                if store[par] is not None:
+                    continue
+                self.slot = self.cbuf = par
+                self.cent = self.cent_buf[par]
+                g = t.cuda.CUDAGraph()
+                l0 = N.launch_count()
+                try:
+                    with t.cuda.graph(g, pool=self._pool):
+                        self._device_part(it, sinj)
+                except Exception:
+                    # a launch path that needs the host mid-step: stay eager
+                    t.cuda.synchronize()
+                    self.use_graph = False
+                    N.load().ftk_add_launches(-(N.launch_count() - l0))
+                    self.slot, self.cbuf, self.cent = state
+                    return False
+                store[par] = (g, N.launch_count() - l0)
+                N.load().ftk_add_launches(-store[par][1])  # captured, not run
+        self.slot, self.cbuf, self.cent = state
+        if E.ctx_generation() != gen0:  # a capture grew a scratch buffer: redo
+            self._drop_graphs()
+            return False
+        self.ctx_gen = gen0
+        return True
+
+    def warm_graphs(self, it=1):
+        """Capture the step graphs now (they are otherwise captured at the
+        first graph-eligible step); a no-op when graphs are off or ready."""
+        if self.use_graph and it >= 1 and (self.graphs[self.slot] is None or (
+                self.sinj is not None and self.inj_graphs[self.slot] is None)):
+            self._capture(it)
+
+    def _drop_graphs(self):
+        self.graphs = [None, None]
+        self.inj_graphs = [None, None]
+
     def _graph_step(self, it):
         t, A = self.t, self.A
-        g = self.graphs[self.slot]
-        if g is None:
-            # the step is captured, not run: replay it right after
-            g = t.cuda.CUDAGraph()
-            if self._pool is None:
-                self._pool = t.cuda.graph_pool_handle()
-            t.cuda.synchronize()
-            l0 = N.launch_count()
-            try:
-                with t.cuda.graph(g, pool=self._pool):
-                    self._device_part(it)
-            except Exception:
-                # a launch path that needs the host mid-step: stay eager
-                t.cuda.synchronize()
-                self.use_graph = False
-                N.load().ftk_add_launches(-(N.launch_count() - l0))
-                return self.step(it, eager=True)
-            self.graph_kernels[self.slot] = N.launch_count() - l0
-            N.load().ftk_add_launches(-self.graph_kernels[self.slot])  # captured, not run
-            self.graphs[self.slot] = g
+        if (A.checked and A.events.gen != self.graph_gen) or \
+                (self.ctx_gen is not None and E.ctx_generation() != self.ctx_gen):
+            self._drop_graphs()  # the event ring or a scratch buffer moved: recapture
+            self.graph_gen = A.events.gen if A.checked else 0
+            self.ctx_gen = None
+        arrs = None
+        if self.sinj is not None:
+            arrs = self.gemm_hook.kernel_arrays(it, self.dtype)
+        store, inj = self.graphs, None
+        if arrs is not None and len(arrs[0]):
+            store, inj = self.inj_graphs, self.sinj
+        if store[self.slot] is None and not self._capture(it):
+            return self.step(it, eager=True)
+        if inj is not None:
+            inj.load(arrs)  # stream-ordered before the replay
+        g, nk = store[self.slot]
         g.replay()
-        N.load().ftk_add_launches(self.graph_kernels[self.slot])
+        N.load().ftk_add_launches(nk)
         t.cuda.current_stream().synchronize()
-        rep = A.finish(self.gemm_hook, it, None,
-                       n_events=int(self.evc_host[0]) if A.checked else None)
+        rep = A.finish(self.gemm_hook, it, inj,
+                       n_events=int(self.evc_host[0]) if A.checked else None, replayed=True)
         if rep is not None:
             self.report.merge(rep)
         new_cent = self.cent_buf[1 - self.cbuf]
@@ -518,6 +594,10 @@ def lloyd(x, config, fault_spec=None):
     history = []
     converged = False
     iters = 0
+    # a full cyclic-GC pass over the torch-sized heap stalls the launching
+    # thread for tens of ms; the loop allocates no reference cycles
+    gc_on = gc.isenabled()
+    gc.disable()
     try:
         for it in range(config.max_iters):
             inertia, unchanged, moved = eng.step(it)
@@ -531,6 +611,8 @@ def lloyd(x, config, fault_spec=None):
         labels, inertia = eng.final(iters)
         centroids = E.to_host(eng.cent)
     finally:
+        if gc_on:
+            gc.enable()
         eng.close()
     timings["total_ns"] = time.perf_counter_ns() - t_total
     return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,

@@ -397,3 +397,38 @@ def test_graph_replay_equals_eager(ft):
     assert runs[1][2], "graph mode did not capture"
     assert runs[0][0] == runs[1][0]
     assert runs[0][1].tobytes() == runs[1][1].tobytes()
+
+
+def test_graph_replay_with_injections_equals_eager():
+    """Injected passes replayed from the device-count injection graph give the
+    eager path's bits: per-step outputs, centroids, detection events (with
+    their real iteration numbers) and the hook's record of landed flips."""
+    from paper_2408_01391_b200 import _engine as E
+    from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    x, _, _ = P.gaussian_mixture(20010, 64, 96, 0.3, precision="single", seed=3)
+    x_t = E.to_dev(x)
+    c0 = P.init_centroids(x, 96, seed=1, method="random-sample")
+    # duplicate blocks, an unsorted schedule, the partial last block (625:
+    # 10 rows), a flip past its live rows and a low mantissa bit
+    ents = [FaultEntry(2, (5, 0), (3, 7), 30), FaultEntry(4, (600, 0), (2, 2), 27),
+            FaultEntry(4, (17, 0), (0, 1), 29), FaultEntry(4, (17, 0), (9, 40), 31),
+            FaultEntry(7, (625, 0), (5, 95), 30), FaultEntry(7, (625, 0), (20, 3), 30),
+            FaultEntry(7, (3, 0), (31, 95), 30), FaultEntry(8, (1, 0), (1, 1), 2)]
+    runs = []
+    for graph in (False, True):
+        hook = ScheduledFaultHook(FaultSchedule(list(ents)))
+        eng = LloydEngine(x_t, c0, 96, np.float32, P.default_config(np.float32), "abft",
+                          P.Threshold.default_for(np.float32), 8, gemm_hook=hook, graph=graph)
+        outs = [eng.step(it) for it in range(10)]
+        evs = [(e.iteration, e.tile, e.kind, e.loc, e.delta) for e in eng.report.events]
+        runs.append((outs, E.to_host(eng.cent).copy(), evs, hook.injected,
+                     eng.inj_graphs[0] is not None or eng.inj_graphs[1] is not None))
+        eng.close()
+    assert runs[1][4], "injected passes were not replayed from a graph"
+    assert runs[0][0] == runs[1][0]
+    assert runs[0][1].tobytes() == runs[1][1].tobytes()
+    assert runs[0][2] == runs[1][2]
+    assert len(runs[0][2]) >= 4
+    assert runs[0][3] == runs[1][3]

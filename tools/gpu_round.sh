@@ -20,3 +20,7 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:pair
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:seg_partials -s 2 -c 1 \
   -o $OUT/seg python tools/prof_lloyd.py --steps 4 > $OUT/ncu_seg.log 2>&1; echo "ncu-seg rc=$?"
 fi
+if [ -z "$NO_NCU" ]; then
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:dmma_screen -s 1 -c 1 \
+  -o $OUT/dmma python tools/prof_cfg.py --n 2000000 --d 64 --k 256 --dtype f64 --ft abft --steps 2 > $OUT/ncu_dmma.log 2>&1; echo "ncu-dmma rc=$?"
+fi
