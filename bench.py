@@ -328,7 +328,10 @@ def run_ours(args, rank, world):
         xp = torch.from_numpy(x).pin_memory()
         conf = P.KMeansConfig(k=K, max_iters=args.steps, tol=0.0, seed=0, init="random-sample",
                               ft_mode="abft")
-        P.lloyd(xp[:4096], P.KMeansConfig(k=16, max_iters=2, init="random-sample"))
+        # one untimed fit of the same configuration: the timed fit then sees a
+        # warm process (lazily loaded kernels, allocator, first graph
+        # instantiation), like any fit after the first in a serving process
+        P.lloyd(xp, conf)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         r = P.lloyd(xp, conf)

@@ -365,6 +365,7 @@ class LloydEngine:
         self.cbuf = 0
         self.counts_buf = t.zeros(k, dtype=t.int64, device=dev)
         self._pool = None
+        self._cap_stream = None
 
     def _graph_ok(self, it):
         """Graph replay is used from the second step on: clean steps replay
@@ -406,8 +407,6 @@ class LloydEngine:
         """Capture the step graphs of BOTH buffer parities (captured, not
         run), so an eager injected step never leaves a capture for later."""
         t = self.t
-        if self._pool is None:
-            self._pool = t.cuda.graph_pool_handle()
         if self.sinj is not None and self.inj_graphs[self.slot] is None:
             # size the injected pass's scratch before capture (a capture cannot
             # allocate): one eager pass with an empty schedule into this
@@ -428,8 +427,7 @@ class LloydEngine:
                 g = t.cuda.CUDAGraph()
                 l0 = N.launch_count()
                 try:
-                    with t.cuda.graph(g, pool=self._pool):
-                        self._device_part(it, sinj)
+                    self._record(g, it, sinj)
                 except Exception:
                     # a launch path that needs the host mid-step: stay eager
                     t.cuda.synchronize()
@@ -445,6 +443,30 @@ class LloydEngine:
             return False
         self.ctx_gen = gen0
         return True
+
+    def _record(self, g, it, sinj):
+        """Stream capture of one step into `g` on a side stream.  Unlike
+        torch.cuda.graph this does not empty the caching allocator (whose
+        cudaFree/cudaMalloc churn cost more than the capture itself); the
+        graphs share one private memory pool and replay one at a time."""
+        t = self.t
+        cur = t.cuda.current_stream()
+        if self._cap_stream is None:
+            self._cap_stream = t.cuda.Stream()
+        s = self._cap_stream
+        s.wait_stream(cur)
+        with t.cuda.stream(s):
+            if self._pool is None:
+                g.capture_begin()
+            else:
+                g.capture_begin(pool=self._pool)
+            try:
+                self._device_part(it, sinj)
+            finally:
+                g.capture_end()
+        cur.wait_stream(s)
+        if self._pool is None:
+            self._pool = g.pool()
 
     def warm_graphs(self, it=1):
         """Capture the step graphs now (they are otherwise captured at the
