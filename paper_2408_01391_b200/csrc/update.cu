@@ -98,6 +98,169 @@ __global__ void exclusive_scan_small_kernel(const int64_t *counts, int64_t k, in
     if (threadIdx.x == 0) offsets[k] = carry;
 }
 
+// ------------------------------------------------- stable counting sort --
+// Member lists (rows of each cluster in ascending sample order) for K up to
+// CS_MAX_K: per-block label histograms, a per-label scan over blocks, and a
+// stable scatter -- four small kernels in place of iota + a two-pass radix
+// sort + boundary counting + the count scan.  Block b owns rows
+// [b*chunk, (b+1)*chunk); within it, warp w owns a contiguous sub-chunk, so
+// (block, warp, lane) order is sample order.
+constexpr int CS_MAX_K = 8192;
+constexpr int CS_WARPS_MAX = 8;
+
+__host__ __device__ inline int cs_warps(int64_t k) {
+    // per-warp label counters in shared memory: <= 64 KB
+    int w = CS_WARPS_MAX;
+    while (w > 1 && int64_t(w) * k * 4 > 64 * 1024) w /= 2;
+    return w;
+}
+
+__global__ void cs_hist_kernel(const int32_t *labels, int64_t m, int64_t k, int64_t chunk,
+                               int32_t *hist, int64_t nb) {
+    extern __shared__ int32_t cnt[];
+    for (int64_t b = threadIdx.x; b < k; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    const int64_t r0 = int64_t(blockIdx.x) * chunk;
+    const int64_t r1 = r0 + chunk < m ? r0 + chunk : m;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        const int32_t lab = labels[i];
+        if (uint32_t(lab) < uint32_t(k)) atomicAdd(&cnt[lab], 1);  // out-of-range rows: no member
+    }
+    __syncthreads();
+    for (int64_t b = threadIdx.x; b < k; b += blockDim.x) hist[b * nb + blockIdx.x] = cnt[b];
+}
+
+// one warp per label: exclusive prefix over blocks (in place), label total
+__global__ void cs_binscan_kernel(int32_t *hist, int64_t nb, int64_t k, int64_t *counts) {
+    const int64_t bin = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (bin >= k) return;
+    int32_t *h = hist + bin * nb;
+    int64_t run = 0;
+    for (int64_t j0 = 0; j0 < nb; j0 += 32) {
+        const int32_t v = j0 + lane < nb ? h[j0 + lane] : 0;
+        int32_t s = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int32_t o = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += o;
+        }
+        if (j0 + lane < nb) h[j0 + lane] = int32_t(run) + s - v;
+        run += __shfl_sync(0xffffffffu, s, 31);
+    }
+    if (lane == 0) counts[bin] = run;
+}
+
+// Stable scatter: the block's per-label bases come from the scans; each warp
+// first counts its sub-chunk per label, the block turns those into per-warp
+// bases, then every warp walks its rows in order, 32 at a time, ranking equal
+// labels with __match_any_sync.
+__global__ void cs_scatter_kernel(const int32_t *labels, int64_t m, int64_t k, int64_t chunk,
+                                  const int32_t *hist, int64_t nb, const int64_t *offsets,
+                                  int32_t *perm) {
+    extern __shared__ int32_t wcnt[];  // [warps][k]
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t e = threadIdx.x; e < int64_t(nw) * k; e += blockDim.x) wcnt[e] = 0;
+    __syncthreads();
+    const int64_t r0 = int64_t(blockIdx.x) * chunk;
+    const int64_t r1 = r0 + chunk < m ? r0 + chunk : m;
+    const int64_t sub = (chunk + nw - 1) / nw;
+    const int64_t w0 = r0 + int64_t(w) * sub < r1 ? r0 + int64_t(w) * sub : r1;
+    const int64_t w1 = w0 + sub < r1 ? w0 + sub : r1;
+    int32_t *mine = wcnt + int64_t(w) * k;
+    for (int64_t i = w0 + lane; i < w1; i += 32) {
+        const int32_t lab = labels[i];
+        if (uint32_t(lab) < uint32_t(k)) atomicAdd(&mine[lab], 1);
+    }
+    __syncthreads();
+    // per-warp bases: global label start + this block's prefix + earlier warps
+    for (int64_t b = threadIdx.x; b < k; b += blockDim.x) {
+        int32_t run = int32_t(offsets[b]) + hist[b * nb + blockIdx.x];
+        for (int q = 0; q < nw; ++q) {
+            const int32_t c = wcnt[int64_t(q) * k + b];
+            wcnt[int64_t(q) * k + b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t base = w0; base < w1; base += 128) {
+        int32_t labs[4];  // four rounds of labels in flight
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = base + 32 * u + lane;
+            labs[u] = i < w1 ? labels[i] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = base + 32 * u + lane;
+            int32_t lab = labs[u];
+            const bool live = uint32_t(lab) < uint32_t(k);
+            if (!live) lab = -1 - lane;  // tail / out-of-range lanes: unique dummies
+            const unsigned peers = __match_any_sync(0xffffffffu, lab);
+            if (live) {
+                const int32_t pos = mine[lab] + __popc(peers & lt);
+                perm[pos] = int32_t(i);
+            }
+            __syncwarp();
+            if (live && (peers & lt) == 0) mine[lab] += __popc(peers);
+            __syncwarp();
+        }
+    }
+}
+
+// Single block: offsets = exclusive scan of the member counts and, for the
+// segmented update, the segment table -- seg_base = exclusive scan of
+// ceil(count / SEG), seg_cl[s] = cluster owning segment s.  Also zeroes the
+// replay queue counter.
+template <typename F>
+__device__ void block_exclusive_scan(F val, int64_t k, int64_t *out) {
+    __shared__ int64_t carry;
+    __shared__ int64_t warp_tot[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t base = 0; base < k; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int64_t v = i < k ? val(i) : 0;
+        int64_t s = v;
+        for (int off = 1; off < 32; off <<= 1) {
+            const int64_t o = __shfl_up_sync(0xffffffffu, s, off);
+            if (lane >= off) s += o;
+        }
+        if (lane == 31) warp_tot[w] = s;
+        __syncthreads();
+        if (w == 0) {
+            int64_t t = lane < int(blockDim.x / 32) ? warp_tot[lane] : 0;
+            for (int off = 1; off < 32; off <<= 1) {
+                const int64_t o = __shfl_up_sync(0xffffffffu, t, off);
+                if (lane >= off) t += o;
+            }
+            warp_tot[lane] = t;
+        }
+        __syncthreads();
+        const int64_t incl = s + (w ? warp_tot[w - 1] : 0);
+        if (i < k) out[i] = carry + incl - v;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) carry += incl;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[k] = carry;
+    __syncthreads();
+}
+
+constexpr int SEG_MEMBERS = 256;  // == SEG (segment length of the certified update)
+
+__global__ void offsets_segs_kernel(const int64_t *counts, int64_t k, int64_t *offsets,
+                                    int64_t *seg_base, int32_t *seg_cl, unsigned *zero) {
+    if (zero && threadIdx.x == 0) *zero = 0u;
+    block_exclusive_scan([&](int64_t i) { return counts[i]; }, k, offsets);
+    if (!seg_base) return;
+    block_exclusive_scan([&](int64_t i) { return (counts[i] + SEG_MEMBERS - 1) / SEG_MEMBERS; }, k,
+                         seg_base);
+    for (int64_t c = threadIdx.x; c < k; c += blockDim.x)
+        for (int64_t s = seg_base[c]; s < seg_base[c + 1]; ++s) seg_cl[s] = int32_t(c);
+}
+
 __global__ void iota_kernel(int32_t *v, int64_t m) {
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
          i += int64_t(gridDim.x) * blockDim.x)
@@ -266,6 +429,7 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
 // Segments of SEG members are summed in parallel; the combine step checks
 // the certificate and queues uncertified chains for the ordered kernel.
 constexpr int SEG = 256;
+static_assert(SEG == SEG_MEMBERS, "segment length");
 
 template <typename T> __device__ __forceinline__ int ulp_exp(T v);
 template <> __device__ __forceinline__ int ulp_exp<float>(float v) {
@@ -277,143 +441,127 @@ template <> __device__ __forceinline__ int ulp_exp<double>(double v) {
     return int(e == 0 ? 1 : e) - 1075;
 }
 
-__global__ void seg_count_kernel(const int64_t *counts, int64_t k, int64_t *nseg) {
-    for (int64_t c = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; c < k;
-         c += int64_t(gridDim.x) * blockDim.x)
-        nseg[c] = (counts[c] + SEG - 1) / SEG;
-}
 
 // Per segment and feature: the float64 partial sum of the segment's members
 // (in member order), max |v| and min (|v| bits - 1) -- the smallest nonzero
-// magnitude, whose exponent bounds the ulp exponent of every value.  Two
-// features per thread with 8-byte loads; ~8 instructions per element.
-template <bool DMR>
+// magnitude, whose exponent bounds the ulp exponent of every value.  V
+// consecutive features per thread (16-byte loads for V = 4); the segment's
+// owner comes from the segment table (seg_cl), not a search.
+template <int V> struct FVec;
+template <> struct FVec<4> { using T = float4; };
+template <> struct FVec<2> { using T = float2; };
+template <> struct FVec<1> { using T = float; };
+
+template <int V>
+__device__ __forceinline__ void fvec_load(const float *p, float (&v)[V]) {
+    if constexpr (V == 4) {
+        const float4 t = *reinterpret_cast<const float4 *>(p);
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else if constexpr (V == 2) {
+        const float2 t = *reinterpret_cast<const float2 *>(p);
+        v[0] = t.x; v[1] = t.y;
+    } else {
+        v[0] = *p;
+    }
+}
+
+template <bool DMR, int V>
 __global__ void __launch_bounds__(256) seg_partials_kernel(
     const float *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
-    int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
+    const int32_t *seg_cl, int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
     // The segment partial is only used when the whole chain is certified
     // exact (then any association gives the reference's bits), so the
     // members of a segment are split across `nph` thread phases and the
     // phase partials are combined through shared memory.
     __shared__ int64_t rowoff[SEG];
-    __shared__ int64_t info[3];
-    __shared__ double red_a[256 * 2], red_b[256 * 2];
-    __shared__ uint32_t red_mx[256 * 2], red_mn[256 * 2];
+    __shared__ double red_a[256 * V], red_b[DMR ? 256 * V : 1];
+    __shared__ uint32_t red_mx[256 * V], red_mn[256 * V];
     const int64_t s = blockIdx.x;
-    if (threadIdx.x == 0) {
-        // cluster owning segment s: largest c with seg_base[c] <= s
-        int64_t lo = 0, hi = k;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi + 1) / 2;
-            if (seg_base[mid] <= s) lo = mid; else hi = mid - 1;
-        }
-        info[0] = s < seg_base[k] ? lo : -1;
-        if (info[0] >= 0) {
-            const int64_t beg = offsets[lo] + (s - seg_base[lo]) * SEG;
-            const int64_t end = offsets[lo + 1];
-            info[1] = beg;
-            info[2] = (end - beg < SEG ? end - beg : SEG);
-        }
-    }
-    __syncthreads();
-    if (info[0] < 0) return;
-    const int64_t beg = info[1];
-    const int n = int(info[2]);
+    if (s >= seg_base[k]) return;  // launched for the largest possible segment count
+    const int64_t c = seg_cl[s];
+    const int64_t beg = offsets[c] + (s - seg_base[c]) * SEG;
+    const int64_t end = offsets[c + 1];
+    const int n = int(end - beg < SEG ? end - beg : SEG);
     for (int t = threadIdx.x; t < n; t += blockDim.x) rowoff[t] = int64_t(perm[beg + t]) * d;
     __syncthreads();
-    const bool pairs = (d & 1) == 0;
-    const int64_t nf = pairs ? d / 2 : d;
+    const int64_t nf = d / V;
     const int nph = nf >= int64_t(blockDim.x) ? 1 : int(blockDim.x / nf);
     const int ph = nph > 1 ? int(threadIdx.x / nf) : 0;
+    constexpr int U = V == 4 ? 4 : 8;  // vector loads in flight per thread
     for (int64_t f = nph > 1 ? int64_t(threadIdx.x % nf) : int64_t(threadIdx.x); f < nf;
          f += (nph > 1 ? nf : int64_t(blockDim.x))) {
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
-        uint32_t mx0 = 0, mx1 = 0, mn0 = 0xFFFFFFFFu, mn1 = 0xFFFFFFFFu;
+        double a[V], b[V];
+        uint32_t mx[V], mn[V];
+#pragma unroll
+        for (int h = 0; h < V; ++h) {
+            a[h] = 0.0;
+            b[h] = 0.0;
+            mx[h] = 0;
+            mn[h] = 0xFFFFFFFFu;
+        }
         if (ph < nph) {
-            constexpr int U = 8;
-            if (pairs) {
-                const float *xb = x + 2 * f;
-                for (int t = ph; t < n; t += U * nph) {
-                    float2 v[U];
+            const float *xb = x + V * f;
+            for (int t = ph; t < n; t += U * nph) {
+                float v[U][V];
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int tt = t + u * nph;
-                        v[u] = tt < n ? *reinterpret_cast<const float2 *>(xb + rowoff[tt])
-                                      : make_float2(0.f, 0.f);
-                    }
+                for (int u = 0; u < U; ++u) {
+                    const int tt = t + u * nph;
+                    if (tt < n) {
+                        fvec_load<V>(xb + rowoff[tt], v[u]);
+                    } else {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        a0 = __dadd_rn(a0, double(v[u].x));
-                        a1 = __dadd_rn(a1, double(v[u].y));
-                        if (DMR) {
-                            b0 = __dadd_rn(b0, double(v[u].x));
-                            b1 = __dadd_rn(b1, double(v[u].y));
-                        }
-                        const uint32_t u0 = __float_as_uint(v[u].x) & 0x7FFFFFFFu;
-                        const uint32_t u1 = __float_as_uint(v[u].y) & 0x7FFFFFFFu;
-                        mx0 = max(mx0, u0);
-                        mx1 = max(mx1, u1);
-                        mn0 = min(mn0, u0 - 1u);  // zeros wrap to 0xFFFFFFFF: ignored
-                        mn1 = min(mn1, u1 - 1u);
+                        for (int h = 0; h < V; ++h) v[u][h] = 0.0f;
                     }
                 }
-            } else {
-                for (int t = ph; t < n; t += nph) {
-                    const float v = x[rowoff[t] + f];
-                    a0 = __dadd_rn(a0, double(v));
-                    if (DMR) b0 = __dadd_rn(b0, double(v));
-                    const uint32_t u0 = __float_as_uint(v) & 0x7FFFFFFFu;
-                    mx0 = max(mx0, u0);
-                    mn0 = min(mn0, u0 - 1u);
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+#pragma unroll
+                    for (int h = 0; h < V; ++h) {
+                        a[h] = __dadd_rn(a[h], double(v[u][h]));
+                        if (DMR) b[h] = __dadd_rn(b[h], double(v[u][h]));
+                        const uint32_t w = __float_as_uint(v[u][h]) & 0x7FFFFFFFu;
+                        mx[h] = max(mx[h], w);
+                        mn[h] = min(mn[h], w - 1u);  // zeros wrap to 0xFFFFFFFF: ignored
+                    }
                 }
             }
         }
         if (nph > 1) {
-            // combine the phases of feature (pair) f
+            // combine the phases of feature group f
             const int slot = ph * int(nf) + int(f);
-            red_a[2 * slot] = a0;
-            red_a[2 * slot + 1] = a1;
-            if (DMR) {
-                red_b[2 * slot] = b0;
-                red_b[2 * slot + 1] = b1;
+#pragma unroll
+            for (int h = 0; h < V; ++h) {
+                red_a[V * slot + h] = a[h];
+                if (DMR) red_b[V * slot + h] = b[h];
+                red_mx[V * slot + h] = mx[h];
+                red_mn[V * slot + h] = mn[h];
             }
-            red_mx[2 * slot] = mx0;
-            red_mx[2 * slot + 1] = mx1;
-            red_mn[2 * slot] = mn0;
-            red_mn[2 * slot + 1] = mn1;
             __syncthreads();  // nph > 1: every thread runs exactly one f iteration
-        }
-        if (nph > 1) {
             if (ph != 0) continue;
             for (int q = 1; q < nph; ++q) {
-                const int slot = q * int(nf) + int(f);
-                a0 = __dadd_rn(a0, red_a[2 * slot]);
-                a1 = __dadd_rn(a1, red_a[2 * slot + 1]);
-                if (DMR) {
-                    b0 = __dadd_rn(b0, red_b[2 * slot]);
-                    b1 = __dadd_rn(b1, red_b[2 * slot + 1]);
+                const int sl = q * int(nf) + int(f);
+#pragma unroll
+                for (int h = 0; h < V; ++h) {
+                    a[h] = __dadd_rn(a[h], red_a[V * sl + h]);
+                    if (DMR) b[h] = __dadd_rn(b[h], red_b[V * sl + h]);
+                    mx[h] = max(mx[h], red_mx[V * sl + h]);
+                    mn[h] = min(mn[h], red_mn[V * sl + h]);
                 }
-                mx0 = max(mx0, red_mx[2 * slot]);
-                mx1 = max(mx1, red_mx[2 * slot + 1]);
-                mn0 = min(mn0, red_mn[2 * slot]);
-                mn1 = min(mn1, red_mn[2 * slot + 1]);
             }
         }
         // q = exponent of the ulp of the smallest nonzero magnitude (a lower
         // bound of every value's ulp exponent); bound = n * max|v|
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !pairs) break;
-            const int64_t ff = pairs ? 2 * f + h : f;
-            const uint32_t mn = h ? mn1 : mn0, mx = h ? mx1 : mx0;
+        for (int h = 0; h < V; ++h) {
+            const int64_t ff = V * f + h;
             int q = INT_MAX;
-            if (mn != 0xFFFFFFFFu) {
-                const int e = int((mn + 1u) >> 23);
+            if (mn[h] != 0xFFFFFFFFu) {
+                const int e = int((mn[h] + 1u) >> 23);
                 q = (e == 0 ? 1 : e) - 150;
             }
-            ps_a[s * d + ff] = h ? a1 : a0;
-            if (DMR) ps_b[s * d + ff] = h ? b1 : b0;
-            ps_abs[s * d + ff] = double(n) * double(__uint_as_float(mx));
+            ps_a[s * d + ff] = a[h];
+            if (DMR) ps_b[s * d + ff] = b[h];
+            ps_abs[s * d + ff] = double(n) * double(__uint_as_float(mx[h]));
             ps_q[s * d + ff] = q;
         }
     }
@@ -935,6 +1083,27 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         }
         FTK_LAUNCHED("histogram_kernel");
     }
+    // update path (decided up front: the member-offset scan also builds the
+    // segment table of the certified segmented sums)
+    const bool dmr = sums_b != nullptr;
+    const int64_t nwarps = k * ((d + 31) / 32);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const bool pipe_chains = m > 0 && (dtype == FTK_F64 || nwarps <= int64_t(nsm) * 12);
+    const bool use_seg = dtype == FTK_F32 && m > 0 && !pipe_chains;
+    const int64_t max_seg = (m + SEG - 1) / SEG + k;
+    int64_t *seg_base = nullptr;
+    int32_t *seg_cl = nullptr;
+    int64_t *fail_list = nullptr;
+    unsigned *fail_count = nullptr;
+    if (use_seg) {
+        seg_base = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_BASE, sizeof(int64_t) * (k + 2) +
+                                                                          sizeof(int32_t) * max_seg, st));
+        fail_list = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_FB, sizeof(int64_t) * (k * d + 2), st));
+        if (!seg_base || !fail_list) return FTK_ERR_CUDA;
+        seg_cl = reinterpret_cast<int32_t *>(seg_base + (k + 2));
+        fail_count = reinterpret_cast<unsigned *>(fail_list + k * d);
+    }
     // stable sort of (label, index) -> member lists in ascending sample order
     int bits = 1;
     while ((int64_t(1) << bits) < k) ++bits;
@@ -943,7 +1112,29 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     int64_t *offsets = static_cast<int64_t *>(scratch(ctx, SLOT_OFFSETS, sizeof(int64_t) * (k + 1), st));
     if (!keys_out || !vals || !offsets) return FTK_ERR_CUDA;
     int32_t *vals_in = vals, *vals_out = vals + (m + 1);
-    if (m > 0) {
+    if (m > 0 && k <= CS_MAX_K && m < (int64_t(1) << 31)) {
+        const int64_t chunk = std::max<int64_t>(2048, (m + 2047) / 2048);
+        const int64_t nb = (m + chunk - 1) / chunk;
+        int32_t *hist = keys_out;  // k x nb counters (<= 4 * 2048 * CS_MAX_K bytes)
+        if (k * nb > 2 * (m + 1)) {
+            hist = static_cast<int32_t *>(scratch(ctx, SLOT_SORT_TMP, sizeof(int32_t) * k * nb, st));
+            if (!hist) return FTK_ERR_CUDA;
+        }
+        const int nw = cs_warps(k);
+        cs_hist_kernel<<<unsigned(nb), 256, sizeof(int32_t) * k, st>>>(labels, m, k, chunk, hist, nb);
+        FTK_LAUNCHED("cs_hist_kernel");
+        cs_binscan_kernel<<<unsigned((k * 32 + 255) / 256), 256, 0, st>>>(hist, nb, k, counts_a);
+        FTK_LAUNCHED("cs_binscan_kernel");
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        FTK_LAUNCHED("offsets_segs_kernel");
+        const size_t smw = sizeof(int32_t) * size_t(nw) * k;
+        if (smw > 48 * 1024)
+            FTK_CUDA(cudaFuncSetAttribute(cs_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(smw)));
+        cs_scatter_kernel<<<unsigned(nb), 32 * nw, smw, st>>>(labels, m, k, chunk, hist, nb, offsets,
+                                                            vals_out);
+        FTK_LAUNCHED("cs_scatter_kernel");
+    } else if (m > 0) {
         iota_kernel<<<grid_for(m, 256), 256, 0, st>>>(vals_in, m);
         FTK_LAUNCHED("iota_kernel");
         size_t tmp_bytes = 0;
@@ -957,17 +1148,15 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         boundary_count_kernel<<<grid_for(m, 256), 256, 0, st>>>(
             keys_out, m, k, reinterpret_cast<unsigned long long *>(counts_a));
         FTK_LAUNCHED("boundary_count_kernel");
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        FTK_LAUNCHED("offsets_segs_kernel");
+    } else {
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        FTK_LAUNCHED("offsets_segs_kernel");
     }
-    exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets);
-    FTK_LAUNCHED("exclusive_scan_small_kernel");
     const int64_t warps = k * ((d + 31) / 32);
     const int block = 256;
     const unsigned grid = unsigned((warps * 32 + block - 1) / block);
-    const bool dmr = sums_b != nullptr;
-    const int64_t nwarps = k * ((d + 31) / 32);
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const bool pipe_chains = m > 0 && (dtype == FTK_F64 || nwarps <= int64_t(nsm) * 12);
     if (pipe_chains) {
         // few long chains: the reference's ordered chain, latency-hidden
         const unsigned g = unsigned((nwarps + CH_WARPS - 1) / CH_WARPS);
@@ -986,33 +1175,24 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         FTK_LAUNCHED("chain_pipe_kernel");
         return FTK_OK;
     }
-    if (dtype == FTK_F32 && m > 0) {
+    if (use_seg) {
         // certified segmented sums (float32 data): segments fold exactly
         // unless their certificate fails, in which case only that segment is
         // re-walked in member order
-        const int64_t max_seg = (m + SEG - 1) / SEG + k;
-        int64_t *seg_base = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_BASE, sizeof(int64_t) * (2 * k + 2), st));
         size_t pbytes = size_t(max_seg) * d * (3 * sizeof(double) + sizeof(int32_t)) + 64;
         char *pbuf = static_cast<char *>(scratch(ctx, SLOT_SEG_PART, pbytes, st));
-        if (!seg_base || !pbuf) return FTK_ERR_CUDA;
-        int64_t *nseg = seg_base + (k + 1);
+        if (!pbuf) return FTK_ERR_CUDA;
         double *ps_a = reinterpret_cast<double *>(pbuf);
         double *ps_b = ps_a + max_seg * d;
         double *ps_abs = ps_b + max_seg * d;
         int32_t *ps_q = reinterpret_cast<int32_t *>(ps_abs + max_seg * d);
-        seg_count_kernel<<<grid_for(k, 256), 256, 0, st>>>(counts_a, k, nseg);
-        FTK_LAUNCHED("seg_count_kernel");
-        exclusive_scan_small_kernel<<<1, 1024, 0, st>>>(nseg, k, seg_base);
-        FTK_LAUNCHED("exclusive_scan_small_kernel");
         auto xx = static_cast<const float *>(x);
-        int64_t *fail_list = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_FB, sizeof(int64_t) * (k * d + 2), st));
-        if (!fail_list) return FTK_ERR_CUDA;
-        unsigned *fail_count = reinterpret_cast<unsigned *>(fail_list + k * d);
-        FTK_CUDA(cudaMemsetAsync(fail_count, 0, sizeof(unsigned), st));
         const unsigned rgrid = unsigned(std::min<int64_t>(k * d, 148 * 8));
         if (dmr) {
-            seg_partials_kernel<true><<<unsigned(max_seg), 256, 0, st>>>(
-                xx, d, vals_out, offsets, seg_base, k, ps_a, ps_b, ps_abs, ps_q);
+            auto kp = d % 4 == 0 ? seg_partials_kernel<true, 4>
+                      : (d % 2 == 0 ? seg_partials_kernel<true, 2> : seg_partials_kernel<true, 1>);
+            kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                  ps_b, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
             seg_fold_kernel<true><<<grid_for(k * d, 128), 128, 0, st>>>(
                 seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count);
@@ -1021,8 +1201,10 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
                                                           ps_b, ps_abs, ps_q, fail_list, fail_count,
                                                           sums_a, sums_b);
         } else {
-            seg_partials_kernel<false><<<unsigned(max_seg), 256, 0, st>>>(
-                xx, d, vals_out, offsets, seg_base, k, ps_a, nullptr, ps_abs, ps_q);
+            auto kp = d % 4 == 0 ? seg_partials_kernel<false, 4>
+                      : (d % 2 == 0 ? seg_partials_kernel<false, 2> : seg_partials_kernel<false, 1>);
+            kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                  nullptr, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
             seg_fold_kernel<false><<<grid_for(k * d, 128), 128, 0, st>>>(
                 seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count);

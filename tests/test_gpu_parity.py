@@ -330,6 +330,8 @@ def test_native_library_is_the_one_loaded():
     (60000, 32, 2048, np.float32, True),    # + tiny values: uncertified chains replayed in order
     (40000, 96, 5, np.float32, True),       # few long chains: pipelined ordered chains
     (30000, 24, 7, np.float64, False),      # float64 data: pipelined ordered chains
+    (200000, 8, 8192, np.float32, False),   # counting sort at its largest K (2 warps, 64 KB smem)
+    (50000, 16, 9000, np.float32, True),    # K beyond the counting sort: radix-sort member lists
 ])
 def test_update_paths_bit_exact(m, d, k, dt, tiny):
     """Every update path (segment partials with the exactness certificate,
