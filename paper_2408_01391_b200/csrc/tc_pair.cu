@@ -52,6 +52,7 @@ constexpr int PR_BM = 128;          // rows per CTA
 constexpr int PR_BN = PAIR_BN;      // centroids per N tile (half per CTA)
 constexpr int PR_NBUF = 512 / PR_BN;  // TMEM accumulator buffers
 constexpr int PR_KB = 32;           // fp32 elements per 128-byte swizzle row
+constexpr int PR_MAX_KB = 8;        // k-blocks of the widest X row (d <= 256)
 constexpr int PR_THREADS = 480;     // 15 warps
 // Warp roles.  The SMSP arbiter favours the highest warp id, so the
 // latency-critical single-thread roles (MMA issue, TMA producers) take the
@@ -96,7 +97,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
     uint64_t *t_full = a_full + 4, *t_empty = t_full + PR_NBUF;
     uint64_t *p_full = t_empty + PR_NBUF, *p_empty = p_full + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(p_empty + 2);
+    // X k-block release, per buffer: the refine warps free each k-block of a
+    // row tile's X half as soon as they have consumed it, so the next X half
+    // streams in behind the refine instead of after it
+    uint64_t *a_kbe = p_empty + 2;  // [2][PR_MAX_KB]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_kbe + 2 * PR_MAX_KB);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -119,6 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&a_full[a], rank == 0 ? 2 : 1);  // leader: own TMA + peer's forward
             mbar_init(&a_empty[a], 4);  // refine warps, done with the X half
+            for (int kb = 0; kb < PR_MAX_KB; ++kb) mbar_init(&a_kbe[a * PR_MAX_KB + kb], 4);
             mbar_init(&p_full[a], 8);
             mbar_init(&p_empty[a], 4);
         }
@@ -196,12 +202,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const uint32_t lead = mapa_shared(smem_u32(&a_full[0]), 0);
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
                 const int ab = it % NA;
-                mbar_wait(&a_empty[ab], (uint32_t(it / NA) & 1) ^ 1);
                 unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
+                const uint32_t par = (uint32_t(it / NA) & 1) ^ 1;
+                mbar_wait(&a_kbe[ab * PR_MAX_KB], par);
                 mbar_expect_tx(&a_full[ab], A_BYTES);
-                for (int kb = 0; kb < nkb; ++kb)
+                for (int kb = 0; kb < nkb; ++kb) {
+                    if (kb) mbar_wait(&a_kbe[ab * PR_MAX_KB + kb], par);
                     tma_load_2d(a_dst + size_t(kb) * PR_A_KB, &tmX, &a_full[ab], kb * PR_KB, row0);
+                }
                 if (rank == 1) {  // the leader's MMA reads this half too
                     mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);
                     mbar_arrive_remote(lead + uint32_t(ab) * 8u);
@@ -377,6 +386,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             float thr_out = INFINITY;          // pass-2 candidate threshold
             unsigned long long seed_out = ~0ull;  // (ordered d1, j1) key
             const bool active = !COLLECT && grow < M && m1 < INFINITY && !(P.dbg & 2);
+            bool released = false;  // X k-blocks handed back (warp-uniform)
             if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
@@ -438,17 +448,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         }
                     }
                 };
+                auto release = [&](int kb) {  // this warp is done reading X k-block kb
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
+                };
                 PROBE_T(lp0_);
                 float4 cA[8], cB[8];
                 load_c(cA, 0);
                 for (int kb = 0; kb < nkb; kb += 2) {
                     if (kb + 1 < nkb) load_c(cB, kb + 1);
                     consume(cA, kb);
+                    release(kb);
                     if (kb + 1 < nkb) {
                         if (kb + 2 < nkb) load_c(cA, kb + 2);
                         consume(cB, kb + 1);
+                        release(kb + 1);
                     }
                 }
+                released = true;
                 PROBE_T(lp1_);
                 PROBE_ADD(8, lp1_ - lp0_);
               if (active) {  // lanes without a live row only helped with the loads
@@ -506,7 +523,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&a_empty[ab]);  // X half no longer read
+            if (!released && lane == 0)
+                for (int kb = 0; kb < nkb; ++kb) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
             PROBE_ADD(7, clock64() - rw1_);
         }
     }
@@ -529,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 size_t pair_smem_bytes(int nkb, int abufs, int stages) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * PR_B_HALF +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
-           8 * 8 * sizeof(float4) + (8 + 2 * PR_NBUF) * 8 + 64;
+           8 * 8 * sizeof(float4) + (2 * size_t(stages) + 8 + 2 * PR_NBUF + 2 * PR_MAX_KB) * 8 + 64;
 }
 
 int pair_plan(int64_t d, int *abufs, int *stages) {

@@ -641,45 +641,68 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
     const int64_t *seg_base, const double *ps_a, const double *ps_b, const double *ps_abs,
     const int32_t *ps_q, const int64_t *fail_list, const unsigned *fail_count, double *sums_a,
     double *sums_b) {
-    constexpr int TILE = 2048;
-    __shared__ float vals[TILE];
+    // Segments of the chain are taken 8 at a time (TILE members): the block
+    // gathers their member values and summaries into shared memory, then one
+    // thread walks them in order -- a segment whose partial provably joins
+    // the running sum exactly (certificate against the running sum's lowest
+    // set bit) is added as a whole, any other segment is summed member by
+    // member, the reference's sequential float64 chain.
+    constexpr int SPT = 8;  // segments per tile
+    constexpr int TILE = SPT * SEG;
+    __shared__ __align__(16) float vals[TILE];
+    __shared__ double sp_a[SPT], sp_b[SPT], sp_abs[SPT];
+    __shared__ int32_t sp_q[SPT];
     __shared__ double run[2];
-    __shared__ int64_t start;
     const unsigned nfail = *fail_count;
     for (unsigned w = blockIdx.x; w < nfail; w += gridDim.x) {
         const int64_t e = fail_list[w];
         const int64_t c = e / d, f = e % d;
-        if (threadIdx.x == 0) {
-            const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
-            double a = 0.0, b = 0.0;
-            int64_t s = s0;
-            for (; s < s1; ++s) {
-                const int qseg = ps_q[s * d + f];
-                if (qseg == INT_MAX) continue;  // all-zero segment
-                const int qa = lowbit_exp(a);
-                const int q = qa < qseg ? qa : qseg;
-                const double bound = fabs(a) + ps_abs[s * d + f] * (1.0 + 0x1p-20);
-                if (!(q > -1000 && bound < ldexp(1.0, 53 + q)) || (DMR && a != b)) break;
-                a = __dadd_rn(a, ps_a[s * d + f]);
-                if (DMR) b = __dadd_rn(b, ps_b[s * d + f]);
-            }
-            run[0] = a;
-            run[1] = b;
-            start = offsets[c] + (s - s0) * SEG;
-        }
-        __syncthreads();
-        const int64_t hi = offsets[c + 1];
-        for (int64_t t0 = start; t0 < hi; t0 += TILE) {
-            const int n = int(hi - t0 < TILE ? hi - t0 : TILE);
+        const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+        const int64_t m0 = offsets[c], m1 = offsets[c + 1];
+        if (threadIdx.x == 0) run[0] = run[1] = 0.0;
+        for (int64_t sb = s0; sb < s1; sb += SPT) {
+            const int ns = int(s1 - sb < SPT ? s1 - sb : SPT);
+            const int64_t t0 = m0 + (sb - s0) * SEG;
+            const int n = int(m1 - t0 < TILE ? m1 - t0 : TILE);
             for (int t = threadIdx.x; t < n; t += blockDim.x)
                 vals[t] = x[int64_t(perm[t0 + t]) * d + f];
+            if (int(threadIdx.x) < ns) {
+                const int64_t q = (sb + threadIdx.x) * d + f;
+                sp_a[threadIdx.x] = ps_a[q];
+                if (DMR) sp_b[threadIdx.x] = ps_b[q];
+                sp_abs[threadIdx.x] = ps_abs[q];
+                sp_q[threadIdx.x] = ps_q[q];
+            }
             __syncthreads();
             if (threadIdx.x == 0) {
                 double a = run[0], b = run[1];
-                for (int t = 0; t < n; ++t) {
-                    const double v = double(vals[t]);
-                    a = __dadd_rn(a, v);
-                    if (DMR) b = __dadd_rn(b, v);
+                for (int j = 0; j < ns; ++j) {
+                    const int qseg = sp_q[j];
+                    if (qseg == INT_MAX) continue;  // all-zero segment
+                    const int qa = lowbit_exp(a);
+                    const int q = qa < qseg ? qa : qseg;
+                    const double bound = fabs(a) + sp_abs[j] * (1.0 + 0x1p-20);
+                    if (q > -1000 && bound < ldexp(1.0, 53 + q) && (!DMR || a == b)) {
+                        a = __dadd_rn(a, sp_a[j]);
+                        if (DMR) b = __dadd_rn(b, sp_b[j]);
+                        continue;
+                    }
+                    const int lo = j * SEG, hi = (j + 1) * SEG < n ? (j + 1) * SEG : n;
+                    const float4 *v4 = reinterpret_cast<const float4 *>(vals);
+                    int t = lo;
+                    for (; t + 8 <= hi; t += 8) {
+                        const float4 p = v4[t / 4], r = v4[t / 4 + 1];
+                        const float vv[8] = {p.x, p.y, p.z, p.w, r.x, r.y, r.z, r.w};
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            a = __dadd_rn(a, double(vv[u]));
+                            if (DMR) b = __dadd_rn(b, double(vv[u]));
+                        }
+                    }
+                    for (; t < hi; ++t) {
+                        a = __dadd_rn(a, double(vals[t]));
+                        if (DMR) b = __dadd_rn(b, double(vals[t]));
+                    }
                 }
                 run[0] = a;
                 run[1] = b;
@@ -1214,6 +1237,12 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
                                                            fail_count, sums_a, nullptr);
         }
         FTK_LAUNCHED("seg_replay_kernel");
+        if (getenv("FTK_UPD_DEBUG")) {  // diagnostics: chains the certificate sent to the replay
+            unsigned nf = 0;
+            cudaMemcpyAsync(&nf, fail_count, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+            cudaStreamSynchronize(st);
+            fprintf(stderr, "update: %u of %lld chains replayed in order\n", nf, (long long)(k * d));
+        }
         return FTK_OK;
     }
     if (dtype == FTK_F32) {
