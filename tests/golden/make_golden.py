@@ -315,6 +315,45 @@ def dmr_cases():
     np.savez_compressed(os.path.join(OUT, "dmr_cases.npz"), meta=np.array(rec), **arrays)
 
 
+CLI_CASES = [
+    # (name, generate args, cluster args)
+    ("gm_off", ["--rows", "3000", "--cols", "16", "--dist", "gm:8:0.1", "--seed", "4"],
+     ["--k", "8", "--max-iters", "50", "--init", "kmeanspp", "--seed", "2"]),
+    ("gm_abft_inject", ["--rows", "4000", "--cols", "24", "--dist", "gm:12:0.2", "--seed", "5"],
+     ["--k", "12", "--ft", "abft", "--inject", "prob:0.05@exp", "--max-iters", "30", "--tol", "0",
+      "--init", "random-sample", "--seed", "1"]),
+    ("uni_dmr_f64", ["--rows", "2500", "--cols", "9", "--precision", "double", "--seed", "6"],
+     ["--k", "5", "--ft", "abft+dmr", "--max-iters", "20", "--init", "random-sample"]),
+]
+
+
+def cli_cases():
+    """Reference ``ftkm cluster`` RunReports (machine-independent rows) on
+    datasets written by the reference ``ftkm generate``."""
+    import csv
+    import tempfile
+
+    from ftkmeans import cli
+
+    out = {}
+    with tempfile.TemporaryDirectory() as td:
+        for name, gen, clu in CLI_CASES:
+            path = os.path.join(td, name + ".ftkm")
+            rep = os.path.join(td, name + ".csv")
+            assert cli.main(["generate", *gen, "--out", path]) == 0
+            code = cli.main(["cluster", "--input", path, *clu, "--report", rep])
+            with open(rep) as fh:
+                rows = [r for r in csv.reader(fh)][1:]
+            keep = [r for r in rows if r[0] in ("result", "ft", "summary", "config")
+                    or (r[0] == "meta" and r[1] in ("precision", "rows", "cols", "schema_version"))]
+            with open(path, "rb") as fh:
+                data_sha = hashlib.sha256(fh.read()).hexdigest()
+            out[name] = {"generate": gen, "cluster": clu, "exit": code, "rows": keep,
+                         "file_sha256": data_sha}
+    with open(os.path.join(OUT, "cli_cases.json"), "w") as fh:
+        json.dump(out, fh, indent=1)
+
+
 if __name__ == "__main__":
     sweep_cases()
     acceptance4_cases()
@@ -328,4 +367,5 @@ if __name__ == "__main__":
     lloyd_cases()
     lloyd_ft_cases()
     lloyd_c1()
+    cli_cases()
     print("golden fixtures written to", OUT)
