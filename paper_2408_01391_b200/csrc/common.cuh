@@ -84,6 +84,7 @@ enum ScratchSlot {
     SLOT_PAIR_CAND = 19,  // pass-2 candidate list, keys, counters
     SLOT_DS = 20,         // float64 screen: bounds, counters, fallback rows
     SLOT_DS_G = 21,       // float64 screen: gathered fallback rows
+    SLOT_EXACT_SPLIT = 22,  // per-(row, column split) argmin partials of the exact kernel
 };
 
 // ------------------------------------------------------- float helpers --

@@ -16,6 +16,8 @@
 
 #include <cfloat>
 
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ftk {
@@ -41,6 +43,10 @@ struct ExactParams {
     const int64_t *ibi, *ibj, *iei, *iej, *ibit;
     int64_t *iapplied;
     double *ibefore, *iafter;
+    // column-split grid (gridDim.y > 1): per-(row, split) argmin partials,
+    // merged by exact_split_merge_kernel
+    void *part_v;
+    int32_t *part_j;
     // events (abft.py:281-294)
     int64_t ev_cap;
     int64_t *ev_rec;
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
         __syncthreads();
     }
 
-    for (int64_t bj = 0; bj < nbj; ++bj) {
+    for (int64_t bj = blockIdx.y; bj < nbj; bj += gridDim.y) {
         const int64_t j0 = bj * bn;
         const int nj = int(bn < P.k - j0 ? bn : P.k - j0);
         const bool live_col = jl < nj;
@@ -512,8 +518,30 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
         T bv = T(INFINITY);
         int32_t bj = 0;
         for (int w = 0; w < nw; ++w) argmin_merge(bv, bj, rv[i * nw + w], rj[i * nw + w]);
-        P.out_idx[i0 + i] = bj;
-        static_cast<T *>(P.out_val)[i0 + i] = bv;
+        if (gridDim.y > 1) {
+            const int64_t q = (i0 + i) * gridDim.y + blockIdx.y;
+            static_cast<T *>(P.part_v)[q] = bv;
+            P.part_j[q] = bj;
+        } else {
+            P.out_idx[i0 + i] = bj;
+            static_cast<T *>(P.out_val)[i0 + i] = bv;
+        }
+    }
+}
+
+// Merge of the column-split partials: the same total order (value, then
+// index; NaN never wins) as the in-CTA reduction, so the split is invisible.
+template <typename T>
+__global__ void exact_split_merge_kernel(const T *pv, const int32_t *pj, int gy, int64_t m,
+                                         const int64_t *m_dev, int32_t *out_idx, T *out_val) {
+    const int64_t mm = m_dev ? *m_dev : m;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < mm;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        T bv = T(INFINITY);
+        int32_t bj = 0;
+        for (int s = 0; s < gy; ++s) argmin_merge(bv, bj, pv[i * gy + s], pj[i * gy + s]);
+        out_idx[i] = bj;
+        out_val[i] = bv;
     }
 }
 
@@ -586,8 +614,20 @@ static int launch_tm(const ExactParams &P, int threads, size_t smem, cudaStream_
         FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       int(smem)));
     int64_t nbi = (P.m + P.prow - 1) / P.prow;
-    kern<<<dim3(unsigned(nbi)), dim3(threads), smem, st>>>(P);
+    // few row blocks (replayed injected blocks, small inputs): split the
+    // logical column blocks over gridDim.y so more SMs share the pass
+    const int64_t nbj = (P.k + P.bn - 1) / P.bn;
+    int gy = 1;
+    if (P.part_v && !P.out_mat && nbj > 1 && nbi < 2 * 148)
+        gy = int(std::min<int64_t>(std::min<int64_t>(nbj, (2 * 148 + nbi - 1) / nbi), 64));
+    kern<<<dim3(unsigned(nbi), unsigned(gy)), dim3(threads), smem, st>>>(P);
     FTK_LAUNCHED("exact_tile_kernel");
+    if (gy > 1) {
+        exact_split_merge_kernel<T><<<unsigned(std::min<int64_t>((P.m + 255) / 256, 148 * 8)), 256, 0, st>>>(
+            static_cast<const T *>(P.part_v), P.part_j, gy, P.m, P.m_dev, P.out_idx,
+            static_cast<T *>(P.out_val));
+        FTK_LAUNCHED("exact_split_merge_kernel");
+    }
     return FTK_OK;
 }
 
@@ -651,6 +691,15 @@ int exact_run_m(ftk_ctx *ctx, int dtype, const void *x, const void *y, const voi
     P.pb = int(pb);
     P.out_idx = out_idx; P.out_val = out_val; P.out_mat = out_mat;
     P.m_dev = m_dev;
+    if (!out_mat && k > bn && m <= 2 * 148 * bm) {  // room for the column-split partials
+        const size_t per = sizeof(double) + sizeof(int32_t);
+        const int64_t nbj = (k + bn - 1) / bn;
+        const int64_t splits = nbj < 64 ? nbj : 64;
+        char *pb = static_cast<char *>(scratch(ctx, SLOT_EXACT_SPLIT, size_t(m) * splits * per + 64, st));
+        if (!pb) return FTK_ERR_CUDA;
+        P.part_v = pb;
+        P.part_j = reinterpret_cast<int32_t *>(pb + size_t(m) * splits * sizeof(double));
+    }
     P.delta_rel = delta_rel; P.abs_tol = abs_tol; P.iteration = iteration;
     if (inj && inj->n > 0) {
         P.n_inj = inj->n;

@@ -245,6 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             int inj_c = -1;
             float inj_b = 0.0f, inj_a = 0.0f;
             const float thr = (COLLECT && grow < M) ? P.thr[grow] : -INFINITY;
+            unsigned ncand = 0;  // COLLECT: this thread's candidates of the row
             if (CHK && P.inj_col && grow < M) {
                 inj_c = P.inj_col[grow];
                 if (inj_c >= 0) {
@@ -294,13 +295,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             ffma2_m2(__uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]),
                                      yv.z, yv.w, d[2], d[3]);
 #pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (d[u] <= thr && c0 + ch * 32 + 4 * q + u < P.k) {
-                                    const unsigned slot = atomicAdd(P.cand_count, 1u);
-                                    atomicAdd(P.row_cnt + grow, 1u);
-                                    if (slot < P.cand_cap)
-                                        P.cand[slot] = make_int2(int(grow), int(c0) + ch * 32 + 4 * q + u);
+                            for (int u = 0; u < 4; ++u) {
+                                // warp-aggregated append: one counter atomic per
+                                // warp and column, not one per candidate
+                                const int col = int(c0) + ch * 32 + 4 * q + u;
+                                const bool hit = d[u] <= thr && col < P.k;
+                                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                                if (bal) {
+                                    const int leader = __ffs(bal) - 1;
+                                    unsigned base = 0;
+                                    if (lane == leader) base = atomicAdd(P.cand_count, unsigned(__popc(bal)));
+                                    base = __shfl_sync(0xffffffffu, base, leader);
+                                    if (hit) {
+                                        const unsigned slot = base + __popc(bal & ((1u << lane) - 1u));
+                                        if (slot < P.cand_cap) P.cand[slot] = make_int2(int(grow), col);
+                                        ++ncand;
+                                    }
                                 }
+                            }
                         }
                     }
                 } else if (!(P.dbg & 1)) {
@@ -339,6 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 asm volatile("bar.sync 1, 256;" ::: "memory");
                 ybuf ^= 1;
             }
+            if (COLLECT && ncand) atomicAdd(P.row_cnt + grow, ncand);
             // publish this warpgroup's partial for the row tile
             mbar_wait(&p_empty[pb], (uint32_t(it >> 1) & 1) ^ 1);
             PairPart pp;
