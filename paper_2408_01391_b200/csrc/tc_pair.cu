@@ -295,24 +295,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             ffma2_m2(__uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]),
                                      yv.z, yv.w, d[2], d[3]);
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                // warp-aggregated append: one counter atomic per
-                                // warp and column, not one per candidate
-                                const int col = int(c0) + ch * 32 + 4 * q + u;
-                                const bool hit = d[u] <= thr && col < P.k;
-                                const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                                if (bal) {
-                                    const int leader = __ffs(bal) - 1;
-                                    unsigned base = 0;
-                                    if (lane == leader) base = atomicAdd(P.cand_count, unsigned(__popc(bal)));
-                                    base = __shfl_sync(0xffffffffu, base, leader);
-                                    if (hit) {
-                                        const unsigned slot = base + __popc(bal & ((1u << lane) - 1u));
-                                        if (slot < P.cand_cap) P.cand[slot] = make_int2(int(grow), col);
-                                        ++ncand;
-                                    }
+                            for (int u = 0; u < 4; ++u)
+                                if (d[u] <= thr && c0 + ch * 32 + 4 * q + u < P.k) {
+                                    const unsigned slot = atomicAdd(P.cand_count, 1u);
+                                    ++ncand;  // row count: one atomic per row and warpgroup
+                                    if (slot < P.cand_cap)
+                                        P.cand[slot] = make_int2(int(grow), int(c0) + ch * 32 + 4 * q + u);
                                 }
-                            }
                         }
                     }
                 } else if (!(P.dbg & 1)) {
