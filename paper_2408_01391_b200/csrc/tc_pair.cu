@@ -78,7 +78,9 @@ __device__ __forceinline__ uint32_t ordered_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-template <bool CHK, bool COLLECT>
+// INJ: the pass carries scheduled flips (P.inj_col); a separate instantiation
+// keeps the per-chunk injection test out of the clean CHK epilogue (-2.7%).
+template <bool CHK, bool COLLECT, bool INJ>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     pair_screen_kernel(const __grid_constant__ CUtensorMap tmX,
                        const __grid_constant__ CUtensorMap tmC, PairParams P) {
@@ -246,7 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             float inj_b = 0.0f, inj_a = 0.0f;
             const float thr = (COLLECT && grow < M) ? P.thr[grow] : -INFINITY;
             unsigned ncand = 0;  // COLLECT: this thread's candidates of the row
-            if (CHK && P.inj_col && grow < M) {
+            if (INJ && P.inj_col && grow < M) {
                 inj_c = P.inj_col[grow];
                 if (inj_c >= 0) {
                     inj_b = P.inj_before[grow];
@@ -265,7 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 float s0 = 0.0f, s1 = 0.0f;
                 const uint32_t tbase = tmem + lane_base + uint32_t(buf * PR_BN + wg * HALF);
                 const float *ynt = yns + ybuf * PR_BN + wg * HALF;
-                const bool inj_here = CHK && inj_c >= int(c0) && inj_c < int(c0) + HALF;
+                const bool inj_here = INJ && inj_c >= int(c0) && inj_c < int(c0) + HALF;
                 if (P.dbg & 4) {
                     // timing probe: TMEM drain only (values folded with one XOR per column)
                     uint32_t va[32], acc = 0;
@@ -313,12 +315,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 #pragma unroll 1
                     for (int ch = 0; ch < HALF / 32; ch += 2) {
                         tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
-                        if (inj_here && (inj_c - int(c0)) >> 5 == ch)
+                        if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
                             inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
                         screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
                         tmem_ld_wait(vb);
                         if (ch + 2 < HALF / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
-                        if (inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
+                        if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
                             inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
                         screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(wg * HALF + (ch + 1) * 32), a1,
                                        a2, s0, s1);
@@ -583,8 +585,11 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int64_t ncl = npt < nsm / 2 ? npt : nsm / 2;
-    auto kern = chk ? (P.thr ? pair_screen_kernel<true, true> : pair_screen_kernel<true, false>)
-                    : (P.thr ? pair_screen_kernel<false, true> : pair_screen_kernel<false, false>);
+    auto kern = chk ? (P.thr ? pair_screen_kernel<true, true, false>
+                             : (P.inj_col ? pair_screen_kernel<true, false, true>
+                                          : pair_screen_kernel<true, false, false>))
+                    : (P.thr ? pair_screen_kernel<false, true, false>
+                             : pair_screen_kernel<false, false, false>);
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<dim3(unsigned(2 * ncl)), dim3(PR_THREADS), smem, st>>>(mx, mc, P);
     FTK_LAUNCHED("pair_screen_kernel");
