@@ -641,18 +641,18 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
     const int64_t *seg_base, const double *ps_a, const double *ps_b, const double *ps_abs,
     const int32_t *ps_q, const int64_t *fail_list, const unsigned *fail_count, double *sums_a,
     double *sums_b) {
-    // Segments of the chain are taken 8 at a time (TILE members): the block
-    // gathers their member values and summaries into shared memory, then one
-    // thread walks them in order -- a segment whose partial provably joins
-    // the running sum exactly (certificate against the running sum's lowest
-    // set bit) is added as a whole, any other segment is summed member by
-    // member, the reference's sequential float64 chain.
-    constexpr int SPT = 8;  // segments per tile
-    constexpr int TILE = SPT * SEG;
-    __shared__ __align__(16) float vals[TILE];
-    __shared__ double sp_a[SPT], sp_b[SPT], sp_abs[SPT];
-    __shared__ int32_t sp_q[SPT];
+    // One thread walks the chain's segment summaries (staged 256 at a time):
+    // a segment whose partial provably joins the running sum exactly
+    // (certificate against the running sum's lowest set bit) is added whole;
+    // at a segment that fails, the block gathers that segment's member values
+    // and the thread sums them one by one, the reference's sequential float64
+    // chain.  Only failing segments touch X.
+    constexpr int SB = 256;  // summaries staged per round (== blockDim.x)
+    __shared__ __align__(16) float vals[SEG];
+    __shared__ double sp_a[SB], sp_b[DMR ? SB : 1], sp_abs[SB];
+    __shared__ int32_t sp_q[SB];
     __shared__ double run[2];
+    __shared__ int next;
     const unsigned nfail = *fail_count;
     for (unsigned w = blockIdx.x; w < nfail; w += gridDim.x) {
         const int64_t e = fail_list[w];
@@ -660,13 +660,10 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
         const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
         const int64_t m0 = offsets[c], m1 = offsets[c + 1];
         if (threadIdx.x == 0) run[0] = run[1] = 0.0;
-        for (int64_t sb = s0; sb < s1; sb += SPT) {
-            const int ns = int(s1 - sb < SPT ? s1 - sb : SPT);
-            const int64_t t0 = m0 + (sb - s0) * SEG;
-            const int n = int(m1 - t0 < TILE ? m1 - t0 : TILE);
-            for (int t = threadIdx.x; t < n; t += blockDim.x)
-                vals[t] = x[int64_t(perm[t0 + t]) * d + f];
-            if (int(threadIdx.x) < ns) {
+        for (int64_t sb = s0; sb < s1; sb += SB) {
+            const int cnt = int(s1 - sb < SB ? s1 - sb : SB);
+            __syncthreads();
+            if (int(threadIdx.x) < cnt) {
                 const int64_t q = (sb + threadIdx.x) * d + f;
                 sp_a[threadIdx.x] = ps_a[q];
                 if (DMR) sp_b[threadIdx.x] = ps_b[q];
@@ -674,23 +671,37 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
                 sp_q[threadIdx.x] = ps_q[q];
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                double a = run[0], b = run[1];
-                for (int j = 0; j < ns; ++j) {
-                    const int qseg = sp_q[j];
-                    if (qseg == INT_MAX) continue;  // all-zero segment
-                    const int qa = lowbit_exp(a);
-                    const int q = qa < qseg ? qa : qseg;
-                    const double bound = fabs(a) + sp_abs[j] * (1.0 + 0x1p-20);
-                    if (q > -1000 && bound < ldexp(1.0, 53 + q) && (!DMR || a == b)) {
+            int j = 0;
+            while (true) {
+                if (threadIdx.x == 0) {
+                    double a = run[0], b = run[1];
+                    for (; j < cnt; ++j) {
+                        const int qseg = sp_q[j];
+                        if (qseg == INT_MAX) continue;  // all-zero segment
+                        const int qa = lowbit_exp(a);
+                        const int q = qa < qseg ? qa : qseg;
+                        const double bound = fabs(a) + sp_abs[j] * (1.0 + 0x1p-20);
+                        if (!(q > -1000 && bound < ldexp(1.0, 53 + q)) || (DMR && a != b)) break;
                         a = __dadd_rn(a, sp_a[j]);
                         if (DMR) b = __dadd_rn(b, sp_b[j]);
-                        continue;
                     }
-                    const int lo = j * SEG, hi = (j + 1) * SEG < n ? (j + 1) * SEG : n;
+                    run[0] = a;
+                    run[1] = b;
+                    next = j;
+                }
+                __syncthreads();
+                j = next;
+                if (j >= cnt) break;
+                // gather the failing segment's members (one per thread)
+                const int64_t t0 = m0 + (sb + j - s0) * SEG;
+                const int n = int(m1 - t0 < SEG ? m1 - t0 : SEG);
+                if (int(threadIdx.x) < n) vals[threadIdx.x] = x[int64_t(perm[t0 + threadIdx.x]) * d + f];
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    double a = run[0], b = run[1];
                     const float4 *v4 = reinterpret_cast<const float4 *>(vals);
-                    int t = lo;
-                    for (; t + 8 <= hi; t += 8) {
+                    int t = 0;
+                    for (; t + 8 <= n; t += 8) {
                         const float4 p = v4[t / 4], r = v4[t / 4 + 1];
                         const float vv[8] = {p.x, p.y, p.z, p.w, r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -699,15 +710,16 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
                             if (DMR) b = __dadd_rn(b, double(vv[u]));
                         }
                     }
-                    for (; t < hi; ++t) {
+                    for (; t < n; ++t) {
                         a = __dadd_rn(a, double(vals[t]));
                         if (DMR) b = __dadd_rn(b, double(vals[t]));
                     }
+                    run[0] = a;
+                    run[1] = b;
                 }
-                run[0] = a;
-                run[1] = b;
+                ++j;
+                __syncthreads();
             }
-            __syncthreads();
         }
         if (threadIdx.x == 0) {
             sums_a[e] = run[0];
@@ -1112,7 +1124,12 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     const int64_t nwarps = k * ((d + 31) / 32);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const bool pipe_chains = m > 0 && (dtype == FTK_F64 || nwarps <= int64_t(nsm) * 12);
+    // float64 data: every partial sum rounds (full 53-bit values), so the
+    // reference's ordered chain runs as is; float32: certified segments,
+    // whatever the chain count (measured faster at c1, c3 and c2)
+    bool pipe_chains = m > 0 && dtype == FTK_F64;
+    if (const char *e = getenv("FTK_UPD_PATH"))  // A/B knob: "seg" or "pipe" (float32 data)
+        if (dtype == FTK_F32 && m > 0) pipe_chains = e[0] == 'p';
     const bool use_seg = dtype == FTK_F32 && m > 0 && !pipe_chains;
     const int64_t max_seg = (m + SEG - 1) / SEG + k;
     int64_t *seg_base = nullptr;
