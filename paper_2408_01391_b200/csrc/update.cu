@@ -577,39 +577,36 @@ template <bool DMR>
 __global__ void seg_fold_kernel(const int64_t *seg_base, int64_t k, int64_t d,
                                 const double *ps_a, const double *ps_b, const double *ps_abs,
                                 const int32_t *ps_q, double *sums_a, double *sums_b,
-                                int64_t *fail_list, unsigned *fail_count) {
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < k * d;
-         e += int64_t(gridDim.x) * blockDim.x) {
+                                int64_t *fail_list, unsigned *fail_count, int lanes) {
+    // `lanes` (a power of two <= 32) threads per chain stride over its
+    // segments and combine by shuffles: any association is exact when the
+    // certificate holds, and the bound's rounding stays far below its margin
+    const int sub = int(threadIdx.x) & (lanes - 1);
+    const int64_t groups = (int64_t(gridDim.x) * blockDim.x) / lanes;
+    const int64_t mine = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / lanes;
+    const int64_t first = (int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31u)) / lanes;
+    // the trip count follows the warp's first group, so whole warps shuffle
+    for (int64_t r = 0; first + r * groups < k * d; ++r) {
+        const int64_t e0 = mine + r * groups;
+        const bool live = e0 < k * d;
+        const int64_t e = live ? e0 : 0;
         const int64_t c = e / d, f = e % d;
-        const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+        const int64_t s0 = live ? seg_base[c] : 0, s1 = live ? seg_base[c + 1] : 0;
         double a = 0.0, b = 0.0, bnd = 0.0;
         int q = INT_MAX;
-        int64_t s = s0;
-        constexpr int U = 4;
-        for (; s + U <= s1; s += U) {
-            double pa[U], pb[U], pn[U];
-            int pq[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                pa[u] = ps_a[(s + u) * d + f];
-                if (DMR) pb[u] = ps_b[(s + u) * d + f];
-                pn[u] = ps_abs[(s + u) * d + f];
-                pq[u] = ps_q[(s + u) * d + f];
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                a = __dadd_rn(a, pa[u]);
-                if (DMR) b = __dadd_rn(b, pb[u]);
-                bnd = __dadd_rn(bnd, pn[u]);
-                q = min(q, pq[u]);
-            }
-        }
-        for (; s < s1; ++s) {
+        for (int64_t s = s0 + sub; s < s1; s += lanes) {
             a = __dadd_rn(a, ps_a[s * d + f]);
             if (DMR) b = __dadd_rn(b, ps_b[s * d + f]);
             bnd = __dadd_rn(bnd, ps_abs[s * d + f]);
             q = min(q, ps_q[s * d + f]);
         }
+        for (int off = lanes / 2; off; off >>= 1) {
+            a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, off, lanes));
+            if (DMR) b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, off, lanes));
+            bnd = __dadd_rn(bnd, __shfl_xor_sync(0xffffffffu, bnd, off, lanes));
+            q = min(q, __shfl_xor_sync(0xffffffffu, q, off, lanes));
+        }
+        if (!live || sub != 0) continue;
         const bool exact = q == INT_MAX || (q > -1000 && bnd * (1.0 + 0x1p-20) < ldexp(1.0, 53 + q));
         if (exact) {
             sums_a[e] = a;
@@ -1227,15 +1224,20 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         double *ps_abs = ps_b + max_seg * d;
         int32_t *ps_q = reinterpret_cast<int32_t *>(ps_abs + max_seg * d);
         auto xx = static_cast<const float *>(x);
-        const unsigned rgrid = unsigned(std::min<int64_t>(k * d, 148 * 8));
+        // replay: one block per failing chain (the count is on the device, so
+        // size for many); fold: enough lanes per chain to cover its segments
+        const unsigned rgrid = unsigned(std::min<int64_t>(k * d, 148 * 32));
+        int lanes = 1;
+        while (lanes < 32 && int64_t(lanes) * k < max_seg) lanes *= 2;
+        const unsigned fgrid = grid_for(k * d * lanes, 128);
         if (dmr) {
             auto kp = d % 4 == 0 ? seg_partials_kernel<true, 4>
                       : (d % 2 == 0 ? seg_partials_kernel<true, 2> : seg_partials_kernel<true, 1>);
             kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
                                                   ps_b, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<true><<<grid_for(k * d, 128), 128, 0, st>>>(
-                seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count);
+            seg_fold_kernel<true><<<fgrid, 128, 0, st>>>(
+                seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count, lanes);
             FTK_LAUNCHED("seg_fold_kernel");
             seg_replay_kernel<true><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
                                                           ps_b, ps_abs, ps_q, fail_list, fail_count,
@@ -1246,8 +1248,8 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
             kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
                                                   nullptr, ps_abs, ps_q);
             FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<false><<<grid_for(k * d, 128), 128, 0, st>>>(
-                seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count);
+            seg_fold_kernel<false><<<fgrid, 128, 0, st>>>(
+                seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count, lanes);
             FTK_LAUNCHED("seg_fold_kernel");
             seg_replay_kernel<false><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
                                                            nullptr, ps_abs, ps_q, fail_list,
