@@ -50,6 +50,7 @@ constexpr int TC_BM = 128;       // rows per CTA (UMMA M)
 constexpr int TC_KB = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int TC_THREADS = 192;  // 6 warps
 constexpr int TC_MAX_D = 256;    // resident-A limit
+constexpr int TC_SX_MAX_D = 8192;  // streamed-X pair screen (k <= PAIR_BN)
 
 struct TcParams {
     const float *x;      // rows x d  (exact values; pass 2: the gathered rows)
@@ -780,7 +781,15 @@ static int screen(int bn, const TcParams &P, const CUtensorMap &mx, const CUtens
 }
 
 int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
-    return dtype == FTK_F32 && d >= 8 && d % 4 == 0 && d <= TC_MAX_D && k >= 1 && m >= 1 &&
+    // d > 256: the CTA-pair screen with X streamed through its stages (one
+    // column tile, k <= 256) -- experimental, FTK_TC_SX=1: its exact refine
+    // reads X rows from global memory and is latency-bound (c3 D=512 K=16:
+    // pass 1 2.0 ms, 0.49 ms without the refine), no faster than the exact
+    // kernel yet.  The resident-X kernels stop at 256.
+    const char *sx = getenv("FTK_TC_SX");
+    const bool sx_on = sx && atoi(sx) == 1;
+    return dtype == FTK_F32 && d >= 8 && d % 4 == 0 &&
+           (d <= TC_MAX_D || (sx_on && k <= PAIR_BN && d <= TC_SX_MAX_D)) && k >= 1 && m >= 1 &&
            m < (int64_t(1) << 31) && k < (int64_t(1) << 24);
 }
 
@@ -988,7 +997,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             P.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));
         }
         const char *pe = getenv("FTK_TC_PAIR");
-        if (!(pe && atoi(pe) == 0) && d <= TC_MAX_D && raw == nullptr) {
+        if (!(pe && atoi(pe) == 0) && (d <= TC_MAX_D || k <= PAIR_BN) && raw == nullptr) {
             // CTA-pair kernel (tc_pair.cu): M = 256 per cluster, half the L2 traffic
             CUtensorMap mc128;
             if ((rc = make_map(&mc128, yf, k, d, PAIR_BN / 2))) return rc;
@@ -1043,6 +1052,10 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                 fprintf(stderr, "pair clk per row tile: refine wait %.0f busy %.0f (loop %.0f, post %.0f)\n", h[6] / nrt, h[7] / nrt, h[8] / nrt, h[9] / nrt);
             }
         } else {
+            if (d > TC_MAX_D) {
+                set_error("tc variant: d > 256 needs the CTA-pair screen");
+                return FTK_ERR_UNSUPPORTED;
+            }
             rc = screen<false>(bn, P, mx, mx, mc, mc, st);
             ctx->last_path = 0;
         }

@@ -80,17 +80,22 @@ __device__ __forceinline__ uint32_t ordered_key(float f) {
 
 // INJ: the pass carries scheduled flips (P.inj_col); a separate instantiation
 // keeps the per-chunk injection test out of the clean CHK epilogue (-2.7%).
-template <bool CHK, bool COLLECT, bool INJ>
+// SX (streamed X, d > 256 with K <= 256, i.e. one column tile): the X half
+// no longer fits resident, so its k-blocks travel with the centroid k-blocks
+// through the stage ring (each stage = centroid half + X half) and the
+// refine reads its row from global memory (L2: the tile was just streamed).
+template <bool CHK, bool COLLECT, bool INJ, bool SX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     pair_screen_kernel(const __grid_constant__ CUtensorMap tmX,
                        const __grid_constant__ CUtensorMap tmC, PairParams P) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int nkb = P.nkb, S = P.stages, NA = P.abufs;
-    const uint32_t A_BYTES = PR_A_KB * nkb;
+    const uint32_t A_BYTES = SX ? 0u : PR_A_KB * nkb;
+    constexpr uint32_t STG = SX ? PR_B_HALF + PR_A_KB : PR_B_HALF;  // bytes per stage
     unsigned char *sA = smem;
     unsigned char *sB = sA + size_t(NA) * A_BYTES;
-    PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * PR_B_HALF);  // [2][2][128]
+    PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * STG);  // [2][2][128]
     double *psum = reinterpret_cast<double *>(part + 2 * 2 * PR_BM);           // [2][2][128]
     float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
     float4 *css = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // ABFT checksum centroid [nkb * 8]
@@ -149,13 +154,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             uint32_t phase = 0;
             int it = 0;
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+                const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
                 for (int t = 0; t < P.ntiles; ++t) {
                     const int c0 = t * PR_BN + int(rank) * (PR_BN / 2);
                     for (int kb = 0; kb < nkb; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
-                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * PR_B_HALF);
-                        tma_load_2d_pair(sB + size_t(stage) * PR_B_HALF, &tmC,
-                                         mapa_shared(smem_u32(&full[stage]), 0), kb * PR_KB, c0);
+                        const uint32_t fb = mapa_shared(smem_u32(&full[stage]), 0);
+                        if (rank == 0) mbar_expect_tx(&full[stage], 2 * STG);
+                        tma_load_2d_pair(sB + size_t(stage) * STG, &tmC, fb, kb * PR_KB, c0);
+                        if (SX)  // this CTA's X half of the k-block, same stage
+                            tma_load_2d_pair(sB + size_t(stage) * STG + PR_B_HALF, &tmX, fb, kb * PR_KB,
+                                             row0);
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -171,8 +180,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             uint32_t g = 0;
             int it = 0;
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
-                const int ab = it % NA;
-                { PROBE_T(c0_); mbar_wait(&a_full[ab], uint32_t(it / NA) & 1); PROBE_ADD(4, clock64() - c0_); }
+                const int ab = SX ? 0 : it % NA;
+                if (!SX) {
+                    PROBE_T(c0_);
+                    mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);
+                    PROBE_ADD(4, clock64() - c0_);
+                }
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA) + uint32_t(ab) * A_BYTES;
                 for (int t = 0; t < P.ntiles; ++t, ++g) {
@@ -183,11 +196,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     for (int kb = 0; kb < nkb; ++kb) {
                         { PROBE_T(c0_); mbar_wait(&full[stage], phase); PROBE_ADD(3, clock64() - c0_); }
                         tc_fence_after();
-                        const uint32_t bs = b_base + uint32_t(stage) * PR_B_HALF;
+                        const uint32_t bs = b_base + uint32_t(stage) * STG;
+                        const uint32_t as = SX ? bs + PR_B_HALF : a_base + uint32_t(kb) * PR_A_KB;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
-                            mma_tf32_pair(d_tmem, smem_desc(a_base + uint32_t(kb) * PR_A_KB + kk * 32),
-                                          smem_desc(bs + kk * 32), idesc, (kb | kk) != 0);
+                            mma_tf32_pair(d_tmem, smem_desc(as + kk * 32), smem_desc(bs + kk * 32), idesc,
+                                          (kb | kk) != 0);
                         mma_commit_pair(&empty[stage], 0x3);
                         if (++stage == S) { stage = 0; phase ^= 1; }
                     }
@@ -199,7 +213,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         // ------------------------------- X producer (+ peer forwarding) --
         // decoupled from the centroid stream so the next row tile's X half
         // loads as soon as its buffer is released, not behind the B stages
-        if (lane == 0) {
+        if (lane == 0 && !SX) {
             int it = 0;
             const uint32_t lead = mapa_shared(smem_u32(&a_full[0]), 0);
             for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
@@ -308,23 +322,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     }
                 } else if (!(P.dbg & 1)) {
                     // software-pipelined TMEM drain, two 32-column chunks per
-                    // (not unrolled) iteration to keep the loop in the I-cache
+                    // (not unrolled) iteration to keep the loop in the I-cache;
+                    // in a partial last tile, chunks past the last centroid are
+                    // skipped (a plain loop: the full-tile loop stays as is)
+                    const int live = int(P.k - c0);
                     uint32_t va[32], vb[32];
-                    tmem_ld32_issue(tbase, va);
-                    tmem_ld_wait(va);
+                    if (live >= HALF) {
+                        tmem_ld32_issue(tbase, va);
+                        tmem_ld_wait(va);
 #pragma unroll 1
-                    for (int ch = 0; ch < HALF / 32; ch += 2) {
-                        tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
-                        if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
-                            inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
-                        screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
-                        tmem_ld_wait(vb);
-                        if (ch + 2 < HALF / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
-                        if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
-                            inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
-                        screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(wg * HALF + (ch + 1) * 32), a1,
-                                       a2, s0, s1);
-                        if (ch + 2 < HALF / 32) tmem_ld_wait(va);
+                        for (int ch = 0; ch < HALF / 32; ch += 2) {
+                            tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
+                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
+                                inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
+                            tmem_ld_wait(vb);
+                            if (ch + 2 < HALF / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
+                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
+                                inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                            screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(wg * HALF + (ch + 1) * 32),
+                                           a1, a2, s0, s1);
+                            if (ch + 2 < HALF / 32) tmem_ld_wait(va);
+                        }
+                    } else {
+#pragma unroll 1
+                        for (int ch = 0; ch * 32 < live; ++ch) {
+                            tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
+                            tmem_ld_wait(va);
+                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
+                                inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
+                        }
                     }
                 }
                 tc_fence_before();
@@ -359,7 +387,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         // ----------------------------------------------------- refine --
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
-        if (CHK) {
+        if (CHK && !SX) {
             const int t = (warp - W_REFINE0) * 32 + lane;  // 0..127
             if (t < nkb * 8) css[t] = __ldg(reinterpret_cast<const float4 *>(P.csum) + t);
             asm volatile("bar.sync 3, 128;" ::: "memory");
@@ -367,7 +395,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         int it = 0;
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
-            const int ab = it % NA;
+            const int ab = SX ? 0 : it % NA;
             PROBE_T(rw0_);
             mbar_wait(&p_full[pb], uint32_t(it >> 1) & 1);
             PROBE_T(rw1_);
@@ -383,7 +411,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const int j = take1 ? q1.j1 : q0.j1;
             const float m2 = fminf(fminf(q0.m2, q1.m2), fmaxf(q0.m1, q1.m1));
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
-            mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // own X half resident + visible
+            if (!SX) mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // own X half resident + visible
             const unsigned char *sAt = sA + size_t(ab) * A_BYTES + uint32_t(r) * 128;
             bool ok = false;
             float dval = 0.0f;
@@ -394,7 +422,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
-                const float4 *cs4 = css;  // staged once per CTA (ABFT)
+                // checksum centroid: staged once per CTA (ABFT), from global when streamed
+                const float4 *cs4 = SX ? reinterpret_cast<const float4 *>(P.csum) : css;
+                const float4 *xg4 = reinterpret_cast<const float4 *>(P.x + (active ? grow : 0) * P.d);
                 const bool have_info = P.rowinfo != nullptr;
                 if (have_info) {
                     const float4 ri = __ldg(P.rowinfo + grow);
@@ -419,7 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     for (int q = 0; q < 8; ++q) {
                         if (k0 + 4 * q < P.d) {
                             const float4 xv =
-                                *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
+                                SX ? __ldg(xg4 + kb * 8 + q)
+                                   : *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
                             const float4 c4 = cv[q];
                             acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
                             acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
@@ -453,6 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     }
                 };
                 auto release = [&](int kb) {  // this warp is done reading X k-block kb
+                    if (SX) return;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
                 };
@@ -527,7 +559,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
             }
             __syncwarp();
-            if (!released && lane == 0)
+            if (!SX && !released && lane == 0)
                 for (int kb = 0; kb < nkb; ++kb) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
             PROBE_ADD(7, clock64() - rw1_);
         }
@@ -548,19 +580,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 }
 
 // ------------------------------------------------------------- host ------
-size_t pair_smem_bytes(int nkb, int abufs, int stages) {
-    return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * PR_B_HALF +
+size_t pair_smem_bytes(int nkb, int abufs, int stages, bool sx) {
+    return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * (sx ? PR_B_HALF + PR_A_KB : PR_B_HALF) +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
            8 * 8 * sizeof(float4) + (2 * size_t(stages) + 8 + 2 * PR_NBUF + 2 * PR_MAX_KB) * 8 + 64;
 }
 
 int pair_plan(int64_t d, int *abufs, int *stages) {
     const int nkb = int((d + PR_KB - 1) / PR_KB);
+    const bool sx = nkb > PR_MAX_KB;  // X streamed through the stages
     const size_t cap = 227 * 1024;
-    int na = 2;
-    if (pair_smem_bytes(nkb, 2, 3) > cap) na = 1;
+    int na = sx ? 0 : 2;
+    if (!sx && pair_smem_bytes(nkb, 2, 3, false) > cap) na = 1;
     int s = 12;
-    while (s >= 2 && pair_smem_bytes(nkb, na, s) > cap) --s;
+    while (s >= 2 && pair_smem_bytes(nkb, na, s, sx) > cap) --s;
     if (s < 2) return -1;
     *abufs = na;
     *stages = s;
@@ -579,17 +612,27 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     }
     P.nkb = int((P.d + PR_KB - 1) / PR_KB);
     P.ntiles = int((P.k + PR_BN - 1) / PR_BN);
-    const size_t smem = pair_smem_bytes(P.nkb, P.abufs, P.stages);
+    const bool sx = P.nkb > PR_MAX_KB;
+    if (sx && P.ntiles != 1) {
+        set_error("tc pair: streamed X (d > 256) needs k <= 256");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    const size_t smem = pair_smem_bytes(P.nkb, P.abufs, P.stages, sx);
     const int64_t npt = (P.m + 2 * PR_BM - 1) / (2 * PR_BM);
     if (npt == 0) return FTK_OK;
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int64_t ncl = npt < nsm / 2 ? npt : nsm / 2;
-    auto kern = chk ? (P.thr ? pair_screen_kernel<true, true, false>
-                             : (P.inj_col ? pair_screen_kernel<true, false, true>
-                                          : pair_screen_kernel<true, false, false>))
-                    : (P.thr ? pair_screen_kernel<false, true, false>
-                             : pair_screen_kernel<false, false, false>);
+    auto kern = sx ? (chk ? (P.thr ? pair_screen_kernel<true, true, false, true>
+                                   : (P.inj_col ? pair_screen_kernel<true, false, true, true>
+                                                : pair_screen_kernel<true, false, false, true>))
+                          : (P.thr ? pair_screen_kernel<false, true, false, true>
+                                   : pair_screen_kernel<false, false, false, true>))
+                   : (chk ? (P.thr ? pair_screen_kernel<true, true, false, false>
+                                   : (P.inj_col ? pair_screen_kernel<true, false, true, false>
+                                                : pair_screen_kernel<true, false, false, false>))
+                          : (P.thr ? pair_screen_kernel<false, true, false, false>
+                                   : pair_screen_kernel<false, false, false, false>));
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<dim3(unsigned(2 * ncl)), dim3(PR_THREADS), smem, st>>>(mx, mc, P);
     FTK_LAUNCHED("pair_screen_kernel");

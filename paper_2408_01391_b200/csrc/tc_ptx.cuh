@@ -512,7 +512,9 @@ __device__ __forceinline__ void screen32t(const uint32_t (&v)[32], const float *
     const float u2 = fminf(fminf(r[6], r[7]), r[8]);
     const float w0 = fminf(fminf(u0, u1), u2);
     const float hmin = fminf(fminf(w0, r[9]), r[10]);
-    M2 = fminf(fminf(M2, hmin), fmaxf(L1, c1));
+    // a chunk with no live column has c1 = NaN: it must not demote the
+    // running champion to runner-up (fmaxf would return L1)
+    M2 = fminf(fminf(M2, hmin), c1 == c1 ? fmaxf(L1, c1) : INFINITY);
     L1 = fminf(L1, c1);
 }
 }  // namespace ftk

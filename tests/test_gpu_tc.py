@@ -136,3 +136,69 @@ def test_tc_checked_matches_reference_events(golden):
         assert inj.tobytes() == z[f"{n}_inj"].tobytes(), n
         # the tensor-core checksum itself saw the above-threshold flips
         assert E.tc_fallback_rows()[2] >= 1, n
+
+
+@pytest.mark.parametrize("m,d,k", [(3000, 512, 16), (1500, 2048, 8), (2000, 300, 200),
+                                   (700, 260, 256), (4100, 1024, 33)])
+def test_tc_streamed_x_matches_reference(m, d, k, monkeypatch):
+    """d > 256 with k <= 256 (experimental, FTK_TC_SX=1): the pair screen
+    streams X through its stages and the refine reads the row from global
+    memory -- still the reference's bits."""
+    monkeypatch.setenv("FTK_TC_SX", "1")
+    rng = np.random.default_rng(m + d + k)
+    x = np.ascontiguousarray(rng.standard_normal((m, d)), dtype=np.float32)
+    y = np.ascontiguousarray(x[rng.choice(m, k, replace=False)] +
+                             0.3 * rng.standard_normal((k, d)).astype(np.float32))
+    lab, val, fb = _tc(x, y)
+    ref_lab, ref_val = O.assign(x, y)
+    assert np.array_equal(lab, ref_lab)
+    assert val.tobytes() == ref_val.tobytes()
+    assert fb[0] < m  # the screen certified rows itself (the TC path ran)
+
+
+def test_tc_streamed_x_checked_with_flips(monkeypatch):
+    """ABFT on the streamed-X screen: fault-free -> no alarm and the reference's
+    bits; scheduled flips -> the exact checked kernel's events and records."""
+    monkeypatch.setenv("FTK_TC_SX", "1")
+    from paper_2408_01391_b200 import gemm as G
+    from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook
+
+    rng = np.random.default_rng(21)
+    x = np.ascontiguousarray(rng.standard_normal((2500, 640)), dtype=np.float32)
+    y = np.ascontiguousarray(rng.standard_normal((24, 640)), dtype=np.float32)
+    res, rep = P.checked_assign(x, y)
+    lab, val = O.assign(x, y)
+    assert np.array_equal(res.assignments, lab) and res.min_dists.tobytes() == val.tobytes()
+    assert rep.detections == 0 and E.tc_fallback_rows()[2] == 0
+    ents = [FaultEntry(0, (3, 0), (5, 7), 30), FaultEntry(0, (40, 0), (0, 23), 29),
+            FaultEntry(0, (78, 0), (3, 1), 27)]
+    outs = []
+    for variant in ("exact", "auto"):
+        old = G.get_variant()
+        G.set_variant(variant)
+        try:
+            h = ScheduledFaultHook(FaultSchedule(list(ents)))
+            r2, rep2 = P.checked_assign(x, y, hook=h)
+        finally:
+            G.set_variant(old)
+        outs.append((r2.assignments.tolist(), r2.min_dists.tobytes(),
+                     [(e.iteration, e.tile, e.kind, e.loc, e.delta) for e in rep2.events],
+                     h.injected))
+    assert outs[0] == outs[1]
+    assert len(outs[1][2]) >= 2
+
+
+@pytest.mark.parametrize("d,k", [(32, 64), (128, 16), (512, 16), (64, 200)])
+def test_tc_small_k_rows_certify(d, k, monkeypatch):
+    """K < 256 leaves whole 32-column chunks without a centroid; they must not
+    demote the running winner to runner-up (which failed every row's
+    certificate and sent the whole pass to the exact fallback)."""
+    monkeypatch.setenv("FTK_TC_SX", "1")  # d = 512 runs the streamed-X screen
+    x, _, _ = P.gaussian_mixture(20000, d, k, 0.25, precision="single", seed=0)
+    rng = np.random.default_rng(2)
+    y = np.ascontiguousarray(x[rng.choice(20000, k, replace=False)])
+    lab, val, fb = _tc(x, y)
+    ref_lab, ref_val = O.assign(x, y)
+    assert np.array_equal(lab, ref_lab)
+    assert val.tobytes() == ref_val.tobytes()
+    assert fb[0] < 0.05 * 20000, fb
