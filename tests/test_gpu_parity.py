@@ -331,6 +331,8 @@ def test_native_library_is_the_one_loaded():
     (40000, 96, 5, np.float32, True),       # few long chains: pipelined ordered chains
     (30000, 24, 7, np.float64, False),      # float64 data: pipelined ordered chains
     (200000, 8, 8192, np.float32, False),   # counting sort at its largest K (2 warps, 64 KB smem)
+    (120000, 64, 256, np.float64, False),   # float64: warp-specialised ordered chains (c4 shape)
+    (20000, 130, 9, np.float64, True),      # float64, partial last consumer warp, long chains
     (50000, 16, 9000, np.float32, True),    # K beyond the counting sort: radix-sort member lists
 ])
 def test_update_paths_bit_exact(m, d, k, dt, tiny):
