@@ -339,7 +339,7 @@ def run_ours(args, rank, world):
         wall = time.perf_counter() - t0
         e2e = {"value": r.iters / wall, "unit": "iter/s",
                "h2d_bytes_per_step": int(x.nbytes // max(r.iters, 1)),
-               "d2h_bytes_per_step": int(N_ROWS * 4 // max(r.iters, 1)),
+               "d2h_bytes_per_step": int(N_ROWS * 8 // max(r.iters, 1)),
                "iters": r.iters, "wall_s": wall}
     cpu = cpu_reference(x) if rank == 0 and world == 1 else None
     if rank != 0:

@@ -585,8 +585,14 @@ class LloydEngine:
         rep = A.finish(self.gemm_hook, iteration, inj)
         if rep is not None:
             self.report.merge(rep)
-        labels = E.to_host(A.labels[self.slot]).astype(np.int64)
-        return labels, max(0.0, float(self.ctl_f64[0].item()))
+        # int64 on the device, one D2H into page-locked memory (the pageable
+        # copy plus a host-side astype cost ~2 ms at c2)
+        t = self.t
+        lab64 = A.labels[self.slot].to(t.int64)
+        host = t.empty(lab64.shape[0], dtype=t.int64, pin_memory=True)
+        host.copy_(lab64, non_blocking=True)
+        inertia = max(0.0, float(self.ctl_f64[0].item()))  # synchronises the stream
+        return host.numpy(), inertia
 
 
 def lloyd(x, config, fault_spec=None):
@@ -605,6 +611,18 @@ def lloyd(x, config, fault_spec=None):
     E._torch()
     gemm_hook, update_hook = _plan_hooks(fault_spec, cfg, m, n, k, config.max_iters, dtype)
 
+    # a full cyclic-GC pass over the torch-sized heap stalls the launching
+    # thread for tens of ms; the fit allocates no reference cycles
+    gc_on = gc.isenabled()
+    gc.disable()
+    try:
+        return _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook)
+    finally:
+        if gc_on:
+            gc.enable()
+
+
+def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     timings = {"init_ns": 0, "assign_ns": 0, "update_ns": 0, "total_ns": 0}
     t_total = time.perf_counter_ns()
     t0 = time.perf_counter_ns()
@@ -616,10 +634,6 @@ def lloyd(x, config, fault_spec=None):
     history = []
     converged = False
     iters = 0
-    # a full cyclic-GC pass over the torch-sized heap stalls the launching
-    # thread for tens of ms; the loop allocates no reference cycles
-    gc_on = gc.isenabled()
-    gc.disable()
     try:
         for it in range(config.max_iters):
             inertia, unchanged, moved = eng.step(it)
@@ -633,8 +647,6 @@ def lloyd(x, config, fault_spec=None):
         labels, inertia = eng.final(iters)
         centroids = E.to_host(eng.cent)
     finally:
-        if gc_on:
-            gc.enable()
         eng.close()
     timings["total_ns"] = time.perf_counter_ns() - t_total
     return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,

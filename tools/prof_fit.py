@@ -20,6 +20,8 @@ x = bench.make_data()
 xp = torch.from_numpy(x).pin_memory()
 P.lloyd(xp[:4096], P.KMeansConfig(k=16, max_iters=2, init="random-sample"))
 graph = os.environ.get("GRAPH", "1") == "1"
+import gc
+gc.disable()
 for rep in range(3):
     torch.cuda.synchronize()
     T = [time.perf_counter()]
