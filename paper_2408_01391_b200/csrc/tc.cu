@@ -788,7 +788,7 @@ int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
     // kernel yet.  The resident-X kernels stop at 256.
     const char *sx = getenv("FTK_TC_SX");
     const bool sx_on = sx && atoi(sx) == 1;
-    return dtype == FTK_F32 && d >= 8 && d % 4 == 0 &&
+    return dtype == FTK_F32 && d >= 4 && d % 4 == 0 &&
            (d <= TC_MAX_D || (sx_on && k <= PAIR_BN && d <= TC_SX_MAX_D)) && k >= 1 && m >= 1 &&
            m < (int64_t(1) << 31) && k < (int64_t(1) << 24);
 }
@@ -1067,7 +1067,10 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             // centroid whose screened value can still beat the row's exact d1
             // is evaluated exactly; rows with too many candidates (or beyond
             // the pass-2 capacity) are resolved by exact_rows_kernel
-            const unsigned cap_rows = unsigned(std::min<int64_t>(m, std::max<int64_t>(65536, m / 8)));
+            // rows pass 2 can take (the rest go to the exact row kernel): an
+            // eighth of the rows, or 64 MB of gathered rows when D is small
+            const unsigned cap_rows = unsigned(std::min<int64_t>(
+                m, std::max<int64_t>(std::max<int64_t>(65536, m / 8), (int64_t(64) << 20) / (4 * d))));
             const unsigned row_cap = 256;
             const unsigned cap = unsigned(std::min<int64_t>(int64_t(cap_rows) * 16 + 65536, int64_t(1) << 30));
             const size_t gbytes = (sizeof(float) * size_t(cap_rows) * d + 255) & ~size_t(255);

@@ -29,7 +29,8 @@ def _tc(x, y):
 
 
 SHAPES = [(1000, 32, 64), (4096, 128, 1024), (333, 40, 70), (129, 8, 5), (2000, 256, 300),
-          (5000, 64, 16), (257, 12, 129), (1, 32, 1), (640, 100, 33), (3000, 200, 40)]
+          (5000, 64, 16), (257, 12, 129), (1, 32, 1), (640, 100, 33), (3000, 200, 40),
+          (3000, 4, 700), (2000, 4, 4096)]
 
 
 @pytest.mark.parametrize("m,d,k", SHAPES)
