@@ -56,18 +56,24 @@ def build(verbose=False, force=False):
     os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(ROOT, "include", "ftk_b200.h"))
-    objs = []
+    objs, jobs = [], []
     for src, extra in SOURCES.items():
         s = os.path.join(CSRC, src)
         o = os.path.join(LIBDIR, "obj", src.replace(".cu", ".o"))
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [nvcc(), *ARCH, *COMMON, *extra, "-c", s, "-o", o]
-            r = subprocess.run(cmd, capture_output=True, text=True)
-            if verbose or r.returncode:
-                sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-            if r.returncode:
-                raise RuntimeError(f"nvcc failed on {src}")
+            jobs.append((src, [nvcc(), *ARCH, *COMMON, *extra, "-c", s, "-o", o]))
+    # translation units compile in parallel (nvcc is single-threaded)
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda j: (j, subprocess.run(j[1], capture_output=True, text=True)),
+                              jobs))
+    for (src, cmd), r in results:
+        if verbose or r.returncode:
+            sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        if r.returncode:
+            raise RuntimeError(f"nvcc failed on {src}")
     if force or _stale(LIB, objs):
         cmd = [nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
