@@ -910,19 +910,33 @@ __global__ void pairwise_leaves_kernel(const double *a, const int64_t *leaf_star
 }
 
 // Internal nodes, level by level (height order), single block.
+// SM: the whole tree (leaf values, node values, child lists) is staged in
+// shared memory, so each of the ~log2(n/128) levels costs a shared-memory
+// round trip instead of an L2 one (c2: 15 -> ~3 us).
+template <bool SM>
 __global__ void pairwise_tree_kernel(double *vals, const int2 *nodes, const int64_t *level_start,
                                      int nlevels, int64_t nleaves, double *out) {
+    extern __shared__ __align__(16) unsigned char pt_smem[];
+    const int64_t nnodes = level_start[nlevels];
+    double *v = vals;
+    const int2 *nd = nodes;
+    if (SM) {
+        double *sv = reinterpret_cast<double *>(pt_smem);
+        int2 *sn = reinterpret_cast<int2 *>(sv + nleaves + nnodes);
+        for (int64_t i = threadIdx.x; i < nleaves; i += blockDim.x) sv[i] = vals[i];
+        for (int64_t i = threadIdx.x; i < nnodes; i += blockDim.x) sn[i] = nodes[i];
+        __syncthreads();
+        v = sv;
+        nd = sn;
+    }
     for (int L = 0; L < nlevels; ++L) {
         for (int64_t q = level_start[L] + threadIdx.x; q < level_start[L + 1]; q += blockDim.x) {
-            int2 ch = nodes[q];
-            vals[nleaves + q] = __dadd_rn(vals[ch.x], vals[ch.y]);
+            int2 ch = nd[q];
+            v[nleaves + q] = __dadd_rn(v[ch.x], v[ch.y]);
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        int64_t total = level_start[nlevels];
-        *out = total > 0 ? vals[nleaves + total - 1] : vals[0];
-    }
+    if (threadIdx.x == 0) *out = nnodes > 0 ? v[nleaves + nnodes - 1] : v[0];
 }
 
 // ---------------------------------------------------------- movement --
@@ -1437,7 +1451,20 @@ int pairwise_sum_run(ftk_ctx *ctx, const double *a, int64_t n, double *out, cuda
     int64_t threads = T->nleaves * 8;
     pairwise_leaves_kernel<<<unsigned((threads + 255) / 256), 256, 0, st>>>(a, T->d_leaf_start, T->nleaves, vals);
     FTK_LAUNCHED("pairwise_leaves_kernel");
-    pairwise_tree_kernel<<<1, 1024, 0, st>>>(vals, T->d_nodes, T->d_level_start, T->nlevels, T->nleaves, out);
+    const size_t tree_smem = sizeof(double) * size_t(T->nleaves + T->nnodes) + sizeof(int2) * size_t(T->nnodes) + 16;
+    if (tree_smem <= 200 * 1024) {
+        static bool attr = false;  // opt in to > 48 KB once
+        if (!attr) {
+            FTK_CUDA(cudaFuncSetAttribute(pairwise_tree_kernel<true>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        pairwise_tree_kernel<true><<<1, 1024, tree_smem, st>>>(vals, T->d_nodes, T->d_level_start,
+                                                               T->nlevels, T->nleaves, out);
+    } else {
+        pairwise_tree_kernel<false><<<1, 1024, 0, st>>>(vals, T->d_nodes, T->d_level_start, T->nlevels,
+                                                        T->nleaves, out);
+    }
     FTK_LAUNCHED("pairwise_tree_kernel");
     return FTK_OK;
 }
