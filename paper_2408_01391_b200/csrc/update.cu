@@ -369,14 +369,19 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
         const int64_t idx = t + lane;
         return (lane < CH_GROUP && idx < n) ? __ldg(perm + lo + idx) : 0;
     };
+    const T *xf = x + f;
     auto issue = [&](int64_t t, int32_t rows) {
+        // t is a multiple of CH_GROUP, which divides CH_RING: one slot base
+        // per group, and no per-member bound test for full groups
+        T(*slot)[32] = rb + int(t % CH_RING);
+        const bool full = t + CH_GROUP <= n;
 #pragma unroll
         for (int u = 0; u < CH_GROUP; ++u) {
             const int32_t row = __shfl_sync(0xffffffffu, rows, u);
-            const bool p = live && (t + u < n);
-            T *dst = &rb[(t + u) % CH_RING][lane];
-            if (sizeof(T) == 8) cp_async_8(dst, x + int64_t(row) * d + f, p);
-            else cp_async_4(dst, x + int64_t(row) * d + f, p);
+            const bool p = full ? live : (live && (t + u < n));
+            T *dst = &slot[u][lane];
+            if (sizeof(T) == 8) cp_async_8(dst, xf + int64_t(row) * d, p);
+            else cp_async_4(dst, xf + int64_t(row) * d, p);
         }
         cp_async_commit();
     };
@@ -400,15 +405,23 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
         cp_async_wait<NG - 1>();  // group of rows [t, t + CH_GROUP) landed
         __syncwarp();
         const int cnt = int(n - t < CH_GROUP ? n - t : CH_GROUP);
-        double v[CH_GROUP];
+        const T(*slot)[32] = rb + int(t % CH_RING);
+        if (cnt == CH_GROUP) {
+            if (live) {  // full group: no per-member tests
+                double v[CH_GROUP];
 #pragma unroll
-        for (int u = 0; u < CH_GROUP; ++u)
-            v[u] = (live && u < cnt) ? double(rb[(t + u) % CH_RING][lane]) : 0.0;
+                for (int u = 0; u < CH_GROUP; ++u) v[u] = double(slot[u][lane]);
 #pragma unroll
-        for (int u = 0; u < CH_GROUP; ++u) {
-            if (u < cnt) {
-                acc_a = __dadd_rn(acc_a, v[u]);
-                if (DMR) acc_b = __dadd_rn(acc_b, v[u]);
+                for (int u = 0; u < CH_GROUP; ++u) {
+                    acc_a = __dadd_rn(acc_a, v[u]);
+                    if (DMR) acc_b = __dadd_rn(acc_b, v[u]);
+                }
+            }
+        } else if (live) {
+            for (int u = 0; u < cnt; ++u) {
+                const double v = double(slot[u][lane]);
+                acc_a = __dadd_rn(acc_a, v);
+                if (DMR) acc_b = __dadd_rn(acc_b, v);
             }
         }
         __syncwarp();  // slots of this group are refilled next iteration
