@@ -366,6 +366,7 @@ class LloydEngine:
         self.counts_buf = t.zeros(k, dtype=t.int64, device=dev)
         self._pool = None
         self._cap_stream = None
+        self._side = None  # graph branch: inertia + label compare
 
     def _graph_ok(self, it):
         """Graph replay is used from the second step on: clean steps replay
@@ -390,14 +391,23 @@ class LloydEngine:
         A.run(self.cent, yn, NOOP_HOOK, it, self.slot, sinj=sinj)
         if sinj is not None:
             sinj.copy_back()
-        E.sq_dists_dev(A.md, self.xsq, self.sq)
-        E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
-        E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
+        # inertia and the label compare only read the assignment: a graph
+        # branch on a side stream, concurrent with the update chain
+        cur = self.t.cuda.current_stream()
+        if self._side is None:
+            self._side = self.t.cuda.Stream()
+        side = self._side
+        side.wait_stream(cur)
+        with self.t.cuda.stream(side):
+            E.sq_dists_dev(A.md, self.xsq, self.sq)
+            E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
+            E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
         sa, ca, _, _ = E.update_sums_dev(self.x_t, A.labels[self.slot], self.k, dmr=False)
         new_cent = self.cent_buf[1 - self.cbuf]
         E.finalize_dev(sa, ca, self.dtype, out=new_cent, n_empty=self.ctl_i32[1:2])
         self.counts_buf.copy_(ca)
         E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+        cur.wait_stream(side)
         self.ctl_host.copy_(self.ctl_f64, non_blocking=True)
         self.ctl_i32_host.copy_(self.ctl_i32, non_blocking=True)
         if A.checked:
