@@ -1103,6 +1103,13 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
                                           rows1, cnt, cap_rows, out_idx, outv, rows2, ccount + 1, st)))
                 return rc;
             if ((rc = exact_rows_run(xf, yf, ynf, k, d, rows2, ccount + 1, out_idx, outv, st))) return rc;
+            if (getenv("FTK_TC_P2_DEBUG")) {  // diagnostics: pass-2 rows and candidates
+                unsigned h[3] = {0, 0, 0};
+                cudaMemcpyAsync(h, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+                cudaMemcpyAsync(h + 1, ccount, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                fprintf(stderr, "pass 2: %u rows, %u candidates, %u rows to the exact kernel\n", h[0], h[1], h[2]);
+            }
             ctx->stat_dev[0] = cnt;          // read lazily by tc_last_fallback
             ctx->stat_dev[1] = ccount + 1;
             ctx->stat_dev[2] = ft ? cnt + 2 : nullptr;

@@ -297,6 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     // pass 2: every column whose screened value can still beat
                     // the row's threshold becomes an exact-evaluation candidate
                     uint32_t va[32];
+                    int nloc = 0, lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0;
 #pragma unroll 1
                     for (int ch = 0; ch < HALF / 32; ++ch) {
                         tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
@@ -313,12 +314,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
                                 if (d[u] <= thr && c0 + ch * 32 + 4 * q + u < P.k) {
-                                    const unsigned slot = atomicAdd(P.cand_count, 1u);
+                                    const int col = int(c0) + ch * 32 + 4 * q + u;
                                     ++ncand;  // row count: one atomic per row and warpgroup
-                                    if (slot < P.cand_cap)
-                                        P.cand[slot] = make_int2(int(grow), int(c0) + ch * 32 + 4 * q + u);
+                                    // the first few per thread wait in registers for one
+                                    // warp-wide append per tile (~2 candidates per row at c2:
+                                    // a same-address atomic each would serialise in L2)
+                                    if (nloc < 4) {
+                                        lc0 = nloc == 0 ? col : lc0;
+                                        lc1 = nloc == 1 ? col : lc1;
+                                        lc2 = nloc == 2 ? col : lc2;
+                                        lc3 = nloc == 3 ? col : lc3;
+                                        ++nloc;
+                                    } else {
+                                        const unsigned slot = atomicAdd(P.cand_count, 1u);
+                                        if (slot < P.cand_cap) P.cand[slot] = make_int2(int(grow), col);
+                                    }
                                 }
                         }
+                    }
+                    // one append per warp for the tile's register-held candidates
+                    int incl = nloc;
+#pragma unroll
+                    for (int off = 1; off < 32; off <<= 1) {
+                        const int o = __shfl_up_sync(0xffffffffu, incl, off);
+                        if (lane >= off) incl += o;
+                    }
+                    const int total = __shfl_sync(0xffffffffu, incl, 31);
+                    if (total) {
+                        unsigned base = 0;
+                        if (lane == 31) base = atomicAdd(P.cand_count, unsigned(total));
+                        base = __shfl_sync(0xffffffffu, base, 31) + unsigned(incl - nloc);
+                        const int cols[4] = {lc0, lc1, lc2, lc3};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            if (i < nloc && base + i < P.cand_cap)
+                                P.cand[base + i] = make_int2(int(grow), cols[i]);
                     }
                 } else if (!(P.dbg & 1)) {
                     // software-pipelined TMEM drain, two 32-column chunks per
