@@ -239,8 +239,11 @@ def run_ours(args, rank, world):
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
         l0 = _native.launch_count()
         evs[0].record()
+        last = warmup + steps
         for i, it in enumerate(range(warmup + 1, warmup + 1 + steps)):
-            eng.step(it)
+            # graph steps keep one replay queued ahead, never past the last timed
+            # step; per-step event gaps are then approximate, the total is exact
+            eng.step(it, more=(lambda it=it: it < last))
             evs[i + 1].record()
         torch.cuda.synchronize()
         launches = _native.launch_count() - l0
@@ -291,7 +294,7 @@ def run_ours(args, rank, world):
         with ClockSampler(torch.cuda.current_device()) as ccs:
             cst.record()
             for it in range(1, c_iters + 1):
-                c_eng.step(it)
+                c_eng.step(it, more=(lambda it=it: it < c_iters))
             cen.record()
             torch.cuda.synchronize()
         gc.enable()

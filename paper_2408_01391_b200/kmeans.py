@@ -261,12 +261,22 @@ class _DeviceAssign:
         self.delta_rel, self.abs_tol = (thr.kernel_params() if thr is not None else (0.0, 0.0))
         self.nbi = (m + cfg.block[0] - 1) // cfg.block[0]
         self.threads = threads
-        self.md = t.empty(m, dtype=x_t.dtype, device=x_t.device)
+        # per buffer parity: min_dists and the event ring, so the next step can
+        # run while the host still reads this one's (LloydEngine._graph_step)
+        self._md = [t.empty(m, dtype=x_t.dtype, device=x_t.device) for _ in range(2)]
         self.labels = [t.empty(m, dtype=t.int32, device=x_t.device) for _ in range(2)]
         mult = max(1, min(threads, self.nbi))
         # storage for a few hundred injected flips per pass, so eager injected
         # steps do not move the ring that captured graph replays write into
-        self.events = E.DevEvents(64 * mult, storage=(64 + 256) * mult) if self.checked else None
+        self._rings = [E.DevEvents(64 * mult, storage=(64 + 256) * mult) if self.checked else None
+                       for _ in range(2)]
+        self.bind(0)
+
+    def bind(self, par):
+        self.md, self.events = self._md[par], self._rings[par]
+
+    def ring_gen(self):
+        return sum(r.gen for r in self._rings) if self.checked else 0
 
     def run(self, cent_t, yn_t, hook, iteration, slot, sinj=None):
         """`sinj`: a StaticInjection (device-count schedule, graph capture)
@@ -328,12 +338,12 @@ class LloydEngine:
         dev = x_t.device
         self.xsq = E.row_sq_norms_dev(x_t).to(t.float64)
         self.rows = E.RowInfo(x_t)  # per-fit screening bounds (X is constant)
-        self.sq = t.empty(m, dtype=t.float64, device=dev)
+        self._sq = [t.empty(m, dtype=t.float64, device=dev) for _ in range(2)]
         self.ctl_f64 = t.zeros(4, dtype=t.float64, device=dev)   # inertia, moved
         self.ctl_i32 = t.zeros(8, dtype=t.int32, device=dev)     # equal, n_empty, dmr flag
-        self.ctl_host = t.zeros(4, dtype=t.float64).pin_memory()
-        self.ctl_i32_host = t.zeros(8, dtype=t.int32).pin_memory()
-        self.evc_host = t.zeros(1, dtype=t.int64).pin_memory()  # detection-event count
+        self._ctl_host = [t.zeros(4, dtype=t.float64).pin_memory() for _ in range(2)]
+        self._ctl_i32_host = [t.zeros(8, dtype=t.int32).pin_memory() for _ in range(2)]
+        self._evc_host = [t.zeros(1, dtype=t.int64).pin_memory() for _ in range(2)]  # event count
         self.cent = E.to_dev(c0) if not _is_torch(c0) else c0.to(dev).contiguous()
         self.eps = float(np.finfo(self.dtype).eps)
         self.A = _DeviceAssign(x_t, m, k, self.dtype, cfg, ft_mode,
@@ -357,16 +367,28 @@ class LloydEngine:
         self.sinj = E.StaticInjection(64) if self.use_graph and self.A.checked and \
             getattr(gemm_hook, "schedule", None) is not None else None
         self.inj_graphs = [None, None]
-        self.graph_gen = self.A.events.gen if self.A.checked else 0
+        self.graph_gen = self.A.ring_gen()
         self.ctx_gen = None
         self.cent_buf = [t.empty_like(self.cent), t.empty_like(self.cent)]
         self.cent_buf[0].copy_(self.cent)
         self.cent = self.cent_buf[0]
         self.cbuf = 0
-        self.counts_buf = t.zeros(k, dtype=t.int64, device=dev)
+        self._counts_buf = [t.zeros(k, dtype=t.int64, device=dev) for _ in range(2)]
+        self._done = [t.cuda.Event(), t.cuda.Event()]  # end of the last replay, per parity
+        self._ahead = None  # iteration already replayed ahead of its step() call
+        self._cent_prev = None
+        self.bind(0)
         self._pool = None
         self._cap_stream = None
         self._side = None  # graph branch: inertia + label compare
+
+    def bind(self, par):
+        """Point the per-parity buffers (min_dists, sq_dists, counts, event
+        ring, pinned control block) at parity `par`."""
+        self.A.bind(par)
+        self.sq, self.counts_buf = self._sq[par], self._counts_buf[par]
+        self.ctl_host, self.ctl_i32_host = self._ctl_host[par], self._ctl_i32_host[par]
+        self.evc_host = self._evc_host[par]
 
     def _graph_ok(self, it):
         """Graph replay is used from the second step on: clean steps replay
@@ -434,6 +456,7 @@ class LloydEngine:
                     continue
                 self.slot = self.cbuf = par
                 self.cent = self.cent_buf[par]
+                self.bind(par)
                 g = t.cuda.CUDAGraph()
                 l0 = N.launch_count()
                 try:
@@ -444,10 +467,12 @@ class LloydEngine:
                     self.use_graph = False
                     N.load().ftk_add_launches(-(N.launch_count() - l0))
                     self.slot, self.cbuf, self.cent = state
+                    self.bind(self.slot)
                     return False
                 store[par] = (g, N.launch_count() - l0)
                 N.load().ftk_add_launches(-store[par][1])  # captured, not run
         self.slot, self.cbuf, self.cent = state
+        self.bind(self.slot)
         if E.ctx_generation() != gen0:  # a capture grew a scratch buffer: redo
             self._drop_graphs()
             return False
@@ -489,47 +514,95 @@ class LloydEngine:
         self.graphs = [None, None]
         self.inj_graphs = [None, None]
 
-    def _graph_step(self, it):
+    def _can_run_ahead(self, it):
+        """Step `it` may be replayed before the host has read the previous
+        step: a clean graph step whose graph is ready and current."""
+        if not self._graph_ok(it) or self.graphs[1 - self.slot] is None:
+            return False
+        sched = getattr(self.gemm_hook, "schedule", None)
+        if sched is not None and sched.for_iteration(it):
+            return False
+        if self.A.ring_gen() != self.graph_gen:
+            return False
+        return self.ctx_gen is not None and E.ctx_generation() == self.ctx_gen
+
+    def _graph_step(self, it, more=None):
         t, A = self.t, self.A
-        if (A.checked and A.events.gen != self.graph_gen) or \
-                (self.ctx_gen is not None and E.ctx_generation() != self.ctx_gen):
-            self._drop_graphs()  # the event ring or a scratch buffer moved: recapture
-            self.graph_gen = A.events.gen if A.checked else 0
-            self.ctx_gen = None
-        arrs = None
-        if self.sinj is not None:
-            arrs = self.gemm_hook.kernel_arrays(it, self.dtype)
-        store, inj = self.graphs, None
-        if arrs is not None and len(arrs[0]):
-            store, inj = self.inj_graphs, self.sinj
-        if store[self.slot] is None and not self._capture(it):
-            return self.step(it, eager=True)
-        if inj is not None:
-            inj.load(arrs)  # stream-ordered before the replay
-        g, nk = store[self.slot]
-        g.replay()
-        N.load().ftk_add_launches(nk)
-        t.cuda.current_stream().synchronize()
-        rep = A.finish(self.gemm_hook, it, inj,
-                       n_events=int(self.evc_host[0]) if A.checked else None, replayed=True)
+        self.bind(self.slot)
+        inj = None
+        if self._ahead == it:
+            self._ahead = None  # already replayed behind the previous step
+        else:
+            self._ahead = None
+            if (A.checked and A.ring_gen() != self.graph_gen) or \
+                    (self.ctx_gen is not None and E.ctx_generation() != self.ctx_gen):
+                self._drop_graphs()  # the event ring or a scratch buffer moved: recapture
+                self.graph_gen = A.ring_gen()
+                self.ctx_gen = None
+            arrs = None
+            if self.sinj is not None:
+                arrs = self.gemm_hook.kernel_arrays(it, self.dtype)
+            store = self.graphs
+            if arrs is not None and len(arrs[0]):
+                store, inj = self.inj_graphs, self.sinj
+            if store[self.slot] is None and not self._capture(it):
+                return self.step(it, eager=True)
+            self.bind(self.slot)
+            if inj is not None:
+                inj.load(arrs)  # stream-ordered before the replay
+            g, nk = store[self.slot]
+            g.replay()
+            N.load().ftk_add_launches(nk)
+            self._done[self.slot].record()
+        # one step queued ahead: the next replay (the other parity's buffers)
+        # goes out before the host reads this step, so the GPU does not idle
+        # through the host turnaround.  If this step turns out to be the last,
+        # the extra replay only touched buffers nothing reads any more.
+        if more is not None and inj is None and self._can_run_ahead(it + 1) and more():
+            # the queued step overwrites this step's input centroids; keep a
+            # copy for a host-side reseed (movement against the old centroids)
+            if self._cent_prev is None:
+                self._cent_prev = t.empty_like(self.cent)
+            self._cent_prev.copy_(self.cent, non_blocking=True)
+            g, nk = self.graphs[1 - self.slot]
+            g.replay()
+            N.load().ftk_add_launches(nk)
+            self._done[1 - self.slot].record()
+            self._ahead = it + 1
+        self._done[self.slot].synchronize()
+        n_ev = int(self.evc_host[0]) if A.checked else None
+        rep = A.finish(self.gemm_hook, it, inj, n_events=n_ev, replayed=True)
         if rep is not None:
             self.report.merge(rep)
         new_cent = self.cent_buf[1 - self.cbuf]
         if int(self.ctl_i32_host[1]):
+            old = self.cent
+            if self._ahead is not None:
+                # the queued step read the centroids before this reseed: rerun it
+                t.cuda.current_stream().synchronize()
+                self._ahead = None
+                old = self._cent_prev
             E.reseed_dev(self.x_t, self.counts_buf, self.sq, new_cent)
-            E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
-            self.ctl_host.copy_(self.ctl_f64)
+            E.movement_dev(new_cent, old, self.eps, self.ctl_f64[1:2])
+            # movement only: ctl_f64[0] may already hold the queued step's inertia
+            self.ctl_host[1:2].copy_(self.ctl_f64[1:2])
         unchanged = bool(int(self.ctl_i32_host[0]))
         self.cbuf = 1 - self.cbuf
         self.cent = self.cent_buf[self.cbuf]
         self.slot = 1 - self.slot
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
 
-    def step(self, it, eager=False):
+    def step(self, it, eager=False, more=None):
         """One Lloyd iteration; returns (inertia, unchanged, moved).  Eager
-        steps also record the phase timings (assign_ms / update_ms)."""
-        if not eager and self._graph_ok(it) and self.slot == self.cbuf:
-            return self._graph_step(it)
+        steps also record the phase timings (assign_ms / update_ms).
+        `more()`: the caller may run step it+1 (lets graph steps keep one
+        replay queued ahead)."""
+        if self._ahead is not None and (self._ahead != it or eager):
+            self.t.cuda.current_stream().synchronize()  # a queued replay nobody reads
+            self._ahead = None
+        if not eager and (self._ahead == it or (self._graph_ok(it) and self.slot == self.cbuf)):
+            return self._graph_step(it, more)
+        self.bind(self.slot)
         t, A, ev = self.t, self.A, self.ev
         ev[0].record()
         yn = E.row_sq_norms_dev(self.cent)
@@ -587,6 +660,8 @@ class LloydEngine:
 
     def final(self, iteration):
         """Final assignment against the current centroids -> (labels, inertia)."""
+        self._ahead = None  # a queued replay runs before this, on buffers final() does not read
+        self.bind(self.slot)
         A = self.A
         yn = E.row_sq_norms_dev(self.cent)
         inj = A.run(self.cent, yn, self.gemm_hook, iteration, self.slot)
@@ -646,7 +721,8 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     iters = 0
     try:
         for it in range(config.max_iters):
-            inertia, unchanged, moved = eng.step(it)
+            more = (lambda it=it: it + 1 < config.max_iters)
+            inertia, unchanged, moved = eng.step(it, more=more)
             timings["assign_ns"] += int(eng.assign_ms * 1e6)
             timings["update_ns"] += int(eng.update_ms * 1e6)
             history.append(inertia)

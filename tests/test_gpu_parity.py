@@ -436,3 +436,33 @@ def test_graph_replay_with_injections_equals_eager():
     assert runs[0][2] == runs[1][2]
     assert len(runs[0][2]) >= 4
     assert runs[0][3] == runs[1][3]
+
+
+@pytest.mark.parametrize("ft", ["off", "abft"])
+def test_run_ahead_steps_equal_plain_steps(ft):
+    """Graph steps with one replay queued ahead (more=...) give the plain
+    steps' bits: per-step outputs, centroids, detections and hook records,
+    with scheduled flips interleaved and an empty-cluster reseed (which
+    discards and reruns the queued step)."""
+    from paper_2408_01391_b200 import _engine as E
+    from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    x, _, _ = P.gaussian_mixture(30000, 64, 96, 0.3, precision="single", seed=5)
+    x_t = E.to_dev(x)
+    c0 = P.init_centroids(x, 96, seed=3, method="random-sample")
+    c0[5] = 1e6  # a far centroid: empty at step 0, reseeded on the host
+    ents = [FaultEntry(3, (7, 0), (2, 9), 30), FaultEntry(6, (100, 0), (1, 50), 29)]
+    runs = []
+    for ahead in (False, True):
+        hook = ScheduledFaultHook(FaultSchedule(list(ents))) if ft == "abft" else P.FaultHook()
+        eng = LloydEngine(x_t, c0, 96, np.float32, P.default_config(np.float32), ft,
+                          P.Threshold.default_for(np.float32), 8, gemm_hook=hook, graph=True)
+        outs = [eng.step(it, more=(lambda it=it: it + 1 < 14) if ahead else None)
+                for it in range(14)]
+        evs = [(e.iteration, e.tile, e.kind, e.loc, e.delta) for e in eng.report.events]
+        lab, inertia = eng.final(14)
+        runs.append((outs, E.to_host(eng.cent).tobytes(), evs,
+                     getattr(hook, "injected", None), lab.tolist(), inertia))
+        eng.close()
+    assert runs[0] == runs[1]
