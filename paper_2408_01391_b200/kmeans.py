@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import dataclasses
 import gc
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -720,8 +721,9 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     converged = False
     iters = 0
     try:
+        ahead = os.environ.get("FTK_RUN_AHEAD", "1") != "0"  # A/B knob
         for it in range(config.max_iters):
-            more = (lambda it=it: it + 1 < config.max_iters)
+            more = (lambda it=it: it + 1 < config.max_iters) if ahead else None
             inertia, unchanged, moved = eng.step(it, more=more)
             timings["assign_ns"] += int(eng.assign_ms * 1e6)
             timings["update_ns"] += int(eng.update_ms * 1e6)
