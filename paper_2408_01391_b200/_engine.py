@@ -61,12 +61,13 @@ def ptr(t):
     return None if t is None else (t.data_ptr() or None)
 
 
-def to_dev(a, dtype=None):
-    """numpy / torch (any device) -> contiguous CUDA tensor."""
+def to_dev(a, dtype=None, copy=False):
+    """numpy / torch (any device) -> contiguous CUDA tensor (`copy`: never
+    alias a CUDA input, e.g. for a buffer that outlives the call)."""
     t = _torch()
     if isinstance(a, t.Tensor):
         out = a.to(device=device(), dtype=tdtype(dtype) if dtype is not None else a.dtype,
-                   non_blocking=True)
+                   non_blocking=True, copy=copy)
         return out.contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype)
     return t.from_numpy(arr).to(device(), non_blocking=False)
@@ -270,6 +271,17 @@ class RowInfo:
         N.check(lib.ftk_row_info(ctx(), ptr(x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
         N.check(lib.ftk_ctx_set_rows(ctx(), ptr(x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
         _ROWS_OWNER[x_t.device.index] = id(self)
+
+    def refresh(self):
+        """Recompute the bounds in place after x_t's contents changed (same
+        buffers, so captured graphs stay valid) and register them again."""
+        if self.info is None:
+            return
+        m, d = self.x_t.shape
+        lib = N.load()
+        N.check(lib.ftk_row_info(ctx(), ptr(self.x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
+        N.check(lib.ftk_ctx_set_rows(ctx(), ptr(self.x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
+        _ROWS_OWNER[self.x_t.device.index] = id(self)
 
     def close(self):
         if self.info is not None:

@@ -504,6 +504,27 @@ class LloydEngine:
         if self._pool is None:
             self._pool = g.pool()
 
+    def reset(self, x, c0, gemm_hook=NOOP_HOOK, update_hook=NOOP_HOOK):
+        """Start a new fit of the same shape on this engine: X copied into the
+        resident buffer, per-fit row bounds and ||x||^2 recomputed in place,
+        centroids and step state reset.  Every buffer keeps its address, so
+        the captured step graphs are reused (no allocation, no capture)."""
+        t = self.t
+        if self._ahead is not None:
+            t.cuda.current_stream().synchronize()
+            self._ahead = None
+        src = x if _is_torch(x) else t.from_numpy(np.ascontiguousarray(x))
+        self.x_t.copy_(src, non_blocking=True)
+        self.xsq.copy_(E.row_sq_norms_dev(self.x_t).to(t.float64))
+        self.rows.refresh()
+        self.cent_buf[0].copy_(E.to_dev(c0) if not _is_torch(c0) else c0)
+        self.cbuf = self.slot = 0
+        self.cent = self.cent_buf[0]
+        self.bind(0)
+        self.gemm_hook, self.update_hook = gemm_hook, update_hook
+        self.report = DetectionReport()
+        self.assign_ms = self.update_ms = 0.0
+
     def warm_graphs(self, it=1):
         """Capture the step graphs now (they are otherwise captured at the
         first graph-eligible step); a no-op when graphs are off or ready."""
@@ -708,6 +729,35 @@ def lloyd(x, config, fault_spec=None):
             gc.enable()
 
 
+# One resident fit workspace (the most recent shape): repeated fits of the same
+# shape reuse its buffers and captured graphs (tools/prof_lloyd_e2e.py).
+_FIT_CACHE = {}
+
+
+def _fit_cache_clear():
+    eng = _FIT_CACHE.pop("eng", None)
+    _FIT_CACHE.pop("key", None)
+    if eng is not None:
+        eng.close()
+
+
+def clear_fit_cache():
+    """Release the resident fit workspace (device memory of the last shape)."""
+    _fit_cache_clear()
+
+
+def _fit_key(x, k, dtype, cfg, ft_mode, threads, gemm_hook, update_hook, graph, thr):
+    """Cache key of a reusable workspace, or None (graph steps only, no
+    update-site hook; FTK_FIT_CACHE=0 disables)."""
+    if not graph or update_hook is not NOOP_HOOK or os.environ.get("FTK_FIT_CACHE", "1") == "0":
+        return None
+    sched = getattr(gemm_hook, "schedule", None) is not None
+    dev = E._torch().cuda.current_device()
+    return (dev, tuple(x.shape), int(k), np.dtype(dtype).str, ft_mode, tuple(cfg.block), int(threads),
+            sched, type(gemm_hook).__name__, get_variant(),
+            tuple(thr.kernel_params()) if ft_mode != "off" else None)
+
+
 def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     timings = {"init_ns": 0, "assign_ns": 0, "update_ns": 0, "total_ns": 0}
     t_total = time.perf_counter_ns()
@@ -715,8 +765,18 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     c0 = init_centroids(x, k, seed=config.seed, method=config.init)
     timings["init_ns"] = time.perf_counter_ns() - t0
 
-    eng = LloydEngine(E.to_dev(x), c0, k, dtype, cfg, config.ft_mode, thr, threads, gemm_hook,
-                      update_hook, graph=config.max_iters >= 8)
+    graph = config.max_iters >= 8
+    key = _fit_key(x, k, dtype, cfg, config.ft_mode, threads, gemm_hook, update_hook, graph, thr)
+    eng = None
+    if key is not None and _FIT_CACHE.get("key") == key:
+        eng = _FIT_CACHE["eng"]
+        eng.reset(x, c0, gemm_hook, update_hook)
+    else:
+        _fit_cache_clear()
+        eng = LloydEngine(E.to_dev(x, copy=key is not None), c0, k, dtype, cfg, config.ft_mode, thr,
+                          threads, gemm_hook, update_hook, graph=graph)
+        if key is not None:
+            _FIT_CACHE.update(key=key, eng=eng)
     history = []
     converged = False
     iters = 0
@@ -735,7 +795,8 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
         labels, inertia = eng.final(iters)
         centroids = E.to_host(eng.cent)
     finally:
-        eng.close()
+        if key is None:
+            eng.close()
     timings["total_ns"] = time.perf_counter_ns() - t_total
     return KMeansResult(centroids=centroids, assignments=labels, inertia=inertia, iters=iters,
                         converged=converged, report=eng.report, timings=timings,

@@ -466,3 +466,30 @@ def test_run_ahead_steps_equal_plain_steps(ft):
                      getattr(hook, "injected", None), lab.tolist(), inertia))
         eng.close()
     assert runs[0] == runs[1]
+
+
+@pytest.mark.parametrize("ft,inject", [("off", None), ("abft", "prob:0.02@exp")])
+def test_fit_workspace_reuse_equals_fresh(ft, inject, monkeypatch):
+    """Back-to-back fits of one shape reuse the resident workspace (buffers and
+    captured graphs): each result equals a fit on a fresh engine."""
+    from paper_2408_01391_b200 import kmeans as K
+
+    xs = [P.gaussian_mixture(6000, 32, 20, 0.3, precision="single", seed=s)[0] for s in (1, 2, 3)]
+    cfg = P.KMeansConfig(k=20, max_iters=12, tol=0.0, seed=4, init="random-sample", ft_mode=ft)
+
+    def fits():
+        out = []
+        for x in xs:
+            r = P.lloyd(x, cfg, fault_spec=inject)
+            out.append((r.assignments.tolist(), r.centroids.tobytes(), r.inertia, r.iters,
+                        r.inertia_history, [(e.iteration, e.tile, e.kind, e.loc, e.delta)
+                                            for e in r.report.events]))
+        return out
+
+    K.clear_fit_cache()
+    cached = fits()
+    assert K._FIT_CACHE.get("eng") is not None
+    monkeypatch.setenv("FTK_FIT_CACHE", "0")
+    K.clear_fit_cache()
+    fresh = fits()
+    assert cached == fresh
