@@ -1146,8 +1146,6 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     // segment table of the certified segmented sums)
     const bool dmr = sums_b != nullptr;
     const int64_t nwarps = k * ((d + 31) / 32);
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     // float64 data: every partial sum rounds (full 53-bit values), so the
     // reference's ordered chain runs as is; float32: certified segments,
     // whatever the chain count (measured faster at c1, c3 and c2)
@@ -1466,12 +1464,9 @@ int pairwise_sum_run(ftk_ctx *ctx, const double *a, int64_t n, double *out, cuda
     FTK_LAUNCHED("pairwise_leaves_kernel");
     const size_t tree_smem = sizeof(double) * size_t(T->nleaves + T->nnodes) + sizeof(int2) * size_t(T->nnodes) + 16;
     if (tree_smem <= 200 * 1024) {
-        static bool attr = false;  // opt in to > 48 KB once
-        if (!attr) {
-            FTK_CUDA(cudaFuncSetAttribute(pairwise_tree_kernel<true>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
-        }
+        // opt in to > 48 KB (per call: cheap, and right for every device)
+        FTK_CUDA(cudaFuncSetAttribute(pairwise_tree_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         pairwise_tree_kernel<true><<<1, 1024, tree_smem, st>>>(vals, T->d_nodes, T->d_level_start,
                                                                T->nlevels, T->nleaves, out);
     } else {
