@@ -198,6 +198,12 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
  * certify (resolved by the exact kernel). */
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream);
 
+/* Diagnostics: cumulative count of rows whose tensor-core / DMMA row
+ * checksum failed (every screened checked assignment on this context since
+ * the last reset; *out = 0 before the first).  reset != 0 zeroes it after
+ * the read.  Synchronises `stream`. */
+int ftk_abft_flags_total(ftk_ctx *ctx, int64_t *out, int reset, void *stream);
+
 /* Diagnostics: device time (CUDA events on the launching stream) of the
  * last tensor-core screen launch (the CTA-pair pass-1 kernel), in ms; -1 if
  * the last TC assignment did not use it. */

@@ -175,6 +175,160 @@ void ftko_assign_f64(const double *x, const double *y, const double *yn, int64_t
     run_rows(assign_f64_worker, J, threads);
 }
 
+/* ------------------------------------------------------- checked assign -- */
+/* The reference's checksum-protected fused assignment, DETECTION ONLY
+ * (_kernels.py:479-612 with _encode_c1_amax 158-180, _apply_col_refs 128-137,
+ * _tile_colsums 183-202 and _block_absmax 117-125): per logical tile
+ * (bm x bn) and k-interval (bk) the e1 column references
+ * ref1[j] += sum_k (e1' X_blk)[k] * C[j][k] (f64) are compared with the
+ * column sums of the accumulator tile (4-row pre-reduction in the data
+ * dtype, then f64) under tol = delta_rel * max(1, amax_X * amax_C) * k_acc
+ * + abs_tol.  The accumulators and the argmin are the unprotected ones
+ * (bit-identical labels), so this is the reference's fault-free ABFT cost;
+ * violations are only counted (no flips are injected on this path, and
+ * _diagnose is not restated), and the caller raises if any occur. */
+typedef struct {
+    const void *x, *y, *yn;
+    int64_t m, k, d, bm, bn, bk, lo, hi;  /* lo/hi: row BLOCKS */
+    double delta_rel, abs_tol;
+    const double *cmax;  /* per column block: max |C| */
+    int64_t *idx;
+    void *val;
+    int64_t viol;
+} chk_job;
+
+#define DEFINE_CHECKED(T, NAME)                                                              \
+static void *NAME(void *arg) {                                                               \
+    chk_job *J = (chk_job *)arg;                                                             \
+    const T *x = J->x, *y = J->y, *yn = J->yn;                                               \
+    const int64_t k = J->k, d = J->d, bm = J->bm, bn = J->bn, bk = J->bk;                    \
+    const int64_t nbk = (d + bk - 1) / bk;                                                   \
+    T *bt = malloc(sizeof(T) * d * OBN);                                                     \
+    T *acc = malloc(sizeof(T) * bm * OBN);                                                   \
+    double *c1 = malloc(sizeof(double) * nbk * bk);                                          \
+    double ref1[OBN], s1[OBN];                                                               \
+    T p[OBN];                                                                                \
+    for (int64_t bi = J->lo; bi < J->hi; ++bi) {                                             \
+        const int64_t i0 = bi * bm, mi = J->m - i0 < bm ? J->m - i0 : bm;                    \
+        double amax = 0.0;                                                                   \
+        for (int64_t q = 0; q < nbk * bk; ++q) c1[q] = 0.0;                                  \
+        for (int64_t i = 0; i < mi; ++i)                                                     \
+            for (int64_t f = 0; f < d; ++f) {                                                \
+                const double v = (double)x[(i0 + i) * d + f];                                \
+                c1[f] += v;                                                                  \
+                const double av = v < 0.0 ? -v : v;                                          \
+                if (av > amax) amax = av;                                                    \
+            }                                                                                \
+        for (int64_t i = 0; i < mi; ++i) {                                                   \
+            ((T *)J->val)[i0 + i] = (T)INFINITY;                                             \
+            J->idx[i0 + i] = 0;                                                              \
+        }                                                                                    \
+        for (int64_t j0 = 0; j0 < k; j0 += bn) {                                             \
+            const int64_t nj = k - j0 < bn ? k - j0 : bn;                                    \
+            double scale = amax * J->cmax[j0 / bn];                                          \
+            if (scale < 1.0) scale = 1.0;                                                    \
+            const double tol_base = J->delta_rel * scale;                                    \
+            for (int64_t s0 = j0; s0 < j0 + nj; s0 += OBN) {                                 \
+                const int64_t sn = j0 + nj - s0 < OBN ? j0 + nj - s0 : OBN;                  \
+                for (int64_t f = 0; f < d; ++f)                                              \
+                    for (int64_t j = 0; j < OBN; ++j)                                        \
+                        bt[f * OBN + j] = j < sn ? y[(s0 + j) * d + f] : (T)0;               \
+                for (int64_t q = 0; q < mi * OBN; ++q) acc[q] = (T)0;                        \
+                for (int64_t j = 0; j < OBN; ++j) ref1[j] = 0.0;                             \
+                for (int64_t t = 0; t < nbk; ++t) {                                          \
+                    const int64_t k0 = t * bk, kk = d - k0 < bk ? d - k0 : bk;               \
+                    for (int64_t i = 0; i < mi; ++i) {                                       \
+                        const T *xr = x + (i0 + i) * d;                                      \
+                        T *ar = acc + i * OBN;                                               \
+                        for (int64_t f = k0; f < k0 + kk; ++f) {                             \
+                            const T xv = xr[f];                                              \
+                            const T *br = bt + f * OBN;                                      \
+                            for (int64_t j = 0; j < OBN; ++j) {                              \
+                                T pr = xv * br[j];                                           \
+                                ar[j] = ar[j] + pr;                                          \
+                            }                                                                \
+                        }                                                                    \
+                    }                                                                        \
+                    for (int64_t f = k0; f < k0 + kk; ++f) {                                 \
+                        const double w1 = c1[f];                                             \
+                        for (int64_t j = 0; j < OBN; ++j) ref1[j] += w1 * (double)bt[f * OBN + j]; \
+                    }                                                                        \
+                    for (int64_t j = 0; j < OBN; ++j) s1[j] = 0.0;                           \
+                    int64_t i = 0;                                                           \
+                    for (; i + 4 <= mi; i += 4) {                                            \
+                        for (int64_t j = 0; j < OBN; ++j)                                    \
+                            p[j] = (acc[i * OBN + j] + acc[(i + 1) * OBN + j]) +             \
+                                   (acc[(i + 2) * OBN + j] + acc[(i + 3) * OBN + j]);        \
+                        for (int64_t j = 0; j < OBN; ++j) s1[j] += (double)p[j];             \
+                    }                                                                        \
+                    for (; i < mi; ++i)                                                      \
+                        for (int64_t j = 0; j < OBN; ++j) s1[j] += (double)acc[i * OBN + j]; \
+                    const int64_t kacc = (t + 1) * bk < d ? (t + 1) * bk : d;                \
+                    const double tol = tol_base * (double)kacc + J->abs_tol;                 \
+                    for (int64_t j = 0; j < sn; ++j)                                         \
+                        if (!(fabs(s1[j] - ref1[j]) <= tol)) J->viol += 1;                   \
+                }                                                                            \
+                for (int64_t i = 0; i < mi; ++i) {                                           \
+                    T bv = ((T *)J->val)[i0 + i];                                            \
+                    int64_t bj = J->idx[i0 + i];                                             \
+                    for (int64_t j = 0; j < sn; ++j) {                                       \
+                        const T a = acc[i * OBN + j];                                        \
+                        const T dd = yn[s0 + j] - (a + a);                                   \
+                        if (dd < bv || (dd == bv && s0 + j < bj)) { bv = dd; bj = s0 + j; }  \
+                    }                                                                        \
+                    ((T *)J->val)[i0 + i] = bv;                                              \
+                    J->idx[i0 + i] = bj;                                                     \
+                }                                                                            \
+            }                                                                                \
+        }                                                                                    \
+    }                                                                                        \
+    free(bt); free(acc); free(c1);                                                           \
+    return NULL;                                                                             \
+}
+
+DEFINE_CHECKED(float, checked_f32_worker)
+DEFINE_CHECKED(double, checked_f64_worker)
+
+static int64_t run_checked(int is64, const void *x, const void *y, const void *yn, int64_t m,
+                           int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk,
+                           double delta_rel, double abs_tol, int64_t *idx, void *val, int threads) {
+    const int64_t nbi = (m + bm - 1) / bm, nbj = (k + bn - 1) / bn;
+    double *cmax = calloc((size_t)(nbj > 0 ? nbj : 1), sizeof(double));
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t f = 0; f < d; ++f) {
+            double v = is64 ? ((const double *)y)[j * d + f] : (double)((const float *)y)[j * d + f];
+            v = v < 0.0 ? -v : v;
+            if (v > cmax[j / bn]) cmax[j / bn] = v;
+        }
+    if (threads < 1) threads = 1;
+    if (threads > MAXT) threads = MAXT;
+    if (nbi < threads) threads = nbi > 0 ? (int)nbi : 1;
+    pthread_t th[MAXT];
+    chk_job jobs[MAXT];
+    const int64_t step = (nbi + threads - 1) / threads;
+    int n = 0;
+    for (int64_t lo = 0; lo < nbi; lo += step, ++n) {
+        chk_job J = {x, y, yn, m, k, d, bm, bn, bk, lo, lo + step < nbi ? lo + step : nbi,
+                     delta_rel, abs_tol, cmax, idx, val, 0};
+        jobs[n] = J;
+    }
+    void *(*fn)(void *) = is64 ? checked_f64_worker : checked_f32_worker;
+    for (int t = 0; t < n; ++t) pthread_create(&th[t], NULL, fn, &jobs[t]);
+    int64_t viol = 0;
+    for (int t = 0; t < n; ++t) {
+        pthread_join(th[t], NULL);
+        viol += jobs[t].viol;
+    }
+    free(cmax);
+    return viol;
+}
+
+int64_t ftko_checked_assign(int is64, const void *x, const void *y, const void *yn, int64_t m,
+                            int64_t k, int64_t d, int64_t bm, int64_t bn, int64_t bk,
+                            double delta_rel, double abs_tol, int64_t *idx, void *val, int threads) {
+    return run_checked(is64, x, y, yn, m, k, d, bm, bn, bk, delta_rel, abs_tol, idx, val, threads);
+}
+
 /* Exact accumulator value acc[i][j] (the quantity the reference's fault hook
  * flips, _kernels.py:462-474). */
 float ftko_dot_f32(const float *a, const float *b, int64_t d) {

@@ -74,6 +74,8 @@ def lib():
     L.ftko_pairwise_sum.argtypes = [p, i64]
     L.ftko_pairwise_sum.restype = dbl
     L.ftko_row_norms_pairwise.argtypes = [p, i64, i64, p]
+    L.ftko_checked_assign.argtypes = [ci, p, p, p, i64, i64, i64, i64, i64, i64, dbl, dbl, p, p, ci]
+    L.ftko_checked_assign.restype = i64
     _LIB = L
     return L
 
@@ -108,6 +110,31 @@ def assign(x, y, y_norms=None, threads=None):
     fn(_ptr(x), _ptr(y), _ptr(yn), m, y.shape[0], x.shape[1], _ptr(idx), _ptr(val),
        _threads(threads))
     return idx, val
+
+
+def checked_assign(x, y, y_norms=None, block=None, delta_rel=None, abs_tol=0.0, threads=None):
+    """abft.checked_assign's fault-free path (abft.py:247-365, _kernels.py:479-612):
+    the same labels/min_dists as ``assign`` plus the reference's per-tile,
+    per-k-interval e1 column-checksum verification.  Detection only: returns
+    (labels, min_dists, violations); a violation cannot be diagnosed here."""
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y, dtype=x.dtype)
+    if y_norms is None:
+        y_norms = row_sq_norms(y)
+    yn = np.ascontiguousarray(y_norms, dtype=x.dtype)
+    f64 = x.dtype == np.float64
+    if block is None:  # the reference's default tiles (tiles.py:70-74)
+        block = (64, 64, 16) if f64 else (32, 256, 16)
+    if delta_rel is None:  # Threshold.default_for (abft.py:41-68)
+        delta_rel = 1e-10 if f64 else 1e-4
+    m = x.shape[0]
+    idx = np.empty(m, dtype=np.int64)
+    val = np.empty(m, dtype=x.dtype)
+    nv = lib().ftko_checked_assign(1 if f64 else 0, _ptr(x), _ptr(y), _ptr(yn), m, y.shape[0],
+                                   x.shape[1], int(block[0]), int(block[1]), int(block[2]),
+                                   float(delta_rel), float(abs_tol), _ptr(idx), _ptr(val),
+                                   _threads(threads))
+    return idx, val, int(nv)
 
 
 def exact_dot(a, b):
@@ -181,10 +208,21 @@ def init_centroids(x, k, seed=0, method="kmeanspp"):
     return np.ascontiguousarray(cs, dtype=x.dtype)
 
 
+def _assign_ft(x, c, ft_mode, threads):
+    if ft_mode == "off":
+        return assign(x, c, threads=threads)
+    lab, md, nv = checked_assign(x, c, threads=threads)
+    if nv:
+        raise RuntimeError(f"oracle checked_assign: {nv} checksum violations (not diagnosed here)")
+    return lab, md
+
+
 def lloyd(x, k, max_iters=300, tol=1e-4, seed=0, init="kmeanspp", threads=None,
-          centroids=None):
-    """kmeans.lloyd (kmeans.py:210-319), fault-free, FT mode irrelevant
-    (a fault-free protected run is bit-identical to the unprotected one)."""
+          centroids=None, ft_mode="off"):
+    """kmeans.lloyd (kmeans.py:210-319), fault-free.  ft_mode "abft" runs the
+    checksum-verified assignment (same results: a fault-free protected run is
+    bit-identical to the unprotected one, test_abft.py:141-149), so its cost
+    is the reference's; a checksum violation raises."""
     x = np.ascontiguousarray(x)
     t_tot = time.perf_counter_ns()
     t0 = time.perf_counter_ns()
@@ -198,7 +236,7 @@ def lloyd(x, k, max_iters=300, tol=1e-4, seed=0, init="kmeanspp", threads=None,
     converged = False
     for it in range(max_iters):
         t0 = time.perf_counter_ns()
-        new, md = assign(x, c, threads=threads)
+        new, md = _assign_ft(x, c, ft_mode, threads)
         timings["assign_ns"] += time.perf_counter_ns() - t0
         sq = md.astype(np.float64) + x_sq
         hist.append(max(0.0, pairwise_sum(sq)))
@@ -215,7 +253,7 @@ def lloyd(x, k, max_iters=300, tol=1e-4, seed=0, init="kmeanspp", threads=None,
         if unchanged or moved < tol:
             converged = True
             break
-    labels, md = assign(x, c, threads=threads)
+    labels, md = _assign_ft(x, c, ft_mode, threads)
     inertia = max(0.0, pairwise_sum(md.astype(np.float64) + x_sq))
     timings["total_ns"] = time.perf_counter_ns() - t_tot
     return {

@@ -440,6 +440,17 @@ def tc_fallback_rows():
     return int(v[0]), int(v[1]), int(v[2])
 
 
+def abft_flags_total(reset=False):
+    """Rows whose screened row checksum failed, summed over every checked
+    assignment on this device since the last reset (ftk_abft_flags_total)."""
+    import ctypes
+
+    v = ctypes.c_int64(0)
+    N.check(N.load().ftk_abft_flags_total(ctx(), ctypes.byref(v), int(bool(reset)), stream()),
+            "ftk_abft_flags_total")
+    return int(v.value)
+
+
 def tc_last_kernel_ms():
     """Device time of the last tensor-core screen launch (ms, -1 if none)."""
     import ctypes

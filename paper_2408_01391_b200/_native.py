@@ -61,6 +61,7 @@ PROTOTYPES = {
     "ftk_flip_f64": (_int, [_p, _p, _i64, _i64, _i64, _i64, _p, _p]),
     "ftk_tc_fallback_rows": (_int, [_p, _p, _p]),
     "ftk_tc_last_kernel_ms": (_int, [_p, _p]),
+    "ftk_abft_flags_total": (_int, [_p, _p, _int, _p]),
     "ftk_tc_raw_dots": (_int, [_p, _int, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p]),
 }
 

@@ -41,6 +41,20 @@ void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st) {
     return s.ptr;
 }
 
+unsigned long long *abft_total_ptr(ftk_ctx *ctx, cudaStream_t st) {
+    if (!ctx->abft_total) {
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(st, &cap);
+        if (cap != cudaStreamCaptureStatusNone) return nullptr;  // counted from the next eager call
+        if (cudaMalloc(&ctx->abft_total, sizeof(unsigned long long)) != cudaSuccess) {
+            ctx->abft_total = nullptr;
+            return nullptr;
+        }
+        cudaMemset(ctx->abft_total, 0, sizeof(unsigned long long));
+    }
+    return ctx->abft_total;
+}
+
 // implemented in exact.cu / update.cu / tc.cu
 int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
@@ -106,6 +120,7 @@ void ftk_ctx_destroy(ftk_ctx *ctx) {
         if (s.ptr) cudaFree(s.ptr);
     for (auto &e : ctx->time_ev)
         if (e) cudaEventDestroy(e);
+    if (ctx->abft_total) cudaFree(ctx->abft_total);
     delete ctx;
 }
 
@@ -270,6 +285,19 @@ int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
 }
 
 void ftk_add_launches(int64_t n) { count_launch(int(n)); }
+
+int ftk_abft_flags_total(ftk_ctx *ctx, int64_t *out, int reset, void *stream) {
+    if (!ctx || !out) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    *out = 0;
+    if (!ctx->abft_total) return FTK_OK;
+    cudaStream_t st = as_stream(stream);
+    unsigned long long v = 0;
+    FTK_CUDA(cudaMemcpyAsync(&v, ctx->abft_total, sizeof(v), cudaMemcpyDeviceToHost, st));
+    FTK_CUDA(cudaStreamSynchronize(st));
+    *out = int64_t(v);
+    if (reset) FTK_CUDA(cudaMemsetAsync(ctx->abft_total, 0, sizeof(v), st));
+    return FTK_OK;
+}
 
 int ftk_tc_last_kernel_ms(ftk_ctx *ctx, float *ms) {
     if (!ctx || !ms) { set_error("bad ctx"); return FTK_ERR_ARG; }

@@ -55,11 +55,15 @@ struct ftk_ctx {
     cudaEvent_t time_ev[2] = {nullptr, nullptr};  // around the last pass-1 launch
     const unsigned *stat_dev[3] = {nullptr, nullptr, nullptr};  // counters still on the device
     int64_t generation = 0;  // scratch (re)allocations: captured graphs go stale
+    unsigned long long *abft_total = nullptr;  // cumulative TC/DMMA row-checksum flags (device)
 };
 
 namespace ftk {
 // Returns a device buffer of at least `bytes` for `slot` of this context.
 void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
+// The context's cumulative row-checksum flag counter (allocated and zeroed
+// on first use, outside any capture; ftk_abft_flags_total reads it).
+unsigned long long *abft_total_ptr(ftk_ctx *ctx, cudaStream_t st);
 
 enum ScratchSlot {
     SLOT_BMAX = 0,

@@ -46,6 +46,7 @@ struct DsParams {
     const double *camax;  // max |c|
     double tau_coef, tau_abs;
     unsigned *abft_count;
+    unsigned long long *abft_total;
 };
 
 __device__ __forceinline__ void cp_async8_zfill(void *dst, const void *src, bool ok) {
@@ -118,7 +119,10 @@ __device__ __forceinline__ void ds_refine_row(const DsParams &P, int64_t row, do
                                    2.0 * (2.0 * double(P.d) + double(P.k)) * 0x1p-53 *
                                        double(P.k) * xn * cm;
                 bad = !(fabs(rsum - rref) <= tau);
-                if (bad) atomicAdd(P.abft_count, 1u);
+                if (bad) {
+                    atomicAdd(P.abft_count, 1u);
+                    if (P.abft_total) atomicAdd(P.abft_total, 1ull);
+                }
             }
             ok = !bad && isfinite(dval) && xn * cm < 1e300 &&
                  (mm2 - A - 0x1p-34 * (fabs(mm2) + fabs(mm1)) > dval);
@@ -528,6 +532,7 @@ int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn
         P.tau_coef = ft->delta_rel * double(d) * std::sqrt(double(k) / 32.0);
         P.tau_abs = ft->abs_tol;
         P.abft_count = cnt + 1;
+        P.abft_total = abft_total_ptr(ctx, st);
     }
     const int64_t nrt = (m + DS_BM - 1) / DS_BM;
     int nsm = 148;

@@ -81,6 +81,7 @@ struct TcParams {
     const float *inj_before;   // exact accumulator value before the flip
     const float *inj_after;    // after the flip
     unsigned *abft_count;      // rows whose checksum failed (diagnostics)
+    unsigned long long *abft_total;  // cumulative (ftk_abft_flags_total)
 };
 
 // ------------------------------------------------------------- kernel ----
@@ -404,7 +405,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                              xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) +
                                              P.a_coef * xn * cm);
                 const float gap_need = 2.0f * A + P.b_coef * (fabsf(m1) + fabsf(m2));
-                if (CHK && abft_bad) atomicAdd(P.abft_count, 1u);
+                if (CHK && abft_bad) {
+                    atomicAdd(P.abft_count, 1u);
+                    if (P.abft_total) atomicAdd(P.abft_total, 1ull);
+                }
                 if (m2 - m1 > gap_need && m1 < INFINITY && !abft_bad) {
                     P.out_idx[orow] = j;
                     P.out_val[orow] = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
@@ -963,6 +967,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         if (rc0) return rc0;  // the 3xTF32 checksum centroid is built by the single-CTA pass 2
         P.tau_abs = float(ft->abs_tol);
         P.abft_count = cnt + 2;
+        P.abft_total = abft_total_ptr(ctx, st);
         if (ft->inj && ft->inj->n > 0) {
             int32_t *ic = static_cast<int32_t *>(scratch(ctx, SLOT_TC_INJROWS, sizeof(float) * 3 * (m + 1), st));
             if (!ic) return FTK_ERR_CUDA;
@@ -1008,6 +1013,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             Q.csum = P.csum; Q.camax = P.camax; Q.tau_coef = P.tau_coef; Q.tau_abs = P.tau_abs;
             Q.inj_col = P.inj_col; Q.inj_before = P.inj_before; Q.inj_after = P.inj_after;
             Q.abft_count = P.abft_count;
+            Q.abft_total = P.abft_total;
             Q.dbg = P.dbg;
             if (ctx->rows_info && ctx->rows_x == x && ctx->rows_m == m && ctx->rows_d == d)
                 Q.rowinfo = reinterpret_cast<const float4 *>(ctx->rows_info);

@@ -550,7 +550,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                       34.0f * 0x1p-24f * sqrtf(xx * (1.0f + 0x1p-10f)) *
                                           sqrtf(P.camax[2] * (1.0f + 0x1p-10f));
                     abft_bad = !(fabs(rsum - rref) <= double(tau));
-                    if (abft_bad) atomicAdd(P.abft_count, 1u);
+                    if (abft_bad) {
+                        atomicAdd(P.abft_count, 1u);
+                        if (P.abft_total) atomicAdd(P.abft_total, 1ull);
+                    }
                 }
                 // magnitudes far from overflow: the screen saw every column finite
                 const bool sane = xn * cm < 1e36f && isfinite(dval);

@@ -30,6 +30,7 @@ struct PairParams {
     const int32_t *inj_col;
     const float *inj_before, *inj_after;
     unsigned *abft_count;
+    unsigned long long *abft_total;  // cumulative over launches (ftk_abft_flags_total)
     // pass 1: per uncertified row, the pass-2 threshold and the (d1, j1) seed key
     float *fb_thr;
     unsigned long long *fb_seed;

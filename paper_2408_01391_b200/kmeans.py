@@ -676,6 +676,10 @@ class LloydEngine:
         self.slot = 1 - self.slot
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
 
+    def labels_view(self):
+        """Device int32 labels of the last completed step (no copy)."""
+        return self.A.labels[1 - self.slot]
+
     def close(self):
         """Unregister the per-fit row bounds (X may be freed afterwards)."""
         self.rows.close()

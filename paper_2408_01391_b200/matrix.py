@@ -158,18 +158,44 @@ def mat_store(x, path, format="ftkm-binary"):
         raise ValueError(f"unknown format {format!r}")
 
 
+def _csv_cell(path, tok, line_no, col_no):
+    """One CSV token -> a finite float, or FormatError at its 1-based
+    (file line, column) position (matrix.py:175-212)."""
+    try:
+        v = float(tok)
+    except ValueError:
+        raise FormatError(f"{path}: bad value {tok.strip()!r} at ({line_no},{col_no})",
+                          row=line_no, col=col_no) from None
+    if not np.isfinite(v):
+        raise FormatError(f"{path}: non-finite value at ({line_no},{col_no})",
+                          row=line_no, col=col_no)
+    return v
+
+
+def _csv_rows(path, dt):
+    """The reference's CSV reader semantics: positions are 1-based FILE line
+    numbers (blank lines are skipped but still counted), every row must have
+    the first row's column count, '#' is an ordinary (bad) token."""
+    out, width = [], None
+    with open(path, "r") as fh:
+        for line_no, raw in enumerate(fh, start=1):
+            text = raw.strip()
+            if not text:
+                continue
+            cells = text.split(",")
+            width = len(cells) if width is None else width
+            if len(cells) != width:
+                raise FormatError(f"{path}: row {line_no} has {len(cells)} columns, expected {width}",
+                                  row=line_no, col=len(cells))
+            out.append([_csv_cell(path, c, line_no, i) for i, c in enumerate(cells, start=1)])
+    if not out:
+        raise FormatError(f"{path}: empty matrix")
+    return np.ascontiguousarray(np.array(out, dtype=np.float64), dtype=dt)
+
+
 def mat_load(path, format="ftkm-binary", precision="double"):
     if format == "csv":
-        try:
-            a = np.loadtxt(path, delimiter=",", ndmin=2, dtype=np.float64)
-        except ValueError as e:
-            raise FormatError(f"{path}: {e}") from None
-        if a.size == 0:
-            raise FormatError(f"{path}: empty matrix")
-        if not np.isfinite(a).all():
-            i, j = np.argwhere(~np.isfinite(a))[0]
-            raise FormatError(f"{path}: non-finite value at ({i + 1},{j + 1})", i + 1, j + 1)
-        return np.ascontiguousarray(a, dtype=dtype_of(precision))
+        return _csv_rows(path, dtype_of(precision))
     if format != "ftkm-binary":
         raise ValueError(f"unknown format {format!r}")
     with open(path, "rb") as fh:

@@ -85,3 +85,31 @@ def test_cluster_report_matches_reference(name, tmp_path):
     lab = np.loadtxt(labels, dtype=np.int64)
     sha = [r[2] for r in keep if r[1] == "assignments_sha256"][0]
     assert hashlib.sha256(lab.tobytes()).hexdigest() == sha
+
+
+@pytest.mark.parametrize("text,row,col", [
+    ("1,2\nabc,3\n", 2, 1),          # bad cell: 1-based file position
+    ("1,2\n\n3,inf\n", 3, 2),        # blank line still counts as a file line
+    ("# c\n1,2\n", 1, 1),            # '#' is not a comment in the reference reader
+    ("1,2\n3\n", 2, 1),              # ragged row: (line, its column count)
+])
+def test_csv_loader_error_positions(tmp_path, text, row, col):
+    """mat_load(format="csv") reports the reference reader's positions
+    (matrix.py:175-212): 1-based file lines and columns."""
+    from paper_2408_01391_b200.errors import FormatError
+    from paper_2408_01391_b200.matrix import mat_load
+
+    p = tmp_path / "m.csv"
+    p.write_text(text)
+    with pytest.raises(FormatError) as ei:
+        mat_load(str(p), format="csv")
+    assert (ei.value.row, ei.value.col) == (row, col)
+
+
+def test_csv_loader_values(tmp_path):
+    from paper_2408_01391_b200.matrix import mat_load
+
+    p = tmp_path / "m.csv"
+    p.write_text("1, 2.5\n\n-3,4e-3\n")
+    a = mat_load(str(p), format="csv", precision="single")
+    assert a.dtype == np.float32 and a.tolist() == [[1.0, 2.5], [-3.0, np.float32(4e-3)]]
