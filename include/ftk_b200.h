@@ -102,12 +102,25 @@ int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const fl
  * captured from this context's launches is stale once it changes. */
 int64_t ftk_ctx_generation(ftk_ctx *ctx);
 
-/* k-means++ seeding step (kmeans.py:95-103): d2[i] = sum_f (x[i,f] - x[pick,f])^2 in
- * float64 with numpy's pairwise association (a single leaf: d <= 128), then
- * np.minimum with the previous d2 unless `first`.  The host keeps the
- * reference's Generator draws and its cumsum/searchsorted. */
+/* k-means++ D^2 seeding (replaces the numpy body of kmeans.init_centroids,
+ * kmeans.py:86-103).  ftk_kpp_d2 / ftk_kpp_update: d2[i] = sum_f (x[i,f] -
+ * x[pick,f])^2 in float64 with numpy's pairwise association over the feature
+ * axis (any d), then np.minimum with the previous d2 unless `first`.  The
+ * pick is `host_pick` when >= 0, else read from *pick_dev; picks[c] records
+ * it (picks may be NULL). */
 int ftk_kpp_d2(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t pick,
                int first, double *d2, void *stream);
+int ftk_kpp_update(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t host_pick,
+                   const int64_t *pick_dev, int first, double *d2, int64_t *picks, int64_t c,
+                   void *stream);
+/* *pick_dev = min(searchsorted(cumsum(d2), r, side="right"), m - 1) with
+ * numpy's SEQUENTIAL float64 cumsum, bit-exact: a parallel scan classifies
+ * every prefix against r under a rigorous rounding bound; if any prefix is
+ * within the bound of r, one thread replays the sequential cumsum (and
+ * *n_replays is incremented).  r = Generator.random() * d2.sum() from the
+ * host, as in the reference.  No host synchronisation. */
+int ftk_kpp_search(ftk_ctx *ctx, const double *d2, int64_t m, double r, int64_t *pick_dev,
+                   uint64_t *n_replays, void *stream);
 
 /* out[i] = left-to-right sum of x[i,j]^2 in the data dtype. */
 int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,
@@ -197,6 +210,14 @@ int ftk_flip_f64(ftk_ctx *ctx, double *a, int64_t d, int64_t i, int64_t j, int64
  * with the 1xTF32 screen, out[1] = rows the 3xTF32 re-screen still could not
  * certify (resolved by the exact kernel). */
 int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream);
+
+/* Upload `nbytes` from PAGEABLE host memory (e.g. a numpy array) to device
+ * memory at pinned-copy speed: parallel host copies into page-locked staging
+ * buffers overlapped with the DMA.  Returns when the host source may be
+ * reused; `stream` is ordered behind the upload (no device synchronisation).
+ * Replaces the reference's implicit numpy residency (its kernels read the
+ * caller's array in place, gemm.py:108-131). */
+int ftk_h2d(ftk_ctx *ctx, void *dst, const void *src, int64_t nbytes, void *stream);
 
 /* Diagnostics: cumulative count of rows whose tensor-core / DMMA row
  * checksum failed (every screened checked assignment on this context since

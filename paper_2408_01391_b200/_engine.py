@@ -70,7 +70,23 @@ def to_dev(a, dtype=None, copy=False):
                    non_blocking=True, copy=copy)
         return out.contiguous()
     arr = np.ascontiguousarray(a, dtype=dtype)
-    return t.from_numpy(arr).to(device(), non_blocking=False)
+    if arr.nbytes < _H2D_MIN:
+        return t.from_numpy(arr).to(device(), non_blocking=False)
+    out = t.empty(arr.shape, dtype=t.from_numpy(arr[:0]).dtype, device=device())
+    upload_into(out, arr)
+    return out
+
+
+_H2D_MIN = 8 << 20  # below this the driver's own pageable copy is as fast
+
+
+def upload_into(dst_t, arr):
+    """Copy a C-contiguous host numpy array into the device tensor `dst_t`
+    (same bytes) through the staged pageable uploader (ftk_h2d); the current
+    stream is ordered behind it.  The source may be reused on return."""
+    arr = np.ascontiguousarray(arr)
+    assert dst_t.is_contiguous() and dst_t.numel() * dst_t.element_size() == arr.nbytes
+    N.check(N.load().ftk_h2d(ctx(), ptr(dst_t), arr.ctypes.data, arr.nbytes, stream()), "ftk_h2d")
 
 
 def to_host(tensor):
@@ -298,12 +314,27 @@ class RowInfo:
             pass
 
 
-def kpp_d2_dev(x_t, pick, first, d2):
-    """k-means++ D^2 update on the device (ftk_kpp_d2)."""
+def kpp_buffers(m, k, dev):
+    """(d2 f64[m], picks i64[k], total f64[1], pick i64[1], replays u64[1])."""
+    t = _torch()
+    return (t.empty(m, dtype=t.float64, device=dev), t.zeros(k, dtype=t.int64, device=dev),
+            t.empty(1, dtype=t.float64, device=dev), t.zeros(1, dtype=t.int64, device=dev),
+            t.zeros(1, dtype=t.int64, device=dev))
+
+
+def kpp_update_dev(x_t, host_pick, pick_dev, first, d2, picks, c):
+    """k-means++ D^2 update (ftk_kpp_update); the pick is `host_pick` if >= 0,
+    else the device scalar `pick_dev`; picks[c] records it."""
     m, d = x_t.shape
-    N.check(N.load().ftk_kpp_d2(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), m, d, int(pick),
-                                int(bool(first)), ptr(d2), stream()), "ftk_kpp_d2")
-    return d2
+    N.check(N.load().ftk_kpp_update(ctx(), code(ndtype(x_t.dtype)), ptr(x_t), m, d, int(host_pick),
+                                    ptr(pick_dev), int(bool(first)), ptr(d2), ptr(picks), int(c),
+                                    stream()), "ftk_kpp_update")
+
+
+def kpp_search_dev(d2, r, pick_dev, n_replays):
+    """pick_dev <- min(searchsorted(cumsum(d2), r, 'right'), m - 1), bit-exact."""
+    N.check(N.load().ftk_kpp_search(ctx(), ptr(d2), d2.shape[0], float(r), ptr(pick_dev),
+                                    ptr(n_replays), stream()), "ftk_kpp_search")
 
 
 def row_sq_norms(x):

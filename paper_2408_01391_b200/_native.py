@@ -41,6 +41,8 @@ PROTOTYPES = {
     "ftk_row_sq_norms": (_int, [_p, _int, _p, _i64, _i64, _p, _p]),
     "ftk_row_info": (_int, [_p, _p, _i64, _i64, _p, _p]),
     "ftk_kpp_d2": (_int, [_p, _int, _p, _i64, _i64, _i64, _int, _p, _p]),
+    "ftk_kpp_update": (_int, [_p, _int, _p, _i64, _i64, _i64, _p, _int, _p, _p, _i64, _p]),
+    "ftk_kpp_search": (_int, [_p, _p, _i64, _dbl, _p, _p, _p]),
     "ftk_ctx_set_rows": (_int, [_p, _p, _i64, _i64, _p]),
     "ftk_ctx_generation": (_i64, [_p]),
     "ftk_assign": (_int, [_p, _int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _p, _p,
@@ -62,6 +64,7 @@ PROTOTYPES = {
     "ftk_tc_fallback_rows": (_int, [_p, _p, _p]),
     "ftk_tc_last_kernel_ms": (_int, [_p, _p]),
     "ftk_abft_flags_total": (_int, [_p, _p, _int, _p]),
+    "ftk_h2d": (_int, [_p, _p, _p, _i64, _p]),
     "ftk_tc_raw_dots": (_int, [_p, _int, _p, _p, _p, _i64, _i64, _i64, _p, _p, _p, _p]),
 }
 

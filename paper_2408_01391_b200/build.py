@@ -24,6 +24,8 @@ SOURCES = {
     "tc.cu": [],
     "tc_pair.cu": [],
     "dscreen.cu": [],
+    "kpp.cu": [],
+    "h2d.cu": [],
 }
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",

@@ -55,13 +55,18 @@ unsigned long long *abft_total_ptr(ftk_ctx *ctx, cudaStream_t st) {
     return ctx->abft_total;
 }
 
-// implemented in exact.cu / update.cu / tc.cu
+// implemented in exact.cu / update.cu / tc.cu / h2d.cu
+void h2d_stage_free(void *);
+int h2d_pageable_run(ftk_ctx *, void *, const void *, size_t, cudaStream_t);
 int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t, int64_t, int64_t,
               int64_t, int64_t, int64_t, int32_t *, void *, void *, bool, double, double, int64_t,
               const ftk_injection *, ftk_events *, cudaStream_t);
 int row_sq_norms_run(int, const void *, int64_t, int64_t, void *, cudaStream_t);
 int row_info_run(const float *, int64_t, int64_t, float *, cudaStream_t);
-int kpp_d2_run(int, const void *, int64_t, int64_t, int64_t, int, double *, cudaStream_t);
+int kpp_update_run(int, const void *, int64_t, int64_t, int64_t, const int64_t *, int, double *,
+                   int64_t *, int64_t, cudaStream_t);
+int kpp_search_run(ftk_ctx *, const double *, int64_t, double, int64_t *, unsigned long long *,
+                   cudaStream_t);
 int update_sums_run(ftk_ctx *, int, const void *, const int32_t *, int64_t, int64_t, int64_t,
                     double *, int64_t *, double *, int64_t *, cudaStream_t);
 int dmr_compare_run(const double *, const int64_t *, const double *, const int64_t *, int64_t,
@@ -121,6 +126,7 @@ void ftk_ctx_destroy(ftk_ctx *ctx) {
     for (auto &e : ctx->time_ev)
         if (e) cudaEventDestroy(e);
     if (ctx->abft_total) cudaFree(ctx->abft_total);
+    h2d_stage_free(ctx->h2d);
     delete ctx;
 }
 
@@ -131,8 +137,25 @@ int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info
 
 int ftk_kpp_d2(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t pick,
                int first, double *d2, void *stream) {
-    if (!ctx || !dtype_ok(dtype) || pick < 0 || pick >= m) { set_error("bad ctx/dtype/pick"); return FTK_ERR_ARG; }
-    return kpp_d2_run(dtype, x, m, d, pick, first, d2, as_stream(stream));
+    if (!ctx || !dtype_ok(dtype) || d < 1 || m < 1 || pick < 0 || pick >= m) { set_error("bad ctx/dtype/pick"); return FTK_ERR_ARG; }
+    return kpp_update_run(dtype, x, m, d, pick, nullptr, first, d2, nullptr, 0, as_stream(stream));
+}
+
+int ftk_kpp_update(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t d, int64_t host_pick,
+                   const int64_t *pick_dev, int first, double *d2, int64_t *picks, int64_t c,
+                   void *stream) {
+    if (!ctx || !dtype_ok(dtype) || d < 1 || m < 1 || host_pick >= m || (host_pick < 0 && !pick_dev)) {
+        set_error("bad ctx/shape/pick");
+        return FTK_ERR_ARG;
+    }
+    return kpp_update_run(dtype, x, m, d, host_pick, pick_dev, first, d2, picks, c, as_stream(stream));
+}
+
+int ftk_kpp_search(ftk_ctx *ctx, const double *d2, int64_t m, double r, int64_t *pick_dev,
+                   uint64_t *n_replays, void *stream) {
+    if (!ctx || m < 1 || !pick_dev || !n_replays) { set_error("bad ctx/args"); return FTK_ERR_ARG; }
+    return kpp_search_run(ctx, d2, m, r, pick_dev, reinterpret_cast<unsigned long long *>(n_replays),
+                          as_stream(stream));
 }
 
 int64_t ftk_ctx_generation(ftk_ctx *ctx) { return ctx ? ctx->generation : -1; }
@@ -285,6 +308,11 @@ int ftk_tc_fallback_rows(ftk_ctx *ctx, int64_t *out, void *stream) {
 }
 
 void ftk_add_launches(int64_t n) { count_launch(int(n)); }
+
+int ftk_h2d(ftk_ctx *ctx, void *dst, const void *src, int64_t nbytes, void *stream) {
+    if (!ctx || nbytes < 0 || (nbytes && (!dst || !src))) { set_error("bad ctx/args"); return FTK_ERR_ARG; }
+    return h2d_pageable_run(ctx, dst, src, size_t(nbytes), as_stream(stream));
+}
 
 int ftk_abft_flags_total(ftk_ctx *ctx, int64_t *out, int reset, void *stream) {
     if (!ctx || !out) { set_error("bad ctx"); return FTK_ERR_ARG; }

@@ -56,6 +56,7 @@ struct ftk_ctx {
     const unsigned *stat_dev[3] = {nullptr, nullptr, nullptr};  // counters still on the device
     int64_t generation = 0;  // scratch (re)allocations: captured graphs go stale
     unsigned long long *abft_total = nullptr;  // cumulative TC/DMMA row-checksum flags (device)
+    void *h2d = nullptr;  // staged pageable upload: pinned buffers, streams (h2d.cu)
 };
 
 namespace ftk {
@@ -89,6 +90,7 @@ enum ScratchSlot {
     SLOT_DS = 20,         // float64 screen: bounds, counters, fallback rows
     SLOT_DS_G = 21,       // float64 screen: gathered fallback rows
     SLOT_EXACT_SPLIT = 22,  // per-(row, column split) argmin partials of the exact kernel
+    SLOT_KPP = 23,          // k-means++: prefix scan of d2, counters, CUB temp
 };
 
 // ------------------------------------------------------- float helpers --

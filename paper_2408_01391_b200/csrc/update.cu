@@ -1019,61 +1019,6 @@ __global__ void movement_warp_kernel(const T *nc, const T *oc, int64_t k, int64_
     }
 }
 
-// k-means++ D^2 update (kmeans.py:95-103): d2[i] = pairwise_sum_f((x64[i,f] -
-// x64[pick,f])^2), then np.minimum with the previous d2 unless `first`.  One
-// thread per row; d <= 128 keeps numpy's pairwise reduce a single leaf (8
-// strided accumulators, fixed combine, sequential tail), evaluated on the fly.
-template <typename T>
-__global__ void kpp_d2_kernel(const T *x, int64_t m, int64_t d, int64_t pick, int first,
-                              double *d2) {
-    const T *cr = x + pick * d;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const T *xr = x + i * d;
-        auto sq = [&](int64_t f) {
-            const double df = __dsub_rn(double(xr[f]), double(cr[f]));
-            return __dmul_rn(df, df);
-        };
-        double s;
-        if (d < 8) {
-            s = 0.0;
-            for (int64_t f = 0; f < d; ++f) s = __dadd_rn(s, sq(f));
-        } else {
-            double r[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = sq(j);
-            int64_t f = 8;
-            for (; f < d - (d % 8); f += 8) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], sq(f + j));
-            }
-            s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-            for (; f < d; ++f) s = __dadd_rn(s, sq(f));
-        }
-        if (first) d2[i] = s;
-        else {
-            const double o = d2[i];
-            d2[i] = (s != s || o != o) ? s + o : (s < o ? s : o);  // np.minimum (NaN propagates)
-        }
-    }
-}
-
-int kpp_d2_run(int dtype, const void *x, int64_t m, int64_t d, int64_t pick, int first, double *d2,
-               cudaStream_t st) {
-    if (d > 128) {
-        set_error("kpp_d2: d > 128 (numpy's pairwise reduce is not a single leaf)");
-        return FTK_ERR_UNSUPPORTED;
-    }
-    const unsigned grid = unsigned(std::min<int64_t>((m + 255) / 256, 148 * 16));
-    if (dtype == FTK_F32)
-        kpp_d2_kernel<float><<<grid, 256, 0, st>>>(static_cast<const float *>(x), m, d, pick, first, d2);
-    else
-        kpp_d2_kernel<double><<<grid, 256, 0, st>>>(static_cast<const double *>(x), m, d, pick, first, d2);
-    FTK_LAUNCHED("kpp_d2_kernel");
-    return FTK_OK;
-}
-
 // sq[i] = pairwise_sum_f((x[i,f] - cent64[label[i], f])^2)  (kmeans.py:199-201)
 template <typename T>
 __global__ void own_sq_dists_kernel(const T *x, const int32_t *lab, const double *c64, int64_t m,

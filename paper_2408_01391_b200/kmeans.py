@@ -74,75 +74,60 @@ class KMeansResult:
 
 def init_centroids(x, k, seed=0, method="kmeanspp"):
     """Deterministic seeding with the reference's Generator draws
-    (kmeans.py:69-103).  Host numpy: random-sample is a gather; kmeanspp's
-    D^2 loop is the reference's own float64 host algorithm."""
-    if _is_torch(x):
+    (kmeans.py:69-103).  random-sample is a gather of the reference's
+    ``rng.choice`` rows; kmeanspp runs its D^2 seeding on the device
+    (_kmeanspp_dev) for every D.  numpy in -> numpy out (data dtype)."""
+    if _is_torch(x) and x.is_cuda:
+        x_t, x_h = x, None
         m = x.shape[0]
-        if k > m:
-            raise ValueError(f"k={k} exceeds the number of samples {m}")
-        if method not in INIT_METHODS:
-            raise ValueError(f"unknown init method {method!r}")
-        if method == "random-sample":
-            idx = np.random.default_rng(seed).choice(m, size=k, replace=False)
-            return E.to_host(x[E._torch().as_tensor(idx, device=x.device)])
-        x = E.to_host(x)
-    x = as_matrix(x)
-    m = x.shape[0]
+    else:
+        x_h = as_matrix(E.to_host(x) if _is_torch(x) else x)
+        x_t, m = None, x_h.shape[0]
     if k > m:
         raise ValueError(f"k={k} exceeds the number of samples {m}")
     if method not in INIT_METHODS:
         raise ValueError(f"unknown init method {method!r}")
     rng = np.random.default_rng(seed)
     if method == "random-sample":
-        return np.ascontiguousarray(x[rng.choice(m, size=k, replace=False)])
-    if x.shape[1] <= 128 and m > 0:
-        return _kmeanspp_dev(x, k, rng)
-    x64 = x.astype(np.float64)
-    cs = np.empty((k, x.shape[1]), dtype=np.float64)
-    cs[0] = x64[int(rng.integers(0, m))]
-    d2 = ((x64 - cs[0]) ** 2).sum(axis=1)
-    for c in range(1, k):
-        total = d2.sum()
-        if total <= 0:
-            pick = int(rng.integers(0, m))
-        else:
-            r = rng.random() * total
-            pick = min(int(np.searchsorted(np.cumsum(d2), r, side="right")), m - 1)
-        cs[c] = x64[pick]
-        d2 = np.minimum(d2, ((x64 - cs[c]) ** 2).sum(axis=1))
-    return np.ascontiguousarray(cs, dtype=x.dtype)
+        idx = rng.choice(m, size=k, replace=False)
+        if x_h is not None:
+            return np.ascontiguousarray(x_h[idx])
+        return E.to_host(x_t[E._torch().as_tensor(idx, device=x_t.device)])
+    if x_t is None:
+        x_t = E.to_dev(x_h)
+    picks = _kmeanspp_dev(x_t, k, rng)
+    if x_h is not None:
+        return np.ascontiguousarray(x_h[picks])
+    return E.to_host(x_t[E._torch().as_tensor(picks, device=x_t.device)])
 
 
-def _kmeanspp_dev(x, k, rng):
-    """k-means++ D^2 seeding with the reference's draws (kmeans.py:86-103).
-    The O(N K D) distance updates run on the device (ftk_kpp_d2: float64,
-    numpy's pairwise row reduce, np.minimum); d2.sum() is the device pairwise
-    sum; the reference's own numpy cumsum/searchsorted run on a pinned host
-    copy of d2, so every pick is the reference's."""
+def _kmeanspp_dev(x_t, k, rng):
+    """k-means++ D^2 seeding with the reference's draws (kmeans.py:86-103),
+    on the device: the D^2 updates (ftk_kpp_update: float64, numpy's
+    pairwise feature reduce, np.minimum), ``d2.sum()`` (device pairwise sum)
+    and ``searchsorted(cumsum(d2), r, "right")`` (ftk_kpp_search: bit-exact
+    against numpy's sequential cumsum).  Per pick the host reads one scalar
+    -- the total its ``rng.random()`` draw is scaled by -- and nothing else.
+    Returns the k picked row indices (int64)."""
     t = E._torch()
-    m = x.shape[0]
-    x_t = E.to_dev(x)
-    d2 = t.empty(m, dtype=t.float64, device=x_t.device)
-    tot = t.empty(1, dtype=t.float64, device=x_t.device)
-    host = t.empty(m, dtype=t.float64).pin_memory()
+    m = x_t.shape[0]
+    if m == 0 or k == 0:
+        return np.zeros(0, dtype=np.int64)
+    d2, picks, tot, pick_dev, n_rep = E.kpp_buffers(m, k, x_t.device)
     tot_h = t.empty(1, dtype=t.float64).pin_memory()
-    picks = [int(rng.integers(0, m))]
-    E.kpp_d2_dev(x_t, picks[0], True, d2)
-    h = host.numpy()
-    for _ in range(1, k):
+    stream = t.cuda.current_stream()
+    E.kpp_update_dev(x_t, int(rng.integers(0, m)), None, True, d2, picks, 0)
+    for c in range(1, k):
         E.pairwise_sum_dev(d2, tot)
         tot_h.copy_(tot, non_blocking=True)
-        host.copy_(d2, non_blocking=True)
-        t.cuda.current_stream().synchronize()
+        stream.synchronize()
         total = float(tot_h[0])
         if total <= 0:
-            pick = int(rng.integers(0, m))
+            E.kpp_update_dev(x_t, int(rng.integers(0, m)), None, False, d2, picks, c)
         else:
-            r = rng.random() * total
-            pick = min(int(np.searchsorted(np.cumsum(h), r, side="right")), m - 1)
-        picks.append(pick)
-        E.kpp_d2_dev(x_t, pick, False, d2)
-    return np.ascontiguousarray(x[np.asarray(picks, dtype=np.int64)])
+            E.kpp_search_dev(d2, rng.random() * total, pick_dev, n_rep)
+            E.kpp_update_dev(x_t, -1, pick_dev, False, d2, picks, c)
+    return E.to_host(picks)
 
 
 def _resolve_tile(tile, x, k, tune_table):
@@ -321,6 +306,24 @@ class _DeviceAssign:
         return report
 
 
+class _StepGraph:
+    """One captured step: the assignment graph and the update graph, replayed
+    back to back with timing events around each (phase times on every graph
+    step, from events recorded between the replays on the stream)."""
+
+    def __init__(self, parts, launches):
+        self.parts = parts
+        self.launches = launches
+
+    def replay(self, ev):
+        ev[0].record()
+        self.parts[0].replay()
+        ev[1].record()
+        self.parts[1].replay()
+        ev[2].record()
+        N.load().ftk_add_launches(self.launches)
+
+
 class LloydEngine:
     """Device-resident Lloyd state: one ``step`` per iteration (assign ->
     inertia -> label compare -> update -> finalize -> movement) with a single
@@ -376,6 +379,8 @@ class LloydEngine:
         self.cbuf = 0
         self._counts_buf = [t.zeros(k, dtype=t.int64, device=dev) for _ in range(2)]
         self._done = [t.cuda.Event(), t.cuda.Event()]  # end of the last replay, per parity
+        # per parity: around the assign graph and the update graph of a replay
+        self._gev = [[t.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2)]
         self._ahead = None  # iteration already replayed ahead of its step() call
         self._cent_prev = None
         self.bind(0)
@@ -405,15 +410,19 @@ class LloydEngine:
         n = len(sched.for_iteration(it))
         return n == 0 or (self.sinj is not None and n <= self.sinj.cap)
 
-    def _device_part(self, it, sinj=None):
-        """Launches of one step with no host synchronisation (graph-capturable):
-        assign, inertia, label compare, update sums, finalize into the other
-        static centroid buffer, movement, control copies."""
-        A = self.A
+    def _part_assign(self, it, sinj=None):
+        """First half of a graph step (capturable): centroid norms and the
+        assignment pass (+ the injected pass's applied/before/after copy)."""
         yn = E.row_sq_norms_dev(self.cent)
-        A.run(self.cent, yn, NOOP_HOOK, it, self.slot, sinj=sinj)
+        self.A.run(self.cent, yn, NOOP_HOOK, it, self.slot, sinj=sinj)
         if sinj is not None:
             sinj.copy_back()
+
+    def _part_update(self):
+        """Second half (capturable, no host synchronisation): inertia + label
+        compare on a side-stream branch, update sums, finalize into the other
+        static centroid buffer, movement, control copies."""
+        A = self.A
         # inertia and the label compare only read the assignment: a graph
         # branch on a side stream, concurrent with the update chain
         cur = self.t.cuda.current_stream()
@@ -458,10 +467,10 @@ class LloydEngine:
                 self.slot = self.cbuf = par
                 self.cent = self.cent_buf[par]
                 self.bind(par)
-                g = t.cuda.CUDAGraph()
                 l0 = N.launch_count()
                 try:
-                    self._record(g, it, sinj)
+                    parts = (self._record(lambda: self._part_assign(it, sinj)),
+                             self._record(self._part_update))
                 except Exception:
                     # a launch path that needs the host mid-step: stay eager
                     t.cuda.synchronize()
@@ -470,8 +479,8 @@ class LloydEngine:
                     self.slot, self.cbuf, self.cent = state
                     self.bind(self.slot)
                     return False
-                store[par] = (g, N.launch_count() - l0)
-                N.load().ftk_add_launches(-store[par][1])  # captured, not run
+                store[par] = _StepGraph(parts, N.launch_count() - l0)
+                N.load().ftk_add_launches(-store[par].launches)  # captured, not run
         self.slot, self.cbuf, self.cent = state
         self.bind(self.slot)
         if E.ctx_generation() != gen0:  # a capture grew a scratch buffer: redo
@@ -480,12 +489,13 @@ class LloydEngine:
         self.ctx_gen = gen0
         return True
 
-    def _record(self, g, it, sinj):
-        """Stream capture of one step into `g` on a side stream.  Unlike
-        torch.cuda.graph this does not empty the caching allocator (whose
-        cudaFree/cudaMalloc churn cost more than the capture itself); the
-        graphs share one private memory pool and replay one at a time."""
+    def _record(self, fn):
+        """Stream capture of `fn`'s launches into a new graph on a side stream.
+        Unlike torch.cuda.graph this does not empty the caching allocator
+        (whose cudaFree/cudaMalloc churn cost more than the capture itself);
+        the graphs share one private memory pool and replay one at a time."""
         t = self.t
+        g = t.cuda.CUDAGraph()
         cur = t.cuda.current_stream()
         if self._cap_stream is None:
             self._cap_stream = t.cuda.Stream()
@@ -497,12 +507,13 @@ class LloydEngine:
             else:
                 g.capture_begin(pool=self._pool)
             try:
-                self._device_part(it, sinj)
+                fn()
             finally:
                 g.capture_end()
         cur.wait_stream(s)
         if self._pool is None:
             self._pool = g.pool()
+        return g
 
     def reset(self, x, c0, gemm_hook=NOOP_HOOK, update_hook=NOOP_HOOK):
         """Start a new fit of the same shape on this engine: X copied into the
@@ -513,8 +524,10 @@ class LloydEngine:
         if self._ahead is not None:
             t.cuda.current_stream().synchronize()
             self._ahead = None
-        src = x if _is_torch(x) else t.from_numpy(np.ascontiguousarray(x))
-        self.x_t.copy_(src, non_blocking=True)
+        if _is_torch(x):
+            self.x_t.copy_(x, non_blocking=True)
+        else:  # numpy (pageable): the staged parallel uploader
+            E.upload_into(self.x_t, np.ascontiguousarray(x, dtype=self.dtype))
         self.xsq.copy_(E.row_sq_norms_dev(self.x_t).to(t.float64))
         self.rows.refresh()
         self.cent_buf[0].copy_(E.to_dev(c0) if not _is_torch(c0) else c0)
@@ -572,9 +585,7 @@ class LloydEngine:
             self.bind(self.slot)
             if inj is not None:
                 inj.load(arrs)  # stream-ordered before the replay
-            g, nk = store[self.slot]
-            g.replay()
-            N.load().ftk_add_launches(nk)
+            store[self.slot].replay(self._gev[self.slot])
             self._done[self.slot].record()
         # one step queued ahead: the next replay (the other parity's buffers)
         # goes out before the host reads this step, so the GPU does not idle
@@ -586,12 +597,13 @@ class LloydEngine:
             if self._cent_prev is None:
                 self._cent_prev = t.empty_like(self.cent)
             self._cent_prev.copy_(self.cent, non_blocking=True)
-            g, nk = self.graphs[1 - self.slot]
-            g.replay()
-            N.load().ftk_add_launches(nk)
+            self.graphs[1 - self.slot].replay(self._gev[1 - self.slot])
             self._done[1 - self.slot].record()
             self._ahead = it + 1
         self._done[self.slot].synchronize()
+        ge = self._gev[self.slot]  # phase times of this step's replay
+        self.assign_ms = ge[0].elapsed_time(ge[1])
+        self.update_ms = ge[1].elapsed_time(ge[2])
         n_ev = int(self.evc_host[0]) if A.checked else None
         rep = A.finish(self.gemm_hook, it, inj, n_events=n_ev, replayed=True)
         if rep is not None:
@@ -615,8 +627,10 @@ class LloydEngine:
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
 
     def step(self, it, eager=False, more=None):
-        """One Lloyd iteration; returns (inertia, unchanged, moved).  Eager
-        steps also record the phase timings (assign_ms / update_ms).
+        """One Lloyd iteration; returns (inertia, unchanged, moved), and the
+        step's device phase times in assign_ms / update_ms (eager steps: CUDA
+        events around the phases; graph steps: events between the assignment
+        and update graph replays).
         `more()`: the caller may run step it+1 (lets graph steps keep one
         replay queued ahead)."""
         if self._ahead is not None and (self._ahead != it or eager):
@@ -766,7 +780,11 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     timings = {"init_ns": 0, "assign_ns": 0, "update_ns": 0, "total_ns": 0}
     t_total = time.perf_counter_ns()
     t0 = time.perf_counter_ns()
-    c0 = init_centroids(x, k, seed=config.seed, method=config.init)
+    src = x
+    if config.init == "kmeanspp" and not (_is_torch(x) and x.is_cuda):
+        # the D^2 seeding runs on the device: upload once, seed from that copy
+        src = E.to_dev(x)
+    c0 = init_centroids(src, k, seed=config.seed, method=config.init)
     timings["init_ns"] = time.perf_counter_ns() - t0
 
     graph = config.max_iters >= 8
@@ -774,11 +792,12 @@ def _lloyd_fit(x, config, dtype, k, cfg, thr, threads, gemm_hook, update_hook):
     eng = None
     if key is not None and _FIT_CACHE.get("key") == key:
         eng = _FIT_CACHE["eng"]
-        eng.reset(x, c0, gemm_hook, update_hook)
+        eng.reset(src, c0, gemm_hook, update_hook)
     else:
         _fit_cache_clear()
-        eng = LloydEngine(E.to_dev(x, copy=key is not None), c0, k, dtype, cfg, config.ft_mode, thr,
-                          threads, gemm_hook, update_hook, graph=graph)
+        own = src is not x  # our own upload: no aliasing of a caller's tensor
+        eng = LloydEngine(src if own else E.to_dev(x, copy=key is not None), c0, k, dtype, cfg,
+                          config.ft_mode, thr, threads, gemm_hook, update_hook, graph=graph)
         if key is not None:
             _FIT_CACHE.update(key=key, eng=eng)
     history = []

@@ -370,15 +370,41 @@ def test_candidate_overflow_rows_go_exact():
 
 
 @pytest.mark.parametrize("m,d,k,prec", [(20000, 32, 64, "single"), (5000, 100, 40, "double"),
-                                        (3000, 5, 17, "single")])
+                                        (3000, 5, 17, "single"), (4000, 300, 24, "single"),
+                                        (2500, 1030, 9, "double"), (200000, 16, 128, "single")])
 def test_kmeanspp_seeding_matches_reference(m, d, k, prec):
-    """GPU D^2 seeding (float64 pairwise row reduce on the device, the
-    reference's Generator draws and cumsum/searchsorted on the host) picks
-    exactly the reference's centroids (kmeans.py:86-103)."""
+    """GPU D^2 seeding (float64 pairwise feature reduce for any D, device
+    pairwise total, bit-exact device searchsorted over numpy's sequential
+    cumsum; only the reference's Generator draws on the host) picks exactly
+    the reference's centroids (kmeans.py:86-103)."""
     x, _, _ = P.gaussian_mixture(m, d, k, 0.3, precision=prec, seed=5)
     got = P.init_centroids(x, k, seed=9, method="kmeanspp")
     ref = O.init_centroids(x, k, 9, "kmeanspp")
     assert got.tobytes() == ref.tobytes()
+
+
+def test_kmeanspp_search_ambiguity_replay():
+    """ftk_kpp_search on adversarial prefixes: r placed exactly on, and one
+    ulp around, sequential-cumsum boundaries (the certified scan cannot
+    decide these; the exact replay must) -- against numpy's searchsorted."""
+    import torch
+
+    from paper_2408_01391_b200 import _engine as E
+
+    rng = np.random.default_rng(3)
+    d2 = rng.random(300_001) * rng.choice([1e-8, 1.0, 1e8], 300_001)
+    d2[1000:1100] = 0.0  # a flat stretch of the cumsum
+    cs = np.cumsum(d2)
+    dev = torch.from_numpy(d2).cuda()
+    pick = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nrep = torch.zeros(1, dtype=torch.int64, device="cuda")
+    rs = [0.0, cs[0], cs[999], cs[1050], cs[150_000], np.nextafter(cs[150_000], 0),
+          np.nextafter(cs[150_000], np.inf), cs[-1], cs[-1] * 2, float(rng.random() * cs[-1])]
+    for r in rs:
+        E.kpp_search_dev(dev, float(r), pick, nrep)
+        want = min(int(np.searchsorted(cs, r, side="right")), len(d2) - 1)
+        assert int(pick.item()) == want, (r, int(pick.item()), want)
+    assert int(nrep.item()) >= 1  # the on-boundary draws went through the exact replay
 
 
 @pytest.mark.parametrize("ft", ["off", "abft"])
@@ -493,3 +519,42 @@ def test_fit_workspace_reuse_equals_fresh(ft, inject, monkeypatch):
     K.clear_fit_cache()
     fresh = fits()
     assert cached == fresh
+
+
+def test_graph_steps_measure_phase_times():
+    """timings_ on graph steps are measured per step (events around the
+    assignment and update graph replays), not copies of an eager step's."""
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    x, _, _ = P.gaussian_mixture(50_000, 64, 64, 0.25, precision="single", seed=4)
+    c0 = P.init_centroids(x, 64, seed=4, method="random-sample")
+    eng = LloydEngine(P._engine.to_dev(x), c0, 64, np.float32, P.default_config(np.float32), "off",
+                      P.Threshold.default_for(np.float32), 8, graph=True)
+    seen = []
+    for it in range(12):
+        eng.step(it, more=(lambda it=it: it < 11))
+        seen.append((eng.assign_ms, eng.update_ms))
+    eng.close()
+    graph = seen[2:]
+    assert all(a > 0 and u > 0 for a, u in graph)
+    assert len(set(graph)) > 1  # measured each step, not repeated
+    r = P.lloyd(x, P.KMeansConfig(k=64, max_iters=12, tol=0.0, seed=4, init="random-sample"))
+    assert 0 < r.timings["assign_ns"] + r.timings["update_ns"] < r.timings["total_ns"]
+
+
+@pytest.mark.parametrize("nbytes", [(8 << 20) + 4, (48 << 20) + 12, (200 << 20) - 4])
+def test_staged_pageable_upload(nbytes):
+    """ftk_h2d (parallel pinned staging, chunked DMA) delivers every byte of a
+    pageable numpy buffer, and work queued after it sees the data."""
+    import torch
+
+    from paper_2408_01391_b200 import _engine as E
+
+    a = np.random.default_rng(nbytes).standard_normal(nbytes // 4).astype(np.float32)
+    dst = torch.empty(a.shape, dtype=torch.float32, device="cuda")
+    E.upload_into(dst, a)
+    s = dst.sum()  # queued behind the upload on the current stream
+    assert np.array_equal(dst.cpu().numpy(), a)
+    assert abs(float(s) - float(a.astype(np.float64).sum())) < 1e-2 * a.size ** 0.5
+    t = E.to_dev(a)
+    assert np.array_equal(t.cpu().numpy(), a)
