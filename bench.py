@@ -323,7 +323,9 @@ def run_ours(args, rank, world):
         import torch.distributed as dist
 
         dist.init_process_group(os.environ.get("FTK_DIST_BACKEND", "nccl"))
-    lo, hi = rank * N_ROWS // world, (rank + 1) * N_ROWS // world
+    from paper_2408_01391_b200.shard import ShardComm
+
+    lo, hi = ShardComm.shard_bounds(N_ROWS, world, rank)
     if args.config == "c2":
         x = make_data(cfg)
         x_t = E.to_dev(x[lo:hi])
@@ -337,11 +339,7 @@ def run_ours(args, rank, world):
             torch.distributed.broadcast(c0, 0)
     tcfg = default_config(np.float32)
     thr = P.Threshold.default_for(np.float32)
-    comm = None
-    if world > 1:
-        from paper_2408_01391_b200.shard import ShardComm
-
-        comm = ShardComm(lo)
+    comm = ShardComm(lo) if world > 1 else None
 
     def engine(ft_mode, hook=None):
         return LloydEngine(x_t, c0, K, np.float32, tcfg, ft_mode, thr, 64,
@@ -562,6 +560,7 @@ def run_ours(args, rank, world):
                    "variant": P.gemm.get_variant()},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": tf32_peak,
                      "unit": "TFLOP/s", "frac": achieved / tf32_peak, "peak_note": peak_note,
+                     "frac_vs_bf16_half": achieved / (_peaks()[1] / 2.0),
                      "kernel": "pair_screen_kernel<CHK> (cta_group::2 tcgen05 tf32 screen + "
                                "fused argmin/certificate/exact refine/ABFT)",
                      "kernel_ms": kern_ms, "traffic": traffic,

@@ -32,31 +32,39 @@
 
 namespace ftk {
 
-// numpy pairwise_sum leaf over f(0..n-1), n <= 128 (loops_utils.h.src)
+// numpy pairwise_sum leaf over f(off..off+n-1), n <= 128 (loops_utils.h.src).
+// f.group(i) is called before each run of up to 8 consecutive elements
+// starting at a multiple of 8 (leaf offsets are multiples of 8), so a staged
+// source can fetch once per group; f(i) returns element i.
 template <class F>
-__device__ __forceinline__ double pw_leaf(const F &f, int64_t off, int64_t n) {
+__device__ __forceinline__ double pw_leaf(F &f, int64_t off, int64_t n) {
     if (n < 8) {
+        f.group(off);
         double s = 0.0;
         for (int64_t i = 0; i < n; ++i) s = __dadd_rn(s, f(off + i));
         return s;
     }
     double r[8];
+    f.group(off);
 #pragma unroll
     for (int j = 0; j < 8; ++j) r[j] = f(off + j);
     int64_t i = 8;
+#pragma unroll 1
     for (; i < n - (n % 8); i += 8) {
+        f.group(off + i);
 #pragma unroll
         for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], f(off + i + j));
     }
     double s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    if (i < n) f.group(off + i);
     for (; i < n; ++i) s = __dadd_rn(s, f(off + i));
     return s;
 }
 
 // recursive halving (n2 = n/2 rounded down to a multiple of 8), post-order
 template <class F>
-__device__ double pw_sum(const F &f, int64_t n) {
+__device__ double pw_sum(F &f, int64_t n) {
     if (n <= 128) return pw_leaf(f, 0, n);
     struct Fr { int64_t off, n; int state; double left; };
     Fr st[40];
@@ -92,26 +100,59 @@ __device__ double pw_sum(const F &f, int64_t n) {
 // d2[i] = pairwise_sum_f((x64[i,f] - x64[pick,f])^2), then np.minimum with the
 // previous d2 unless `first`.  pick: `host_pick` if >= 0, else *pick_dev.
 // Block 0 records the pick in picks[c].
+//
+// One warp per 32 rows, lane = row.  Every lane walks the same feature
+// sequence (the pairwise schedule depends only on d), so the warp stages its
+// 32 rows 32 features at a time in shared memory with coalesced 128-byte row
+// loads, and each lane reads its own row back from the staged tile.
 template <typename T>
-__global__ void kpp_update_kernel(const T *x, int64_t m, int64_t d, int64_t host_pick,
-                                  const int64_t *pick_dev, int first, double *d2, int64_t *picks,
-                                  int64_t c) {
+struct StagedSq {
+    const T *x, *cr;
+    int64_t d, r0;
+    int rows, lane;
+    T (*tile)[33];
+    int64_t loaded;
+    __device__ void group(int64_t f) {
+        const int64_t ch = f >> 5;
+        if (ch == loaded) return;  // warp-uniform
+        __syncwarp();
+        const int64_t col = ch * 32 + lane;
+#pragma unroll 4
+        for (int rr = 0; rr < 32; ++rr)
+            tile[rr][lane] = (rr < rows && col < d) ? x[(r0 + rr) * d + col] : T(0);
+        __syncwarp();
+        loaded = ch;
+    }
+    __device__ double operator()(int64_t f) const {
+        const double df = __dsub_rn(double(tile[lane][f & 31]), double(cr[f]));
+        return __dmul_rn(df, df);
+    }
+};
+
+template <typename T, int W>
+__global__ void __launch_bounds__(W * 32) kpp_update_kernel(const T *x, int64_t m, int64_t d,
+                                                            int64_t host_pick, const int64_t *pick_dev,
+                                                            int first, double *d2, int64_t *picks,
+                                                            int64_t c) {
+    __shared__ T tile_all[W][32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t pick = host_pick >= 0 ? host_pick : *pick_dev;
     if (picks && blockIdx.x == 0 && threadIdx.x == 0) picks[c] = pick;
-    const T *cr = x + pick * d;
-    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
-         i += int64_t(gridDim.x) * blockDim.x) {
-        const T *xr = x + i * d;
-        auto sq = [&](int64_t f) {
-            const double df = __dsub_rn(double(xr[f]), double(cr[f]));
-            return __dmul_rn(df, df);
-        };
-        const double s = pw_sum(sq, d);
-        if (first) {
-            d2[i] = s;
-        } else {
-            const double o = d2[i];
-            d2[i] = (s != s || o != o) ? s + o : (s < o ? s : o);  // np.minimum (NaN propagates)
+    StagedSq<T> f{x, x + pick * d, d, 0, 0, lane, tile_all[w], -1};
+    const int64_t ngroups = (m + 31) / 32;
+    for (int64_t g = int64_t(blockIdx.x) * W + w; g < ngroups; g += int64_t(gridDim.x) * W) {
+        f.r0 = g * 32;
+        f.rows = m - f.r0 < 32 ? int(m - f.r0) : 32;
+        f.loaded = -1;
+        const double s = pw_sum(f, d);
+        if (lane < f.rows) {
+            const int64_t i = f.r0 + lane;
+            if (first) {
+                d2[i] = s;
+            } else {
+                const double o = d2[i];
+                d2[i] = (s != s || o != o) ? s + o : (s < o ? s : o);  // np.minimum (NaN propagates)
+            }
         }
     }
 }
@@ -188,9 +229,11 @@ template <typename T>
 static int update_launch(const void *x, int64_t m, int64_t d, int64_t host_pick,
                          const int64_t *pick_dev, int first, double *d2, int64_t *picks, int64_t c,
                          cudaStream_t st) {
-    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((m + 255) / 256, 148 * 16)));
-    kpp_update_kernel<T><<<grid, 256, 0, st>>>(static_cast<const T *>(x), m, d, host_pick, pick_dev,
-                                               first, d2, picks, c);
+    constexpr int W = sizeof(T) == 8 ? 4 : 8;  // warps per block (staging tile <= 34 KB)
+    const int64_t groups = (m + 31) / 32;
+    const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>((groups + W - 1) / W, 148 * 16)));
+    kpp_update_kernel<T, W><<<grid, W * 32, 0, st>>>(static_cast<const T *>(x), m, d, host_pick, pick_dev,
+                                                     first, d2, picks, c);
     FTK_LAUNCHED("kpp_update_kernel");
     return FTK_OK;
 }

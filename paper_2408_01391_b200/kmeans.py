@@ -362,7 +362,8 @@ class LloydEngine:
         # state across replays.  Eager steps remain for iterations with
         # scheduled flips, DMR, update-site hooks or multi-GPU.
         # (only the fp32 CTA-pair assignment is free of host synchronisation)
-        self.use_graph = bool(graph) and dist is None and ft_mode != "abft+dmr" and \
+        self.use_graph = bool(graph) and (dist is None or dist.capturable) and \
+            ft_mode != "abft+dmr" and \
             update_hook is NOOP_HOOK and self.dtype == np.float32 and \
             8 <= x_t.shape[1] <= 256 and x_t.shape[1] % 4 == 0 and get_variant() != "exact"
         self.graphs = [None, None]
@@ -435,6 +436,11 @@ class LloydEngine:
             E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
             E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
         sa, ca, _, _ = E.update_sums_dev(self.x_t, A.labels[self.slot], self.k, dmr=False)
+        if self.dist is not None:
+            # row shards: ONE packed all-reduce of the partial sums, counts,
+            # inertia and changed-label count (NCCL, captured in the graph)
+            cur.wait_stream(side)
+            self.dist.reduce_partials(sa, ca, self.ctl_f64, self.ctl_i32)
         new_cent = self.cent_buf[1 - self.cbuf]
         E.finalize_dev(sa, ca, self.dtype, out=new_cent, n_empty=self.ctl_i32[1:2])
         self.counts_buf.copy_(ca)
@@ -616,7 +622,10 @@ class LloydEngine:
                 t.cuda.current_stream().synchronize()
                 self._ahead = None
                 old = self._cent_prev
-            E.reseed_dev(self.x_t, self.counts_buf, self.sq, new_cent)
+            if self.dist is not None:
+                self.dist.reseed(self.x_t, self.counts_buf, self.sq, new_cent)
+            else:
+                E.reseed_dev(self.x_t, self.counts_buf, self.sq, new_cent)
             E.movement_dev(new_cent, old, self.eps, self.ctl_f64[1:2])
             # movement only: ctl_f64[0] may already hold the queued step's inertia
             self.ctl_host[1:2].copy_(self.ctl_f64[1:2])
@@ -710,6 +719,8 @@ class LloydEngine:
         rep = A.finish(self.gemm_hook, iteration, inj)
         if rep is not None:
             self.report.merge(rep)
+        if self.dist is not None:  # the inertia of every shard
+            self.dist.all_reduce_(self.ctl_f64[0:1])
         # int64 on the device, one D2H into page-locked memory (the pageable
         # copy plus a host-side astype cost ~2 ms at c2)
         t = self.t

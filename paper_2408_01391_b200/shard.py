@@ -6,9 +6,16 @@ only exchange per iteration is ONE packed all-reduce of
 ``[per-cluster float64 sums (K*D) | counts (K, as float64: exact below 2^53)
 | partial inertia | changed-label count]`` (4.2 MB at K=4096, D=128) -- after
 it every rank runs the identical finalize, so the centroids stay bit-identical
-across ranks.  The rare empty-cluster reseed is a MAXLOC: every rank offers
-its shard's farthest point, ties resolve to the lowest global row index
-(np.argmax's first-maximum rule, kmeans.py:197-206).
+across ranks.  With the NCCL backend the pack, the all-reduce and the unpack
+are captured in the step's CUDA graph (``capturable``): a sharded step is one
+graph replay like a single-GPU step.  The rare empty-cluster reseed is a
+MAXLOC: every rank offers its shard's farthest point, ties resolve to the
+lowest global row index (np.argmax's first-maximum rule, kmeans.py:197-206).
+
+Shards start on multiples of ``ALIGN`` rows, so the reference's logical
+fault-tile grid (bm = 32 or 64 rows) maps onto shards without splitting a
+tile, and every shard's tiles are the global tiles offset by
+``row_offset // bm``.
 
 Parity caveat: the float64 sums are summed per shard then across ranks, so
 for world_size > 1 the summation association differs from the reference's
@@ -17,6 +24,8 @@ row-local and exact given identical centroids).
 """
 
 from __future__ import annotations
+
+ALIGN = 256
 
 
 class ShardComm:
@@ -28,24 +37,44 @@ class ShardComm:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.row_offset = int(row_offset)
+        # NCCL collectives can be captured in a CUDA graph; gloo cannot
+        self.capturable = dist.get_backend(group) == "nccl"
+        self._buf = None
 
     @staticmethod
-    def shard_bounds(n_rows, world, rank):
-        return rank * n_rows // world, (rank + 1) * n_rows // world
+    def shard_bounds(n_rows, world, rank, align=ALIGN):
+        """[lo, hi) of `rank`: near-equal shards whose starts are multiples of
+        `align` rows (the last shard takes the remainder)."""
+        per = -(-n_rows // world)
+        per = -(-per // align) * align
+        lo = min(n_rows, rank * per)
+        return lo, min(n_rows, lo + per)
+
+    def all_reduce_(self, t):
+        self.dist.all_reduce(t, group=self.group)
+        return t
 
     def reduce_partials(self, sums, counts, ctl_f64, ctl_i32, iteration=0):
         """sums (K, D) f64, counts (K,) i64, ctl_f64[0] = partial inertia,
-        ctl_i32[0] = this shard's labels-unchanged flag; all in place."""
+        ctl_i32[0] = this shard's labels-unchanged flag; all in place.  No
+        allocation after the first call (graph-capturable)."""
         import torch
 
         k, d = sums.shape
-        changed = (1 - ctl_i32[0:1]).to(torch.float64)
-        buf = torch.cat([sums.reshape(-1), counts.to(torch.float64), ctl_f64[0:1], changed])
+        n = k * d + k + 2
+        if self._buf is None or self._buf.numel() != n or self._buf.device != sums.device:
+            self._buf = torch.empty(n, dtype=torch.float64, device=sums.device)
+        buf = self._buf
+        kd = k * d
+        buf[:kd].view(k, d).copy_(sums)
+        buf[kd:kd + k].copy_(counts)
+        buf[kd + k:kd + k + 1].copy_(ctl_f64[0:1])
+        buf[kd + k + 1:].copy_(ctl_i32[0:1]).neg_().add_(1.0)  # changed = 1 - unchanged
         self.dist.all_reduce(buf, group=self.group)
-        sums.copy_(buf[: k * d].view(k, d))
-        counts.copy_(buf[k * d: k * d + k].to(torch.int64))
-        ctl_f64[0:1].copy_(buf[k * d + k: k * d + k + 1])
-        ctl_i32[0:1].copy_((buf[k * d + k + 1:] == 0).to(ctl_i32.dtype))
+        sums.copy_(buf[:kd].view(k, d))
+        counts.copy_(buf[kd:kd + k])
+        ctl_f64[0:1].copy_(buf[kd + k:kd + k + 1])
+        ctl_i32[0:1].copy_(buf[kd + k + 1:].eq(0.0))
 
     def reseed(self, x_t, counts, sq, cent):
         """Empty clusters (ascending) take successive global farthest points."""

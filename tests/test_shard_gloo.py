@@ -52,7 +52,7 @@ def _worker(rank, port, out):
 
         x, labels, sq = _data()
         k = 6
-        lo, hi = ShardComm.shard_bounds(len(x), WORLD, rank)
+        lo, hi = ShardComm.shard_bounds(len(x), WORLD, rank, align=1)
         comm = ShardComm(lo)
         xs, ls = x[lo:hi], labels[lo:hi]
         sums = torch.zeros((k, x.shape[1]), dtype=torch.float64)
@@ -92,3 +92,96 @@ def test_sharded_partials_and_reseed_match_single_process():
     # every rank holds the same result (the all-reduce is the only exchange)
     assert all(np.array_equal(res[0][0], res[r][0]) for r in range(WORLD))
     assert all(np.array_equal(res[0][4], res[r][4]) for r in range(WORLD))
+
+
+def test_shard_bounds_aligned_and_covering():
+    from paper_2408_01391_b200.shard import ALIGN, ShardComm
+
+    for n, w in [(1_000_000, 8), (100_000_000, 8), (1000, 3), (300, 2), (5, 4)]:
+        b = [ShardComm.shard_bounds(n, w, r) for r in range(w)]
+        assert b[0][0] == 0 and b[-1][1] == n
+        assert all(b[r][1] == b[r + 1][0] for r in range(w - 1))
+        assert all(lo % ALIGN == 0 or lo == n for lo, _ in b)
+
+
+# ---- the sharded ENGINE (GPU): two ranks on one GPU over gloo (eager
+# steps), and one rank over NCCL with the all-reduce captured in the graphs
+
+
+def _engine_run(x, c0, k, steps, dist=None, graph=False):
+    from paper_2408_01391_b200 import _engine as E
+    from paper_2408_01391_b200.kmeans import LloydEngine
+    from paper_2408_01391_b200.tiles import default_config
+    from paper_2408_01391_b200.abft import Threshold
+
+    eng = LloydEngine(E.to_dev(x), c0, k, np.float32, default_config(np.float32), "abft",
+                      Threshold.default_for(np.float32), 8, dist=dist, graph=graph)
+    hist = []
+    for it in range(steps):
+        inertia, _, moved = eng.step(it, more=(lambda it=it: it + 1 < steps))
+        hist.append((inertia, moved))
+    labels, inertia = eng.final(steps)
+    cent = E.to_host(eng.cent)
+    eng.close()
+    return labels, cent, hist, inertia
+
+
+def _engine_data():
+    rng = np.random.default_rng(11)
+    centers = rng.random((40, 24)) * 10
+    lab = rng.integers(0, 40, 60_000)
+    x = (centers[lab] + 0.3 * rng.standard_normal((60_000, 24))).astype(np.float32)
+    c0 = np.ascontiguousarray(x[rng.choice(len(x), 40, replace=False)])
+    return x, c0
+
+
+def _engine_worker(rank, port, backend, world, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
+    try:
+        from paper_2408_01391_b200.shard import ShardComm
+
+        x, c0 = _engine_data()
+        lo, hi = ShardComm.shard_bounds(len(x), world, rank)
+        comm = ShardComm(lo)
+        labels, cent, hist, inertia = _engine_run(x[lo:hi], c0, 40, 10, dist=comm,
+                                                  graph=backend == "nccl")
+        out[rank] = (lo, labels, cent, hist, inertia)
+    finally:
+        dist.destroy_process_group()
+
+
+def _cuda_ok():
+    return torch.cuda.is_available()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
+def test_sharded_engine_matches_single_process(backend, world):
+    """LloydEngine(dist=ShardComm): gloo world 2 (eager steps, both ranks on
+    cuda:0) and NCCL world 1 (the packed all-reduce captured in the step
+    graphs) reproduce the single-process engine: labels identical,
+    centroids / inertia equal to float64 re-association (world 2) or bitwise
+    (world 1)."""
+    if not _cuda_ok():
+        pytest.skip("needs a CUDA device")
+    x, c0 = _engine_data()
+    ref_lab, ref_c, ref_hist, ref_inertia = _engine_run(x, c0, 40, 10, graph=True)
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_engine_worker, args=(_free_port(), backend, world, out), nprocs=world, join=True)
+        res = dict(out)
+    labels = np.concatenate([res[r][1] for r in range(world)])
+    assert np.array_equal(labels, ref_lab)
+    for r in range(world):
+        _, _, cent, hist, inertia = res[r]
+        if world == 1:
+            assert cent.tobytes() == ref_c.tobytes()
+            assert hist == ref_hist and inertia == ref_inertia
+        else:
+            np.testing.assert_allclose(cent, ref_c, rtol=1e-6, atol=0)
+            assert abs(inertia - ref_inertia) <= 1e-12 * ref_inertia
+            assert all(abs(a[0] - b[0]) <= 1e-12 * b[0] for a, b in zip(hist, ref_hist))
+    assert all(np.array_equal(res[0][2], res[r][2]) for r in range(world))
