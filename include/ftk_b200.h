@@ -98,6 +98,24 @@ int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info
  * modified while registered; pass x = NULL to unregister.  The reference has
  * no counterpart (its kernels recompute nothing across calls). */
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info);
+/* Label hint for the next assignments on this context: labels (m int32,
+ * device) of the previous Lloyd iteration.  The narrow screen (d > 256,
+ * k + 4 <= 256) computes the exact reference value of the hinted centroid
+ * while X streams through shared memory, so rows whose label is unchanged
+ * need no second read of X.  Only a speed hint: any content (even out of
+ * range) gives the same results.  Used while m matches; NULL clears it.  The
+ * caller keeps the buffer alive while it is set.  No reference counterpart. */
+int ftk_ctx_set_label_hint(ftk_ctx *ctx, const int32_t *labels, int64_t m);
+
+/* Context options.  FTK_OPT_INJ_REPLAY (default 1): the logical row blocks
+ * carrying scheduled flips are replayed by the exact checked kernel after a
+ * screened checked assignment, so their detection events are the reference's
+ * own.  0 (validation of the in-kernel correction): the screen's own
+ * detect/locate/correct result stands and it records an event for every
+ * detection (narrow screen). */
+#define FTK_OPT_INJ_REPLAY 1
+int ftk_ctx_set_option(ftk_ctx *ctx, int option, int64_t value);
+
 /* Number of scratch (re)allocations on this context so far: a CUDA graph
  * captured from this context's launches is stale once it changes. */
 int64_t ftk_ctx_generation(ftk_ctx *ctx);

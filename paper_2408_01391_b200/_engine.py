@@ -262,6 +262,19 @@ class DevEvents:
 
 
 # ------------------------------------------------------------ kernels ----
+def set_label_hint(labels_t, m):
+    """Previous-iteration labels as the assignment's speed hint
+    (ftk_ctx_set_label_hint); None clears it."""
+    N.check(N.load().ftk_ctx_set_label_hint(ctx(), None if labels_t is None else ptr(labels_t),
+                                            int(m) if labels_t is not None else 0),
+            "ftk_ctx_set_label_hint")
+
+
+def set_inj_replay(on):
+    """FTK_OPT_INJ_REPLAY: exact replay of blocks with scheduled flips (default on)."""
+    N.check(N.load().ftk_ctx_set_option(ctx(), 1, 1 if on else 0), "ftk_ctx_set_option")
+
+
 def row_sq_norms_dev(x_t):
     t = _torch()
     out = t.empty(x_t.shape[0], dtype=x_t.dtype, device=x_t.device)

@@ -23,6 +23,7 @@ SOURCES = {
     "update.cu": ["--fmad=false"],
     "tc.cu": [],
     "tc_pair.cu": [],
+    "tc_narrow.cu": [],
     "dscreen.cu": [],
     "kpp.cu": [],
     "h2d.cu": [],

@@ -169,6 +169,21 @@ int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const fl
     return FTK_OK;
 }
 
+int ftk_ctx_set_label_hint(ftk_ctx *ctx, const int32_t *labels, int64_t m) {
+    if (!ctx || m < 0) { set_error("bad ctx/m"); return FTK_ERR_ARG; }
+    ctx->hint = labels;
+    ctx->hint_m = labels ? m : 0;
+    return FTK_OK;
+}
+
+int ftk_ctx_set_option(ftk_ctx *ctx, int option, int64_t value) {
+    if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    switch (option) {
+        case FTK_OPT_INJ_REPLAY: ctx->inj_replay = value != 0; return FTK_OK;
+        default: set_error("unknown option"); return FTK_ERR_ARG;
+    }
+}
+
 int ftk_row_sq_norms(ftk_ctx *ctx, int dtype, const void *x, int64_t m, int64_t n, void *out,
                      void *stream) {
     (void)ctx;

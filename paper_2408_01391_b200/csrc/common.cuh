@@ -44,7 +44,7 @@ struct Scratch {
 
 struct ftk_ctx {
     int device = 0;
-    ftk::Scratch slots[24];
+    ftk::Scratch slots[32];
     // per-fit row bounds registered by ftk_ctx_set_rows (X constant for the fit)
     const void *rows_x = nullptr;
     int64_t rows_m = 0, rows_d = 0;
@@ -57,6 +57,11 @@ struct ftk_ctx {
     int64_t generation = 0;  // scratch (re)allocations: captured graphs go stale
     unsigned long long *abft_total = nullptr;  // cumulative TC/DMMA row-checksum flags (device)
     void *h2d = nullptr;  // staged pageable upload: pinned buffers, streams (h2d.cu)
+    // label hint of the next assignment (ftk_ctx_set_label_hint): the previous
+    // iteration's labels, used by the narrow screen to pick the exact chain
+    const int32_t *hint = nullptr;
+    int64_t hint_m = 0;
+    int inj_replay = 1;  // FTK_OPT_INJ_REPLAY: replay blocks with scheduled flips exactly
 };
 
 namespace ftk {
@@ -91,6 +96,7 @@ enum ScratchSlot {
     SLOT_DS_G = 21,       // float64 screen: gathered fallback rows
     SLOT_EXACT_SPLIT = 22,  // per-(row, column split) argmin partials of the exact kernel
     SLOT_KPP = 23,          // k-means++: prefix scan of d2, counters, CUB temp
+    SLOT_NARROW = 24,       // narrow screen: augmented centroids, tolerances, winner-pass rows
 };
 
 // ------------------------------------------------------- float helpers --

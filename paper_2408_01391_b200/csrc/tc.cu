@@ -730,6 +730,32 @@ static int make_map(CUtensorMap *map, const float *base, int64_t rows, int64_t c
     return FTK_OK;
 }
 
+int make_tc_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols, uint32_t box_rows) {
+    return make_map(map, base, rows, cols, box_rows);
+}
+
+// Unswizzled 2-D map with an arbitrary box (cols * 4 bytes a multiple of 16).
+int make_plain_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
+                   uint32_t box_cols, uint32_t box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return FTK_ERR_CUDA;
+    }
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows < 1 ? 1 : rows)};
+    cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(float)};
+    cuuint32_t box[2] = {box_cols, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims,
+                     strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (plain) failed (" + std::to_string(int(r)) + ")");
+        return FTK_ERR_CUDA;
+    }
+    return FTK_OK;
+}
+
 template <int BN, bool SPLIT, bool CHK>
 static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &mxl,
                          const CUtensorMap &mc, const CUtensorMap &mcl, cudaStream_t st) {
@@ -790,10 +816,12 @@ int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
     // reads X rows from global memory and is latency-bound (c3 D=512 K=16:
     // pass 1 2.0 ms, 0.49 ms without the refine), no faster than the exact
     // kernel yet.  The resident-X kernels stop at 256.
+    // d > 256 with k + 4 <= 256: the streamed-X narrow screen (tc_narrow.cu)
     const char *sx = getenv("FTK_TC_SX");
     const bool sx_on = sx && atoi(sx) == 1;
     return dtype == FTK_F32 && d >= 4 && d % 4 == 0 &&
-           (d <= TC_MAX_D || (sx_on && k <= PAIR_BN && d <= TC_SX_MAX_D)) && k >= 1 && m >= 1 &&
+           (d <= TC_MAX_D || (sx_on && k <= PAIR_BN && d <= TC_SX_MAX_D) ||
+            (!sx_on && narrow_supported(k, d, true))) && k >= 1 && m >= 1 &&
            m < (int64_t(1) << 31) && k < (int64_t(1) << 24);
 }
 
@@ -981,6 +1009,24 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             P.inj_after = ia;
         }
     }
+    {
+        const char *sx = getenv("FTK_TC_SX");
+        if (!split_only && raw == nullptr && d > TC_MAX_D && !(sx && atoi(sx) == 1) &&
+            narrow_supported(k, d, ft != nullptr)) {
+            // wide rows, few centroids: the streamed-X narrow screen
+            NarrowIn in{};
+            in.x = xf; in.y = yf; in.yn = ynf; in.m = m; in.k = k; in.d = d;
+            in.out_idx = out_idx; in.out_val = outv;
+            in.cmax2 = P.cmax2; in.ecmax2 = P.ecmax2;
+            in.fb_rows = rows1; in.cnt = cnt; in.ft = ft;
+            in.inj_col = P.inj_col; in.inj_before = P.inj_before; in.inj_after = P.inj_after;
+            int rcn = narrow_assign_run(ctx, in, st);
+            if (rcn) return rcn;
+            if (ft && ft->inj && ft->inj->n > 0 && ctx->inj_replay)
+                return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
+            return FTK_OK;
+        }
+    }
     CUtensorMap mx, mc;
     float *pair_fb_thr = nullptr;
     unsigned long long *pair_fb_seed = nullptr;
@@ -1119,7 +1165,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             ctx->stat_dev[0] = cnt;          // read lazily by tc_last_fallback
             ctx->stat_dev[1] = ccount + 1;
             ctx->stat_dev[2] = ft ? cnt + 2 : nullptr;
-            if (ft && ft->inj && ft->inj->n > 0)
+            if (ft && ft->inj && ft->inj->n > 0 && ctx->inj_replay)
                 return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
             return FTK_OK;
         }
@@ -1223,7 +1269,7 @@ template int emulate_injected_blocks<double>(ftk_ctx *, const double *, const do
 
 // Device time of the last CTA-pair pass-1 launch (ms), -1 if none.
 float tc_last_pass1_ms(ftk_ctx *ctx) {
-    if (!ctx->time_ev[0] || ctx->last_path != 1) return -1.0f;
+    if (!ctx->time_ev[0] || (ctx->last_path != 1 && ctx->last_path != 2)) return -1.0f;
     float ms = -1.0f;
     if (cudaEventSynchronize(ctx->time_ev[1]) != cudaSuccess) return -1.0f;
     cudaEventElapsedTime(&ms, ctx->time_ev[0], ctx->time_ev[1]);

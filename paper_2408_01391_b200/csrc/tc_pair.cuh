@@ -75,6 +75,22 @@ struct TcFt {  // checksum-protected (abft) mode of a screened assignment
     ftk_events *ev;
 };
 
+// streamed-X narrow screen (tc_narrow.cu): K + 4 <= 256, any D % 4 == 0
+struct NarrowIn {
+    const float *x, *y, *yn;
+    int64_t m, k, d;
+    int32_t *out_idx;
+    float *out_val;
+    const float *cmax2, *ecmax2;  // device scalars (tc_prep_kernel)
+    int32_t *fb_rows;             // m + 1 entries
+    unsigned *cnt;                // [0] exact rows, [2] abft flags, [3] winner rows, [4] corrected
+    const TcFt *ft;               // null: FT off
+    const int32_t *inj_col;
+    const float *inj_before, *inj_after;
+};
+bool narrow_supported(int64_t k, int64_t d, bool chk);
+int narrow_assign_run(ftk_ctx *ctx, const NarrowIn &in, cudaStream_t st);
+
 // The logical row blocks that carry scheduled flips are recomputed by the
 // exact checked kernel (the reference's detection, location, correction and
 // event record, bit for bit) and overwrite the screened results of those rows.

@@ -250,7 +250,8 @@ class _DeviceAssign:
         # per buffer parity: min_dists and the event ring, so the next step can
         # run while the host still reads this one's (LloydEngine._graph_step)
         self._md = [t.empty(m, dtype=x_t.dtype, device=x_t.device) for _ in range(2)]
-        self.labels = [t.empty(m, dtype=t.int32, device=x_t.device) for _ in range(2)]
+        # -1: no label yet (the first pass has no hint for the narrow screen)
+        self.labels = [t.full((m,), -1, dtype=t.int32, device=x_t.device) for _ in range(2)]
         mult = max(1, min(threads, self.nbi))
         # storage for a few hundred injected flips per pass, so eager injected
         # steps do not move the ring that captured graph replays write into
@@ -271,10 +272,16 @@ class _DeviceAssign:
         if self.checked:
             self.events.set_cap(self.ev_cap(inj.cap if sinj is not None else (inj.n if inj else 0)))
             self.events.reset()
-        E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=get_variant(), inj=inj,
-                     checked=self.checked, delta_rel=self.delta_rel, abs_tol=self.abs_tol,
-                     iteration=iteration, events=self.events, out_idx=self.labels[slot],
-                     out_val=self.md)
+        # the other parity holds the previous iteration's labels: the narrow
+        # screen's exact-chain hint (a speed hint only, results never depend on it)
+        E.set_label_hint(self.labels[1 - slot], self.m)
+        try:
+            E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=get_variant(), inj=inj,
+                         checked=self.checked, delta_rel=self.delta_rel, abs_tol=self.abs_tol,
+                         iteration=iteration, events=self.events, out_idx=self.labels[slot],
+                         out_val=self.md)
+        finally:
+            E.set_label_hint(None, 0)
         return inj
 
     def ev_cap(self, n_inj):
@@ -324,6 +331,13 @@ class _StepGraph:
         N.load().ftk_add_launches(self.launches)
 
 
+def _graphable_shape(d, k):
+    """fp32 shapes whose screened assignment is free of host synchronisation:
+    the CTA-pair screen (8 <= d <= 256) and the narrow screen (d > 256,
+    k + 4 <= 256), both with d % 4 == 0."""
+    return d % 4 == 0 and (8 <= d <= 256 or (d > 256 and k + 4 <= 256))
+
+
 class LloydEngine:
     """Device-resident Lloyd state: one ``step`` per iteration (assign ->
     inertia -> label compare -> update -> finalize -> movement) with a single
@@ -365,7 +379,7 @@ class LloydEngine:
         self.use_graph = bool(graph) and (dist is None or dist.capturable) and \
             ft_mode != "abft+dmr" and \
             update_hook is NOOP_HOOK and self.dtype == np.float32 and \
-            8 <= x_t.shape[1] <= 256 and x_t.shape[1] % 4 == 0 and get_variant() != "exact"
+            _graphable_shape(x_t.shape[1], k) and get_variant() != "exact"
         self.graphs = [None, None]
         # injected passes replay their own graphs, the schedule staged into
         # fixed device arrays (count on the device) before the replay
