@@ -239,51 +239,62 @@ __global__ void __launch_bounds__(NR_THREADS, 1)
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 if (work) {
+                    // all 16 shared-memory loads of the stage first, then the
+                    // stage is released, then the arithmetic: the dependent
+                    // fp32 chain (32 FADDs) runs while the producer refills.
+                    // Features past D are zero in both TMA slices, and x*c = 0
+                    // leaves the chain unchanged (acc is never -0).
                     const unsigned char *xs = sS + size_t(stage) * STG + uint32_t(r) * 128u;
                     const int pp = p < 0 ? 0 : p;
                     const unsigned char *cs = sS + size_t(stage) * STG + C_OFF + uint32_t(pp) * 128u;
-                    // transposed slice: element (f, p) at f * kt + p -- for a fixed
-                    // feature the 32 lanes' centroids sit in distinct banks
                     const float *ct = reinterpret_cast<const float *>(sS + size_t(stage) * STG + CT_OFF) + pp;
-                    const int k0 = kb * NR_KB;
+                    float4 xv[8], cv[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        if (k0 + 4 * q < D) {
-                            const float4 xv = *reinterpret_cast<const float4 *>(xs + ((q ^ (r & 7)) << 4));
-                            if (p >= 0) {
-                                float4 cv;
-                                if (kt) {
-                                    cv.x = ct[(4 * q + 0) * kt];
-                                    cv.y = ct[(4 * q + 1) * kt];
-                                    cv.z = ct[(4 * q + 2) * kt];
-                                    cv.w = ct[(4 * q + 3) * kt];
-                                } else {
-                                    cv = *reinterpret_cast<const float4 *>(cs + ((q ^ (pp & 7)) << 4));
-                                }
-                                acc = __fadd_rn(acc, __fmul_rn(xv.x, cv.x));
-                                acc = __fadd_rn(acc, __fmul_rn(xv.y, cv.y));
-                                acc = __fadd_rn(acc, __fmul_rn(xv.z, cv.z));
-                                acc = __fadd_rn(acc, __fmul_rn(xv.w, cv.w));
-                            }
-                            if (need_info) {
-                                xx = fmaf(xv.x, xv.x, xx);
-                                xx = fmaf(xv.y, xv.y, xx);
-                                xx = fmaf(xv.z, xv.z, xx);
-                                xx = fmaf(xv.w, xv.w, xx);
-                                const float r0 = xv.x - tf32_trunc(xv.x), r1 = xv.y - tf32_trunc(xv.y);
-                                const float r2 = xv.z - tf32_trunc(xv.z), r3 = xv.w - tf32_trunc(xv.w);
-                                ee = fmaf(r0, r0, ee);
-                                ee = fmaf(r1, r1, ee);
-                                ee = fmaf(r2, r2, ee);
-                                ee = fmaf(r3, r3, ee);
-                                amax = fmaxf(amax, fmaxf(fmaxf(fabsf(xv.x), fabsf(xv.y)),
-                                                         fmaxf(fabsf(xv.z), fabsf(xv.w))));
-                            }
+                    for (int q = 0; q < 8; ++q) xv[q] = *reinterpret_cast<const float4 *>(xs + ((q ^ (r & 7)) << 4));
+                    if (kt) {
+                        // transposed slice: element (f, p) at f * kt + p
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            cv[q] = make_float4(ct[(4 * q + 0) * kt], ct[(4 * q + 1) * kt],
+                                                ct[(4 * q + 2) * kt], ct[(4 * q + 3) * kt]);
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            cv[q] = *reinterpret_cast<const float4 *>(cs + ((q ^ (pp & 7)) << 4));
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (p >= 0) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            acc = __fadd_rn(acc, __fmul_rn(xv[q].x, cv[q].x));
+                            acc = __fadd_rn(acc, __fmul_rn(xv[q].y, cv[q].y));
+                            acc = __fadd_rn(acc, __fmul_rn(xv[q].z, cv[q].z));
+                            acc = __fadd_rn(acc, __fmul_rn(xv[q].w, cv[q].w));
                         }
                     }
+                    if (need_info) {
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const float4 v = xv[q];
+                            xx = fmaf(v.x, v.x, xx);
+                            xx = fmaf(v.y, v.y, xx);
+                            xx = fmaf(v.z, v.z, xx);
+                            xx = fmaf(v.w, v.w, xx);
+                            const float r0 = v.x - tf32_trunc(v.x), r1 = v.y - tf32_trunc(v.y);
+                            const float r2 = v.z - tf32_trunc(v.z), r3 = v.w - tf32_trunc(v.w);
+                            ee = fmaf(r0, r0, ee);
+                            ee = fmaf(r1, r1, ee);
+                            ee = fmaf(r2, r2, ee);
+                            ee = fmaf(r3, r3, ee);
+                            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)),
+                                                     fmaxf(fabsf(v.z), fabsf(v.w))));
+                        }
+                    }
+                } else {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[stage]);
                 if (++stage == S) { stage = 0; phase ^= 1; }
             }
             mbar_wait(&c_empty[cb], (uint32_t(it >> 1) & 1) ^ 1);
@@ -713,9 +724,11 @@ int narrow_assign_run(ftk_ctx *ctx, const NarrowIn &in, cudaStream_t st) {
     const int kp = int((kaug + 15) / 16 * 16);
     const int nkb = int((d + NR_KB - 1) / NR_KB);
     const unsigned nfb = unsigned((d + 255) / 256);
-    // transposed chain operand for k <= 64 (conflict-free gathers of the
-    // hinted centroid); wider sets read the swizzled MMA slice
-    const int kt = k <= 64 ? int((k + 3) / 4 * 4) : 0;
+    // the chain warps read the hinted centroid from the swizzled MMA slice
+    // (FTK_NARROW_CT=1: from an extra transposed slice, bank-conflict free
+    // for k <= 32 but 4x the load instructions -- measured slower)
+    const char *cte = getenv("FTK_NARROW_CT");  // A/B knob: transposed chain operand
+    const int kt = (cte && atoi(cte) == 1 && k <= 64) ? int((k + 3) / 4 * 4) : 0;
     // scratch: augmented matrix, cinfo + partials, row lists
     const size_t aug_bytes = (sizeof(float) * size_t(kaug) * d + 255) & ~size_t(255);
     const size_t info_bytes = (256 + sizeof(float) * 3 * nfb + 64 + 255) & ~size_t(255);
