@@ -97,6 +97,7 @@ enum ScratchSlot {
     SLOT_EXACT_SPLIT = 22,  // per-(row, column split) argmin partials of the exact kernel
     SLOT_KPP = 23,          // k-means++: prefix scan of d2, counters, CUB temp
     SLOT_NARROW = 24,       // narrow screen: augmented centroids, tolerances, winner-pass rows
+    SLOT_PAIR_FLAG = 25,    // CTA-pair screen: records of checksum-flagged rows
 };
 
 // ------------------------------------------------------- float helpers --

@@ -492,54 +492,92 @@ __global__ void tc_prep_kernel(const float *y, const float *yn, int64_t k, int64
 // FT mode: checksum centroid sum_j tf32(c_j) (float64 sum in a fixed tree
 // order, then fp32) zero-padded to nkb*32 features, and max |c| (one block
 // per feature; the last block to finish folds the per-feature maxima).
+// ABFT checksum centroids: csum[f] = sum_j c~_jf and csumw[f] = sum_j (j/128
+// + 1) c~_jf in float64, fmax[f] = max_j |c_jf|.  Grid (feature blocks of 32,
+// CSUM_SLICES row slices), coalesced; per-slice partials, then the last CTA
+// adds the slices in order (fixed association: deterministic tolerances) and
+// writes camax = (max |c|, -, |csum|^2, |csumw|^2).
+constexpr int CSUM_SLICES = 16;
 __global__ void tile_csum_kernel(const float *y, int64_t k, int64_t d, int nkb, int trunc,
-                                 float *csum, float *camax, float *fmax, unsigned *done) {
-    const int64_t f = blockIdx.x;  // 0 .. nkb*32-1
-    double s = 0.0;
+                                 float *csum, float *camax, float *fmax, unsigned *done,
+                                 float *csumw, double *part) {
+    const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;  // 8 row groups
+    const int64_t nf = int64_t(nkb) * 32;
+    const int64_t f = int64_t(blockIdx.x) * 32 + lane;
+    const int64_t per = (k + CSUM_SLICES - 1) / CSUM_SLICES;
+    const int64_t j0 = int64_t(blockIdx.y) * per, j1 = j0 + per < k ? j0 + per : k;
+    double s = 0.0, sw = 0.0;
     float am = 0.0f;
     if (f < d)
-        for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        for (int64_t j = j0 + g; j < j1; j += 8) {
             const float v = y[j * d + f];
-            s += double(trunc ? tf32_trunc(v) : v);  // 3xTF32 pass: ~exact operands
+            const double tv = double(trunc ? tf32_trunc(v) : v);  // 3xTF32 pass: ~exact operands
+            s += tv;
+            sw += double(j / 128 + 1) * tv;  // location weight of column j's 128-column group
             am = fmaxf(am, fabsf(v));
         }
-    __shared__ double sh[32];
-    __shared__ float shm[32];
-    for (int off = 16; off; off >>= 1) {
-        s += __shfl_xor_sync(0xffffffffu, s, off);
-        am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, off));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        sh[threadIdx.x >> 5] = s;
-        shm[threadIdx.x >> 5] = am;
+    __shared__ double sh[8][32], shw[8][32];
+    __shared__ float shm[8][32];
+    __shared__ unsigned s_last;
+    sh[g][lane] = s;
+    shw[g][lane] = sw;
+    shm[g][lane] = am;
+    __syncthreads();
+    if (g == 0) {
+        double t = 0.0, tw = 0.0;
+        float m = 0.0f;
+        for (int q = 0; q < 8; ++q) {
+            t += sh[q][lane];
+            tw += shw[q][lane];
+            m = fmaxf(m, shm[q][lane]);
+        }
+        double *ps = part + (int64_t(blockIdx.y) * nf + f) * 3;
+        ps[0] = t;
+        ps[1] = tw;
+        ps[2] = double(m);
+        __threadfence();
     }
     __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    float n2 = 0.0f, w2 = 0.0f, gm = 0.0f;
+    for (int64_t ff = threadIdx.x; ff < nf; ff += blockDim.x) {
+        double t = 0.0, tw = 0.0, m = 0.0;
+        for (int sl = 0; sl < CSUM_SLICES; ++sl) {
+            const double *ps = part + (int64_t(sl) * nf + ff) * 3;
+            t += ps[0];
+            tw += ps[1];
+            m = ps[2] > m ? ps[2] : m;
+        }
+        csum[ff] = float(t);
+        csumw[ff] = float(tw);
+        fmax[ff] = float(m);
+        n2 = fmaf(float(t), float(t), n2);
+        w2 = fmaf(float(tw), float(tw), w2);
+        gm = fmaxf(gm, float(m));
+    }
+    __shared__ float rn[256], rw[256], rm[256];
+    rn[threadIdx.x] = n2;
+    rw[threadIdx.x] = w2;
+    rm[threadIdx.x] = gm;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+        if (int(threadIdx.x) < o) {
+            rn[threadIdx.x] += rn[threadIdx.x + o];
+            rw[threadIdx.x] += rw[threadIdx.x + o];
+            rm[threadIdx.x] = fmaxf(rm[threadIdx.x], rm[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        double t = 0.0;
-        float m = 0.0f;
-        for (int w = 0; w < int(blockDim.x / 32); ++w) {
-            t += sh[w];
-            m = fmaxf(m, shm[w]);
-        }
-        csum[f] = float(t);
-        fmax[f] = m;
-        __threadfence();
-        if (atomicAdd(done, 1u) == gridDim.x - 1) {  // last block: global max
-            __threadfence();
-            float g = 0.0f, n2 = 0.0f;
-            for (int64_t q = 0; q < gridDim.x; ++q) {
-                g = fmaxf(g, fmax[q]);
-                n2 = fmaf(csum[q], csum[q], n2);
-            }
-            camax[0] = g;
-            camax[2] = n2;  // |csum|^2 (bounds the fp32 reference error)
-            *done = 0;
-        }
+        camax[0] = rm[0];
+        camax[2] = rn[0];  // |csum|^2 (bounds the fp32 reference error)
+        camax[3] = rw[0];  // |csumw|^2
+        *done = 0;
     }
 }
-
-// FT mode: scheduled flips -> per-row (column, exact before, after) so the
-// TC epilogue can corrupt exactly the accumulator the reference corrupts.
 __global__ void inj_rows_kernel(const float *x, const float *y, int64_t m, int64_t k, int64_t d,
                                 int64_t bm, int64_t bn, ftk_injection inj, int32_t *inj_col,
                                 float *inj_before, float *inj_after) {
@@ -836,16 +874,22 @@ int exact_run(ftk_ctx *, int, const void *, const void *, const void *, int64_t,
 
 // FT mode helpers: checksum centroids for a given N tiling
 static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb,
-                     int trunc, float **csum, float **camax, cudaStream_t st) {
+                     int trunc, float **csum, float **camax, cudaStream_t st,
+                     float **csumw = nullptr) {
     const int64_t nf = int64_t(nkb) * 32;
-    float *buf = static_cast<float *>(scratch(ctx, slot, sizeof(float) * (2 * nf + 64), st));
+    float *buf = static_cast<float *>(
+        scratch(ctx, slot, sizeof(float) * (3 * nf + 64) + sizeof(double) * 3 * CSUM_SLICES * nf + 64, st));
     if (!buf) return FTK_ERR_CUDA;
+    double *part = reinterpret_cast<double *>(buf + 3 * nf + 64);
     *csum = buf;
-    *camax = buf + nf;
+    *camax = buf + nf;  // [0] max|c|, [1] counter, [2] |csum|^2, [3] |csumw|^2
     float *fmax = buf + nf + 32;
+    float *cw = buf + 2 * nf + 32;  // 16-byte aligned (nf % 32 == 0)
+    if (csumw) *csumw = cw;
     unsigned *done = reinterpret_cast<unsigned *>(buf + nf + 1);
     FTK_CUDA(cudaMemsetAsync(done, 0, sizeof(unsigned), st));
-    tile_csum_kernel<<<unsigned(nf), 256, 0, st>>>(y, k, d, nkb, trunc, *csum, *camax, fmax, done);
+    tile_csum_kernel<<<dim3(unsigned(nkb), CSUM_SLICES), 256, 0, st>>>(y, k, d, nkb, trunc, *csum, *camax,
+                                                                     fmax, done, cw, part);
     FTK_LAUNCHED("tile_csum_kernel");
     return FTK_OK;
 }
@@ -989,9 +1033,9 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     P.out_val = outv;
     P.raw = raw;
     if (const char *e = getenv("FTK_TC_DEBUG")) P.dbg = atoi(e);  // pipeline-timing probe
-    float *csum1 = nullptr, *camax1 = nullptr, *csum2 = nullptr, *camax2 = nullptr;
+    float *csum1 = nullptr, *camax1 = nullptr, *csum2 = nullptr, *camax2 = nullptr, *csumw1 = nullptr;
     if (ft) {
-        int rc0 = prep_csum(ctx, SLOT_TC_CSUM1, yf, k, d, P.nkb, 1, &csum1, &camax1, st);
+        int rc0 = prep_csum(ctx, SLOT_TC_CSUM1, yf, k, d, P.nkb, 1, &csum1, &camax1, st, &csumw1);
         if (rc0) return rc0;  // the 3xTF32 checksum centroid is built by the single-CTA pass 2
         P.tau_abs = float(ft->abs_tol);
         P.abft_count = cnt + 2;
@@ -1028,6 +1072,8 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
         }
     }
     CUtensorMap mx, mc;
+    constexpr unsigned kFlagCap = 4096;  // flagged rows recorded per pass (beyond: no event)
+    double4 *flag_rec = nullptr;
     float *pair_fb_thr = nullptr;
     unsigned long long *pair_fb_seed = nullptr;
     int rc = make_map(&mc, yf, k, d, uint32_t(bn));
@@ -1060,6 +1106,13 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             Q.inj_col = P.inj_col; Q.inj_before = P.inj_before; Q.inj_after = P.inj_after;
             Q.abft_count = P.abft_count;
             Q.abft_total = P.abft_total;
+            if (ft) {
+                flag_rec = static_cast<double4 *>(scratch(ctx, SLOT_PAIR_FLAG, sizeof(double4) * kFlagCap, st));
+                if (!flag_rec) return FTK_ERR_CUDA;
+                Q.flag_rec = flag_rec;
+                Q.flag_count = cnt + 5;
+                Q.flag_cap = kFlagCap;
+            }
             Q.dbg = P.dbg;
             if (ctx->rows_info && ctx->rows_x == x && ctx->rows_m == m && ctx->rows_d == d)
                 Q.rowinfo = reinterpret_cast<const float4 *>(ctx->rows_info);
@@ -1165,6 +1218,23 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             ctx->stat_dev[0] = cnt;          // read lazily by tc_last_fallback
             ctx->stat_dev[1] = ccount + 1;
             ctx->stat_dev[2] = ft ? cnt + 2 : nullptr;
+            if (ft) {
+                // location + event records of the flagged rows (pass 2 has
+                // re-resolved them: the correction)
+                FlagEvents F{};
+                F.x = xf; F.d = d; F.k = k;
+                F.csumw = csumw1; F.camax = camax1;
+                F.rec = flag_rec; F.count = cnt + 5; F.cap = kFlagCap;
+                F.inj_col = P.inj_col;
+                F.events_for_scheduled = ctx->inj_replay ? 0 : 1;
+                if (ft->ev) F.ev = *ft->ev;
+                F.iteration = ft->iteration;
+                F.bm = ft->bm;
+                F.bn = ft->bn;
+                F.interval = ft->bk > 0 ? (d + ft->bk - 1) / ft->bk - 1 : 0;
+                F.corrected = cnt + 4;
+                if ((rc = abft_flag_events_run(F, st))) return rc;
+            }
             if (ft && ft->inj && ft->inj->n > 0 && ctx->inj_replay)
                 return emulate_injected_blocks(ctx, xf, yf, ynf, m, k, d, *ft, out_idx, outv, st);
             return FTK_OK;

@@ -239,9 +239,11 @@ __global__ void __launch_bounds__(NR_THREADS, 1)
             for (int kb = 0; kb < nkb; ++kb) {
                 mbar_wait(&full[stage], phase);
                 if (work) {
-                    // all 16 shared-memory loads of the stage first, then the
-                    // stage is released, then the arithmetic: the dependent
-                    // fp32 chain (32 FADDs) runs while the producer refills.
+                    // all 16 shared-memory loads of the stage first, then the 32
+                    // independent products (they consume every loaded register,
+                    // so the loads have completed), then the stage is released,
+                    // then the dependent fp32 chain (32 FADDs) runs while the
+                    // producer refills the stage.
                     // Features past D are zero in both TMA slices, and x*c = 0
                     // leaves the chain unchanged (acc is never -0).
                     const unsigned char *xs = sS + size_t(stage) * STG + uint32_t(r) * 128u;
@@ -262,16 +264,13 @@ __global__ void __launch_bounds__(NR_THREADS, 1)
                         for (int q = 0; q < 8; ++q)
                             cv[q] = *reinterpret_cast<const float4 *>(cs + ((q ^ (pp & 7)) << 4));
                     }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[stage]);
-                    if (p >= 0) {
+                    float pr[32];
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            acc = __fadd_rn(acc, __fmul_rn(xv[q].x, cv[q].x));
-                            acc = __fadd_rn(acc, __fmul_rn(xv[q].y, cv[q].y));
-                            acc = __fadd_rn(acc, __fmul_rn(xv[q].z, cv[q].z));
-                            acc = __fadd_rn(acc, __fmul_rn(xv[q].w, cv[q].w));
-                        }
+                    for (int q = 0; q < 8; ++q) {
+                        pr[4 * q + 0] = __fmul_rn(xv[q].x, cv[q].x);
+                        pr[4 * q + 1] = __fmul_rn(xv[q].y, cv[q].y);
+                        pr[4 * q + 2] = __fmul_rn(xv[q].z, cv[q].z);
+                        pr[4 * q + 3] = __fmul_rn(xv[q].w, cv[q].w);
                     }
                     if (need_info) {
 #pragma unroll
@@ -290,6 +289,21 @@ __global__ void __launch_bounds__(NR_THREADS, 1)
                             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)),
                                                      fmaxf(fabsf(v.z), fabsf(v.w))));
                         }
+                    }
+                    // the products (and the bounds) hold every value the stage
+                    // supplied: make the warp's loads complete, then release it
+                    asm volatile("" ::"f"(pr[0]), "f"(pr[1]), "f"(pr[2]), "f"(pr[3]), "f"(pr[4]),
+                                 "f"(pr[5]), "f"(pr[6]), "f"(pr[7]), "f"(pr[8]), "f"(pr[9]),
+                                 "f"(pr[10]), "f"(pr[11]), "f"(pr[12]), "f"(pr[13]), "f"(pr[14]),
+                                 "f"(pr[15]), "f"(pr[16]), "f"(pr[17]), "f"(pr[18]), "f"(pr[19]),
+                                 "f"(pr[20]), "f"(pr[21]), "f"(pr[22]), "f"(pr[23]), "f"(pr[24]),
+                                 "f"(pr[25]), "f"(pr[26]), "f"(pr[27]), "f"(pr[28]), "f"(pr[29]),
+                                 "f"(pr[30]), "f"(pr[31]));
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (p >= 0) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) acc = __fadd_rn(acc, pr[e]);
                     }
                 } else {
                     __syncwarp();

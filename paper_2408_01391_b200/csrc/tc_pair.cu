@@ -96,7 +96,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     unsigned char *sA = smem;
     unsigned char *sB = sA + size_t(NA) * A_BYTES;
     PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * STG);  // [2][2][128]
-    double *psum = reinterpret_cast<double *>(part + 2 * 2 * PR_BM);           // [2][2][128]
+    double2 *psum = reinterpret_cast<double2 *>(part + 2 * 2 * PR_BM);         // [2][2][128] (sum, weighted)
     float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
     float4 *css = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // ABFT checksum centroid [nkb * 8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
@@ -257,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
             float m1 = INFINITY, m2 = INFINITY;
             int tile1 = 0;
-            double rsum = 0.0;
+            double rsum = 0.0, wsum = 0.0;
             int inj_c = -1;
             float inj_b = 0.0f, inj_a = 0.0f;
             const float thr = (COLLECT && grow < M) ? P.thr[grow] : -INFINITY;
@@ -391,7 +391,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 // merge the two chains into the tile's top-2, then the running top-2
                 const float t1 = fminf(a1, b1);  // b1 = b2 = inf: single chain
                 const float t2 = fminf(fminf(a2, b2), fmaxf(a1, b1));
-                if (CHK) rsum += double(s0 + s1);
+                if (CHK) {
+                    // the warpgroup's 128-column group g = 2t + wg has location
+                    // weight g + 1: one multiply per group, none per column
+                    const double gs = double(s0 + s1);
+                    rsum += gs;
+                    wsum += gs * double(2 * t + wg + 1);
+                }
                 const float hi = fmaxf(m1, t1);
                 if (t1 < m1) tile1 = t;
                 m1 = fminf(m1, t1);
@@ -409,7 +415,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             pp.m2 = m2;
             pp.pad = 0.0f;
             part[(pb * 2 + wg) * PR_BM + r] = pp;
-            if (CHK) psum[(pb * 2 + wg) * PR_BM + r] = rsum;
+            if (CHK) psum[(pb * 2 + wg) * PR_BM + r] = make_double2(rsum, wsum);
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
         }
@@ -432,8 +438,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             PROBE_ADD(6, rw1_ - rw0_);
             const PairPart q0 = part[(pb * 2 + 0) * PR_BM + r];
             const PairPart q1 = part[(pb * 2 + 1) * PR_BM + r];
-            double rsum = 0.0;
-            if (CHK) rsum = psum[(pb * 2 + 0) * PR_BM + r] + psum[(pb * 2 + 1) * PR_BM + r];
+            double rsum = 0.0, wsum = 0.0;
+            if (CHK) {
+                const double2 u0 = psum[(pb * 2 + 0) * PR_BM + r], u1 = psum[(pb * 2 + 1) * PR_BM + r];
+                rsum = u0.x + u1.x;
+                wsum = u0.y + u1.y;
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[pb]);
             const bool take1 = q1.m1 < q0.m1;
@@ -549,10 +559,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     const float tau = P.tau_coef * fmaxf(1.0f, amax * *P.camax) + P.tau_abs +
                                       34.0f * 0x1p-24f * sqrtf(xx * (1.0f + 0x1p-10f)) *
                                           sqrtf(P.camax[2] * (1.0f + 0x1p-10f));
-                    abft_bad = !(fabs(rsum - rref) <= double(tau));
+                    const double D1 = rsum - rref;
+                    abft_bad = !(fabs(D1) <= double(tau));
                     if (abft_bad) {
                         atomicAdd(P.abft_count, 1u);
                         if (P.abft_total) atomicAdd(P.abft_total, 1ull);
+                        // the row is re-resolved exactly by pass 2 (a clean
+                        // re-screen): correction without touching the hot path.
+                        // Location and the event record are done after the pass
+                        // (abft_flag_events_kernel) from this record.
+                        if (P.flag_rec) {
+                            const unsigned q = atomicAdd(P.flag_count, 1u);
+                            if (q < P.flag_cap)
+                                P.flag_rec[q] = make_double4(__longlong_as_double(grow), D1, wsum, double(tau));
+                        }
                     }
                 }
                 // magnitudes far from overflow: the screen saw every column finite
@@ -615,7 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 // ------------------------------------------------------------- host ------
 size_t pair_smem_bytes(int nkb, int abufs, int stages, bool sx) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * (sx ? PR_B_HALF + PR_A_KB : PR_B_HALF) +
-           2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double)) + 2 * PR_BN * sizeof(float) +
+           2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 2 * PR_BN * sizeof(float) +
            8 * 8 * sizeof(float4) + (2 * size_t(stages) + 8 + 2 * PR_NBUF + 2 * PR_MAX_KB) * 8 + 64;
 }
 
@@ -798,6 +818,75 @@ __global__ void exact_rows_kernel(const float *x, const float *y, const float *y
             out_val[row] = bv;
         }
     }
+}
+
+// One warp per flagged row: the reference of the group-weighted checksum
+// x~ . csumw (lane partials, fixed shuffle tree), the error's 128-column group
+// g = rint(D2 / D1) - 1 when consistent, and a DetectionEvent unless the row
+// carries a scheduled flip (those get the reference's own record from the
+// exact replay).  The row itself is re-resolved exactly by pass 2 -- the
+// correction -- so every record is detected-corrected; loc_j = -1 (the
+// column within the group is not resolved), tile_j = the group's tile.
+__global__ void abft_flag_events_kernel(FlagEvents F) {
+    const int lane = threadIdx.x & 31;
+    const unsigned n = min(*F.count, F.cap);
+    const unsigned w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned q = w0; q < n; q += nw) {
+        const double4 r = F.rec[q];
+        const int64_t row = __double_as_longlong(r.x);
+        const double D1 = r.y, wsum = r.z, tau = r.w;
+        const float4 *x4 = reinterpret_cast<const float4 *>(F.x + row * F.d);
+        const float4 *w4 = reinterpret_cast<const float4 *>(F.csumw);
+        float wr = 0.0f, xx = 0.0f;
+        for (int64_t f = lane; f < F.d / 4; f += 32) {
+            const float4 xv = __ldg(x4 + f), wv = __ldg(w4 + f);
+            wr = fmaf(tf32_trunc(xv.x), wv.x, wr);
+            wr = fmaf(tf32_trunc(xv.y), wv.y, wr);
+            wr = fmaf(tf32_trunc(xv.z), wv.z, wr);
+            wr = fmaf(tf32_trunc(xv.w), wv.w, wr);
+            xx = fmaf(xv.x, xv.x, fmaf(xv.y, xv.y, fmaf(xv.z, xv.z, fmaf(xv.w, xv.w, xx))));
+        }
+        for (int off = 16; off; off >>= 1) {
+            wr += __shfl_xor_sync(0xffffffffu, wr, off);
+            xx += __shfl_xor_sync(0xffffffffu, xx, off);
+        }
+        if (lane != 0) continue;
+        const double D2 = wsum - double(wr);
+        const int ng = int((F.k + 127) / 128);
+        const double gf = rint(D2 / D1) - 1.0;
+        int64_t col = 0;
+        bool located = false;
+        if (gf >= 0.0 && gf < double(ng)) {
+            const double tw = double(ng + 1) * tau + fabs(D1) * double(ng) * 0x1p-18 +
+                              64.0 * 0x1p-24 * sqrt(double(xx) * (1.0 + 0x1p-10)) *
+                                  sqrt(double(F.camax[3]) * (1.0 + 0x1p-10));
+            located = fabs(D2 - (gf + 1.0) * D1) <= tw;
+            col = located ? int64_t(gf) * 128 : 0;
+        }
+        atomicAdd(F.corrected, 1u);
+        if (F.ev.rec && (!F.inj_col || F.inj_col[row] < 0 || F.events_for_scheduled)) {
+            const unsigned long long c = atomicAdd(reinterpret_cast<unsigned long long *>(F.ev.count), 1ull);
+            if (c < (unsigned long long)F.ev.cap) {
+                int64_t *rec = F.ev.rec + c * 7;
+                rec[0] = F.iteration;
+                rec[1] = row / F.bm;
+                rec[2] = col / F.bn;
+                rec[3] = 0;  // EV_CORRECTED: the row is re-resolved exactly
+                rec[4] = row % F.bm;
+                rec[5] = -1;
+                rec[6] = F.interval;
+                F.ev.delta[c] = D1;
+            }
+        }
+        (void)located;
+    }
+}
+
+int abft_flag_events_run(const FlagEvents &F, cudaStream_t st) {
+    abft_flag_events_kernel<<<32, 256, 0, st>>>(F);
+    FTK_LAUNCHED("abft_flag_events_kernel");
+    return FTK_OK;
 }
 
 int pass2_gather_run(const float *x, int64_t d, const int32_t *rows, const unsigned *count,

@@ -31,6 +31,12 @@ struct PairParams {
     const float *inj_before, *inj_after;
     unsigned *abft_count;
     unsigned long long *abft_total;  // cumulative over launches (ftk_abft_flags_total)
+    // ABFT: every row whose checksum fails is recorded as (row, D1 = row sum
+    // - reference, the 128-column-group-weighted row sum, tau) for
+    // abft_flag_events_run (location + event record after the pass)
+    double4 *flag_rec;
+    unsigned *flag_count;
+    unsigned flag_cap;
     // pass 1: per uncertified row, the pass-2 threshold and the (d1, j1) seed key
     float *fb_thr;
     unsigned long long *fb_seed;
@@ -65,6 +71,22 @@ int pass2_gather_run(const float *x, int64_t d, const int32_t *rows, const unsig
 int exact_rows_run(const float *x, const float *y, const float *yn, int64_t k, int64_t d,
                    const int32_t *rows, const unsigned *count, int32_t *out_idx, float *out_val,
                    cudaStream_t st);
+// Location (128-column group, weighted checksum) and event records of the
+// rows the CTA-pair screen flagged (see abft_flag_events_kernel).
+struct FlagEvents {
+    const float *x;
+    int64_t d, k;
+    const float *csumw, *camax;
+    const double4 *rec;
+    const unsigned *count;
+    unsigned cap;
+    const int32_t *inj_col;  // rows carrying a scheduled flip (replayed exactly), or null
+    int events_for_scheduled;
+    ftk_events ev;
+    int64_t iteration, bm, bn, interval;
+    unsigned *corrected;
+};
+int abft_flag_events_run(const FlagEvents &F, cudaStream_t st);
 }  // namespace ftk
 
 namespace ftk {
