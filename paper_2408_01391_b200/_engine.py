@@ -11,7 +11,9 @@ from . import _native as N
 
 _CTX = {}
 _ROWS_OWNER = {}  # device -> id of the RowInfo registered on its context
-_VARIANT = {"auto": N.VARIANT_AUTO, "exact": N.VARIANT_EXACT, "tc": N.VARIANT_TC}
+_VARIANT = {"auto": N.VARIANT_AUTO, "exact": N.VARIANT_EXACT, "tc": N.VARIANT_TC,
+            "pair": N.VARIANT_TC_PAIR, "narrow": N.VARIANT_TC_NARROW,
+            "dmma": N.VARIANT_F64_DMMA, "dfma": N.VARIANT_F64_DFMA}
 
 
 def _torch():

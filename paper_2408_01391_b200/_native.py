@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("FTK_LIB_PATH") or os.path.join(HERE, "_lib", "libftkb
 FTK_OK, FTK_OVERFLOW = 0, 1
 FTK_F32, FTK_F64 = 0, 1
 VARIANT_AUTO, VARIANT_EXACT, VARIANT_TC = 0, 1, 2
+VARIANT_TC_PAIR, VARIANT_TC_NARROW, VARIANT_F64_DMMA, VARIANT_F64_DFMA = 3, 4, 5, 6
 
 _i64, _i32, _p, _dbl, _int = ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p, ctypes.c_double, ctypes.c_int
 

@@ -156,7 +156,10 @@ def _checked_run(a, b, cfg, thr, hook, iteration, threads, y_norms, materialize)
                            abs_tol=abs_tol, iteration=iteration, events=events)
     else:
         yn_t = _ynorms_dev(b_t, y_norms, dt, k)
-        idx, val = E.assign_dev(a_t, b_t, yn_t, cfg.block, variant=get_variant(), inj=inj,
+        from .variants import resolve
+
+        idx, val = E.assign_dev(a_t, b_t, yn_t, cfg.block,
+                                variant=resolve((m, a_t.shape[1], k), dt, ft_on=True), inj=inj,
                                 checked=True, delta_rel=delta_rel, abs_tol=abs_tol,
                                 iteration=iteration, events=events)
     overflow, raw = events.read()

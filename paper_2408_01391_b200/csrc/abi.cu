@@ -98,6 +98,30 @@ float tc_last_pass1_ms(ftk_ctx *);
 
 static bool dtype_ok(int dt) { return dt == FTK_F32 || dt == FTK_F64; }
 
+// Variant code -> forced kernel family for the duration of one call.
+struct FamilyScope {
+    ftk_ctx *ctx;
+    bool ok = true;
+    FamilyScope(ftk_ctx *c, int dtype, int variant) : ctx(c) {
+        int fam = 0;
+        switch (variant) {
+            case FTK_VARIANT_TC_PAIR: fam = 1; break;
+            case FTK_VARIANT_TC_NARROW: fam = 2; break;
+            case FTK_VARIANT_F64_DMMA: fam = 3; break;
+            case FTK_VARIANT_F64_DFMA: fam = 4; break;
+            case FTK_VARIANT_AUTO: case FTK_VARIANT_EXACT: case FTK_VARIANT_TC: break;
+            default: ok = false;
+        }
+        if ((fam == 1 || fam == 2) && dtype != FTK_F32) ok = false;
+        if ((fam == 3 || fam == 4) && dtype != FTK_F64) ok = false;
+        if (!ok) set_error("variant does not apply to this dtype");
+        ctx->family = ok ? fam : 0;
+    }
+    ~FamilyScope() { ctx->family = 0; }
+};
+static bool forced_tc(int v) { return v == FTK_VARIANT_TC || v == FTK_VARIANT_TC_PAIR || v == FTK_VARIANT_TC_NARROW; }
+static bool forced_any(int v) { return v != FTK_VARIANT_AUTO && v != FTK_VARIANT_EXACT; }
+
 }  // namespace ftk
 
 using namespace ftk;
@@ -196,19 +220,23 @@ int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *
                int64_t bk, int32_t *out_idx, void *out_val, const ftk_injection *inj,
                void *stream) {
     if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    FamilyScope fs(ctx, dtype, variant);
+    if (!fs.ok) return FTK_ERR_ARG;
     cudaStream_t st = as_stream(stream);
     bool has_inj = inj && inj->n > 0;
     if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && !has_inj) {
-        // float64: DFMA screen + certified exact refine (dscreen.cu)
+        // float64: DMMA / DFMA screen + certified exact refine (dscreen.cu)
         int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
                              static_cast<const double *>(ynorms), m, k, d, out_idx,
                              static_cast<double *>(out_val), nullptr, st);
-        if (rc != FTK_ERR_UNSUPPORTED) return rc;
+        if (rc != FTK_ERR_UNSUPPORTED || forced_any(variant)) return rc;
     }
-    if (variant == FTK_VARIANT_TC || (variant == FTK_VARIANT_AUTO && !has_inj)) {
+    // scheduled flips in an unprotected pass: the reference's corrupted
+    // result is the exact kernel's (the screens apply flips only when checked)
+    if (!has_inj && (forced_tc(variant) || variant == FTK_VARIANT_AUTO)) {
         int rc = tc_assign_run(ctx, dtype, x, y, ynorms, m, k, d, out_idx, out_val, st, nullptr, 0,
                                nullptr);
-        if (rc != FTK_ERR_UNSUPPORTED || variant == FTK_VARIANT_TC) return rc;
+        if (rc != FTK_ERR_UNSUPPORTED || forced_tc(variant)) return rc;
     }
     return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
                      false, 0.0, 0.0, 0, inj, nullptr, st);
@@ -220,20 +248,27 @@ int ftk_checked_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, cons
                        int64_t iteration, int32_t *out_idx, void *out_val,
                        const ftk_injection *inj, ftk_events *ev, void *stream) {
     if (!ctx || !dtype_ok(dtype)) { set_error("bad ctx/dtype"); return FTK_ERR_ARG; }
+    FamilyScope fs(ctx, dtype, variant);
+    if (!fs.ok) return FTK_ERR_ARG;
     cudaStream_t st = as_stream(stream);
     if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && bn >= 1 && bm >= 1) {
         TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
         int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
                              static_cast<const double *>(ynorms), m, k, d, out_idx,
                              static_cast<double *>(out_val), &ft, st);
-        if (rc != FTK_ERR_UNSUPPORTED) return rc;
+        if (rc != FTK_ERR_UNSUPPORTED || forced_any(variant)) return rc;
     }
     // TC path: screened assignment with per-tile row checksums; flagged rows
     // and the logical blocks carrying scheduled flips are resolved exactly
-    if ((variant == FTK_VARIANT_TC || variant == FTK_VARIANT_AUTO) &&
-        tc_supported(dtype, m, k, d) && bn >= 1 && bm >= 1)
-        return tc_checked_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, delta_rel, abs_tol,
-                              iteration, out_idx, out_val, inj, ev, st);
+    if ((forced_tc(variant) || variant == FTK_VARIANT_AUTO) && bn >= 1 && bm >= 1) {
+        if (tc_supported(dtype, m, k, d))
+            return tc_checked_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, delta_rel, abs_tol,
+                                  iteration, out_idx, out_val, inj, ev, st);
+        if (forced_tc(variant)) {
+            set_error("tensor-core variant: unsupported shape");
+            return FTK_ERR_UNSUPPORTED;
+        }
+    }
     return exact_run(ctx, dtype, x, y, ynorms, m, k, d, bm, bn, bk, out_idx, out_val, nullptr,
                      true, delta_rel, abs_tol, iteration, inj, ev, st);
 }

@@ -62,6 +62,7 @@ struct ftk_ctx {
     const int32_t *hint = nullptr;
     int64_t hint_m = 0;
     int inj_replay = 1;  // FTK_OPT_INJ_REPLAY: replay blocks with scheduled flips exactly
+    int family = 0;      // forced kernel family of the current call (0 auto, 1 pair, 2 narrow, 3 dmma, 4 dfma)
 };
 
 namespace ftk {

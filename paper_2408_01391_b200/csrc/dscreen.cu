@@ -539,7 +539,7 @@ int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const unsigned grid = unsigned(std::min<int64_t>(nrt, int64_t(nsm)));
     const char *se = getenv("FTK_F64_SIMT");
-    if (se && atoi(se)) {  // DFMA SIMT screen (comparison)
+    if (ctx->family == 4 || (ctx->family != 3 && se && atoi(se))) {  // DFMA SIMT screen
         const size_t smem = sizeof(double) * (DS_STAGES * DS_KC * (DS_BM + DS_BN) + DS_BN);
         auto kern = ft ? dscreen_kernel<true> : dscreen_kernel<false>;
         FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -50,7 +50,7 @@ constexpr int TC_BM = 128;       // rows per CTA (UMMA M)
 constexpr int TC_KB = 32;        // fp32 elements per 128-byte swizzle row
 constexpr int TC_THREADS = 192;  // 6 warps
 constexpr int TC_MAX_D = 256;    // resident-A limit
-constexpr int TC_SX_MAX_D = 8192;  // streamed-X pair screen (k <= PAIR_BN)
+constexpr int TC_SX_MAX_D = 8192;  // streamed-X pair screen (any k)
 
 struct TcParams {
     const float *x;      // rows x d  (exact values; pass 2: the gathered rows)
@@ -854,12 +854,10 @@ int tc_supported(int dtype, int64_t m, int64_t k, int64_t d) {
     // reads X rows from global memory and is latency-bound (c3 D=512 K=16:
     // pass 1 2.0 ms, 0.49 ms without the refine), no faster than the exact
     // kernel yet.  The resident-X kernels stop at 256.
-    // d > 256 with k + 4 <= 256: the streamed-X narrow screen (tc_narrow.cu)
-    const char *sx = getenv("FTK_TC_SX");
-    const bool sx_on = sx && atoi(sx) == 1;
+    // d > 256: the streamed-X narrow screen (tc_narrow.cu, k + 4 <= 256) or
+    // the CTA-pair screen with X streamed through its stages (any k)
     return dtype == FTK_F32 && d >= 4 && d % 4 == 0 &&
-           (d <= TC_MAX_D || (sx_on && k <= PAIR_BN && d <= TC_SX_MAX_D) ||
-            (!sx_on && narrow_supported(k, d, true))) && k >= 1 && m >= 1 &&
+           (d <= TC_SX_MAX_D || narrow_supported(k, d, true)) && k >= 1 && m >= 1 &&
            m < (int64_t(1) << 31) && k < (int64_t(1) << 24);
 }
 
@@ -998,7 +996,8 @@ int emulate_injected_blocks(ftk_ctx *ctx, const T *xf, const T *yf, const T *ynf
 int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const void *yn,
                   int64_t m, int64_t k, int64_t d, int32_t *out_idx, void *out_val,
                   cudaStream_t st, float *raw, int split_only, const TcFt *ft) {
-    if (!tc_supported(dtype, m, k, d)) {
+    if (!tc_supported(dtype, m, k, d) || (ctx->family == 1 && d > TC_SX_MAX_D) ||
+        (ctx->family == 2 && !narrow_supported(k, d, ft != nullptr))) {
         set_error("tc variant: unsupported shape/dtype");
         return FTK_ERR_UNSUPPORTED;
     }
@@ -1055,8 +1054,12 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
     }
     {
         const char *sx = getenv("FTK_TC_SX");
-        if (!split_only && raw == nullptr && d > TC_MAX_D && !(sx && atoi(sx) == 1) &&
-            narrow_supported(k, d, ft != nullptr)) {
+        // auto: wide rows go to the narrow screen when it can take k (the
+        // variant table measures the rest; FTK_TC_SX=1 forces the pair screen)
+        const bool narrow = ctx->family == 2 ||
+                            (ctx->family == 0 && d > TC_MAX_D && !(sx && atoi(sx) == 1) &&
+                             narrow_supported(k, d, ft != nullptr));
+        if (!split_only && raw == nullptr && narrow && narrow_supported(k, d, ft != nullptr)) {
             // wide rows, few centroids: the streamed-X narrow screen
             NarrowIn in{};
             in.x = xf; in.y = yf; in.yn = ynf; in.m = m; in.k = k; in.d = d;
@@ -1094,7 +1097,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             P.tau_coef = float(ft->delta_rel * double(d) * sqrt(double(k) / 32.0));
         }
         const char *pe = getenv("FTK_TC_PAIR");
-        if (!(pe && atoi(pe) == 0) && (d <= TC_MAX_D || k <= PAIR_BN) && raw == nullptr) {
+        if (!(pe && atoi(pe) == 0) && d <= TC_SX_MAX_D && raw == nullptr) {
             // CTA-pair kernel (tc_pair.cu): M = 256 per cluster, half the L2 traffic
             CUtensorMap mc128;
             if ((rc = make_map(&mc128, yf, k, d, PAIR_BN / 2))) return rc;

@@ -80,10 +80,11 @@ __device__ __forceinline__ uint32_t ordered_key(float f) {
 
 // INJ: the pass carries scheduled flips (P.inj_col); a separate instantiation
 // keeps the per-chunk injection test out of the clean CHK epilogue (-2.7%).
-// SX (streamed X, d > 256 with K <= 256, i.e. one column tile): the X half
-// no longer fits resident, so its k-blocks travel with the centroid k-blocks
-// through the stage ring (each stage = centroid half + X half) and the
-// refine reads its row from global memory (L2: the tile was just streamed).
+// SX (streamed X, d > 256): the X half no longer fits resident, so its
+// k-blocks travel with the centroid k-blocks through the stage ring (each
+// stage = centroid half + X half; with several column tiles the row tile's X
+// is re-read from L2 per tile) and the refine reads its row from global
+// memory (L2: the tile was just streamed).
 template <bool CHK, bool COLLECT, bool INJ, bool SX>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     pair_screen_kernel(const __grid_constant__ CUtensorMap tmX,
@@ -665,11 +666,7 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     }
     P.nkb = int((P.d + PR_KB - 1) / PR_KB);
     P.ntiles = int((P.k + PR_BN - 1) / PR_BN);
-    const bool sx = P.nkb > PR_MAX_KB;
-    if (sx && P.ntiles != 1) {
-        set_error("tc pair: streamed X (d > 256) needs k <= 256");
-        return FTK_ERR_UNSUPPORTED;
-    }
+    const bool sx = P.nkb > PR_MAX_KB;  // streamed X: re-read per column tile (from L2)
     const size_t smem = pair_smem_bytes(P.nkb, P.abufs, P.stages, sx);
     const int64_t npt = (P.m + 2 * PR_BM - 1) / (2 * PR_BM);
     if (npt == 0) return FTK_OK;

@@ -24,8 +24,10 @@ _VARIANT = os.environ.get("FTK_VARIANT", "auto")
 
 
 def set_variant(name):
-    """Select the assign kernel family: 'auto' (tensor-core screen where it
-    applies, exact SIMT otherwise), 'exact' or 'tc'."""
+    """Select the assign kernel family: 'auto' (variants.resolve: the
+    measured variant table, else tensor cores where they apply), 'exact',
+    'tc', or a family of variants.FAMILIES ('pair', 'narrow', 'dmma',
+    'dfma')."""
     global _VARIANT
     E.variant_code(name)
     _VARIANT = name
@@ -124,7 +126,10 @@ def fused_assign(x, y, y_norms=None, cfg=None, threads=None, hook=None, iteratio
     if m == 0:
         return AssignResult(np.empty(0, np.int64), np.empty(0, dt))
     inj = E.injection_for(hook, iteration, dt)
-    idx, val = E.assign_dev(x_t, y_t, yn_t, cfg.block, variant=_VARIANT, inj=inj)
+    from .variants import resolve
+
+    idx, val = E.assign_dev(x_t, y_t, yn_t, cfg.block, variant=resolve((m, x.shape[1], k), dt),
+                            inj=inj)
     labels = E.to_host(idx).astype(np.int64)
     md = E.to_host(val)
     if inj is not None:

@@ -244,6 +244,10 @@ class _DeviceAssign:
         t = E._torch()
         self.x_t, self.m, self.k, self.dtype, self.cfg = x_t, m, k, dtype, cfg
         self.checked = ft_mode != "off"
+        from .variants import resolve
+
+        # kernel family (variants.py: explicit choice, measured table, rule)
+        self.variant = resolve((m, x_t.shape[1], k), dtype, ft_on=self.checked)
         self.delta_rel, self.abs_tol = (thr.kernel_params() if thr is not None else (0.0, 0.0))
         self.nbi = (m + cfg.block[0] - 1) // cfg.block[0]
         self.threads = threads
@@ -276,7 +280,7 @@ class _DeviceAssign:
         # screen's exact-chain hint (a speed hint only, results never depend on it)
         E.set_label_hint(self.labels[1 - slot], self.m)
         try:
-            E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=get_variant(), inj=inj,
+            E.assign_dev(self.x_t, cent_t, yn_t, self.cfg.block, variant=self.variant, inj=inj,
                          checked=self.checked, delta_rel=self.delta_rel, abs_tol=self.abs_tol,
                          iteration=iteration, events=self.events, out_idx=self.labels[slot],
                          out_val=self.md)
@@ -333,9 +337,9 @@ class _StepGraph:
 
 def _graphable_shape(d, k):
     """fp32 shapes whose screened assignment is free of host synchronisation:
-    the CTA-pair screen (8 <= d <= 256) and the narrow screen (d > 256,
-    k + 4 <= 256), both with d % 4 == 0."""
-    return d % 4 == 0 and (8 <= d <= 256 or (d > 256 and k + 4 <= 256))
+    the CTA-pair screen (X resident up to d = 256, streamed up to 8192) and
+    the narrow screen, both with d % 4 == 0."""
+    return d % 4 == 0 and 8 <= d <= 8192
 
 
 class LloydEngine:
@@ -379,7 +383,7 @@ class LloydEngine:
         self.use_graph = bool(graph) and (dist is None or dist.capturable) and \
             ft_mode != "abft+dmr" and \
             update_hook is NOOP_HOOK and self.dtype == np.float32 and \
-            _graphable_shape(x_t.shape[1], k) and get_variant() != "exact"
+            _graphable_shape(x_t.shape[1], k) and self.A.variant in ("pair", "narrow", "tc")
         self.graphs = [None, None]
         # injected passes replay their own graphs, the schedule staged into
         # fixed device arrays (count on the device) before the replay

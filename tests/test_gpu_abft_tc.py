@@ -102,3 +102,31 @@ def test_pair_in_kernel_location_and_correction(m, d, k):
     for e in evs:
         r = e.tile[0] * bm + e.loc[0]
         assert e.tile[1] == (group_of[r] * 128) // bn and e.iteration == 5
+
+
+@pytest.mark.parametrize("m,d,k", [(2000, 512, 600), (1200, 1024, 300)])
+def test_pair_streamed_x_checked_with_replay(m, d, k):
+    """d > 256 with several column tiles (X streamed through the stages and
+    re-read per tile): clean pass = oracle, injected pass = the exact checked
+    kernel's values and events (the reference's)."""
+    x, y = _data(m, d, k, seed=23)
+    lab, val = O.assign(x, y)
+    r_lab, r_val, evs = _checked(x, y, (32, 256, 16))
+    assert np.array_equal(r_lab, lab) and r_val.tobytes() == val.tobytes() and evs == []
+    flips, arrs = _flips(x, y, 8, 32, 256, seed=4)
+
+    def run(variant):
+        x_t, y_t = E.to_dev(x), E.to_dev(y)
+        ev = E.DevEvents(256)
+        d_rel, a_tol = Threshold.default_for(np.float32).kernel_params()
+        inj = E.DevInjection(tuple(np.array(a, copy=True) for a in arrs))
+        idx, v = E.assign_dev(x_t, y_t, E.row_sq_norms_dev(y_t), (32, 256, 16), variant=variant,
+                              inj=inj, checked=True, delta_rel=d_rel, abs_tol=a_tol, iteration=1,
+                              events=ev)
+        return E.to_host(idx), E.to_host(v), events_from_ring(ev.read()[1])
+
+    li, vi, ei = run("exact")
+    lp, vp, ep = run("pair")
+    assert np.array_equal(li, lp) and vi.tobytes() == vp.tobytes()
+    key = lambda e: (e.iteration, e.tile, e.interval, e.loc)  # noqa: E731
+    assert sorted(ei, key=key) == sorted(ep, key=key) and len(ei) >= 1
