@@ -269,8 +269,17 @@ __global__ void __launch_bounds__(DS_THREADS, 1) dscreen_kernel(DsParams P) {
 // row tig, column gid; accumulators: rows gid / gid + 8, columns 2 tig, +1.
 // The DMMA accumulates each product into the sum without intermediate
 // rounding of the product (like DFMA), so the DFMA error bound holds.
-constexpr int DM_BM = 128, DM_BN = 128, DM_KC = 16, DM_STAGES = 4;
-constexpr int DM_PA = DM_BM + 4, DM_PB = DM_BN + 4;  // padded k-rows: conflict-free fragments
+// MT = m16 tiles per warp: 4 -> 128-row CTA tiles (255 registers, one CTA
+// per SM); 2 -> 64-row tiles, <= 128 registers and a 3-stage ring, so two
+// CTAs share an SM and one's refine / epilogue overlaps the other's DMMAs.
+constexpr int DM_BN = 128, DM_KC = 16, DM_PB = DM_BN + 4;  // padded k-rows: conflict-free fragments
+template <int MT> struct DmGeom {
+    static constexpr int BM = 32 * MT, PA = BM + 4, STAGES = MT == 4 ? 4 : 3, MINB = MT == 4 ? 1 : 2;
+    static constexpr size_t smem() {
+        return sizeof(double) * (size_t(STAGES) * DM_KC * (PA + DM_PB) + DM_BN + 4 * BM * 3) +
+               sizeof(int) * 4 * BM;
+    }
+};
 
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
     asm volatile(
@@ -286,8 +295,10 @@ __device__ __forceinline__ void top2_d(double s, double &t1, double &t2) {
     t2 = fmin(t2, hi);
 }
 
-template <bool CHK>
-__global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
+template <bool CHK, int MT>
+__global__ void __launch_bounds__(256, DmGeom<MT>::MINB) dmma_screen_kernel(DsParams P) {
+    constexpr int DM_BM = DmGeom<MT>::BM, DM_PA = DmGeom<MT>::PA, DM_STAGES = DmGeom<MT>::STAGES;
+    constexpr int NR = 2 * MT;  // accumulator rows per thread (mt, half)
     extern __shared__ __align__(16) double dm_smem[];
     double(*As)[DM_KC][DM_PA] = reinterpret_cast<double(*)[DM_KC][DM_PA]>(dm_smem);
     double(*Bs)[DM_KC][DM_PB] =
@@ -304,10 +315,10 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
     for (int64_t rt = blockIdx.x; rt < nrt; rt += gridDim.x) {
         const int64_t r0 = rt * DM_BM;
         // running per-row state for this thread's 8 rows (mt, half)
-        double m1[8], m2[8], rs[8];
-        int t1[8];
+        double m1[NR], m2[NR], rs[NR];
+        int t1[NR];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < NR; ++i) {
             m1[i] = INFINITY;
             m2[i] = INFINITY;
             rs[i] = 0.0;
@@ -315,9 +326,9 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
         }
         for (int64_t ct = 0; ct < nct; ++ct) {
             const int64_t c0 = ct * DM_BN;
-            double acc[4][4][4];
+            double acc[MT][4][4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a)
+            for (int a = 0; a < MT; ++a)
 #pragma unroll
                 for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -354,16 +365,16 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
 #pragma unroll
                 for (int ks = 0; ks < DM_KC / 4; ++ks) {
                     const int kr = ks * 4 + tig;
-                    double a0[4], a1[4], b0[4];
+                    double a0[MT], a1[MT], b0[4];
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt) {
-                        a0[mt] = As[buf][kr][wm * 64 + mt * 16 + gid];
-                        a1[mt] = As[buf][kr][wm * 64 + mt * 16 + gid + 8];
+                    for (int mt = 0; mt < MT; ++mt) {
+                        a0[mt] = As[buf][kr][wm * (16 * MT) + mt * 16 + gid];
+                        a1[mt] = As[buf][kr][wm * (16 * MT) + mt * 16 + gid + 8];
                     }
 #pragma unroll
                     for (int nt = 0; nt < 4; ++nt) b0[nt] = Bs[buf][kr][wn * 32 + nt * 8 + gid];
 #pragma unroll
-                    for (int mt = 0; mt < 4; ++mt)
+                    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                         for (int nt = 0; nt < 4; ++nt) dmma16x8x4(acc[mt][nt], a0[mt], a1[mt], b0[nt]);
                 }
@@ -372,7 +383,7 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
             // epilogue: per row, top-2 over this thread's 8 columns, then over
             // the 4 lanes (tig) sharing the row -> the warp's 32-column strip
 #pragma unroll
-            for (int mt = 0; mt < 4; ++mt)
+            for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     double a1v = INFINITY, a2v = INFINITY, ssum = 0.0;
@@ -406,8 +417,8 @@ __global__ void __launch_bounds__(256, 1) dmma_screen_kernel(DsParams P) {
         // merge the 4 column-strip warps of every row through shared memory
         if (tig == 0) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int rr = wm * 64 + (i >> 1) * 16 + gid + (i & 1) * 8;
+            for (int i = 0; i < NR; ++i) {
+                const int rr = wm * (16 * MT) + (i >> 1) * 16 + gid + (i & 1) * 8;
                 double *q = red + (wn * DM_BM + rr) * 3;
                 q[0] = m1[i];
                 q[1] = m2[i];
@@ -545,11 +556,15 @@ int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn
         FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<grid, DS_THREADS, smem, st>>>(P);
     } else {
-        const size_t smem = sizeof(double) * (DM_STAGES * DM_KC * (DM_PA + DM_PB) + DM_BN +
-                                              4 * DM_BM * 3) + sizeof(int) * 4 * DM_BM;
-        const int64_t nrt2 = (m + DM_BM - 1) / DM_BM;
-        const unsigned grid2 = unsigned(std::min<int64_t>(nrt2, int64_t(nsm)));
-        auto kern = ft ? dmma_screen_kernel<true> : dmma_screen_kernel<false>;
+        const char *mte = getenv("FTK_DMMA_MT");  // A/B knob: 4 = one 128-row CTA per SM
+        const bool big = mte && atoi(mte) == 4;
+        const int bm = big ? DmGeom<4>::BM : DmGeom<2>::BM;
+        const size_t smem = big ? DmGeom<4>::smem() : DmGeom<2>::smem();
+        const int64_t nrt2 = (m + bm - 1) / bm;
+        const int per_sm = big ? 1 : 2;
+        const unsigned grid2 = unsigned(std::min<int64_t>(nrt2, int64_t(nsm) * per_sm));
+        auto kern = big ? (ft ? dmma_screen_kernel<true, 4> : dmma_screen_kernel<false, 4>)
+                        : (ft ? dmma_screen_kernel<true, 2> : dmma_screen_kernel<false, 2>);
         FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         kern<<<grid2, 256, smem, st>>>(P);
     }

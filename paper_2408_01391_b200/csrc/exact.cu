@@ -98,7 +98,7 @@ __device__ void diagnose(const ExactParams &P, T *tile, int ts, double *s1, doub
                          double *s2, double *ref2, double *t1, double *t2, double *r1,
                          double *r2, double *rs1, double *rs2, double *c2, int *ints,
                          int64_t i0, int mi, int64_t j0, int nj, int64_t t_last, double tol,
-                         double *out_delta) {
+                         double *out_delta, T *Xs, T *Cs, int64_t xs_stride) {
     const T *a = static_cast<const T *>(P.x);
     const T *b = static_cast<const T *>(P.y);
     const int64_t kdim = P.d;
@@ -129,25 +129,46 @@ __device__ void diagnose(const ExactParams &P, T *tile, int ts, double *s1, doub
     for (int64_t tt = 0; tt <= t_last; ++tt) {
         int64_t k0 = tt * bk;
         int kk = int(bk < kdim - k0 ? bk : kdim - k0);
+        // the interval's operand panels, staged in the (now idle) k-chunk
+        // buffers: the sequential sums below then read shared memory instead
+        // of strided global loads (same values, same order)
+        const bool staged = kk <= KC;
+        if (staged) {
+            __syncthreads();
+            for (int e = tid; e < mi * kk; e += nth) {
+                const int i = e / kk, k = e % kk;
+                Xs[k * xs_stride + i] = a[(i0 + i) * kdim + k0 + k];
+            }
+            for (int e = tid; e < nj * kk; e += nth) {
+                const int j = e / kk, k = e % kk;
+                Cs[j * (KC + 1) + k] = b[(j0 + j) * kdim + k0 + k];
+            }
+            __syncthreads();
+        }
+        auto A_ = [&](int i, int k) {
+            return double(staged ? Xs[k * xs_stride + i] : a[(i0 + i) * kdim + k0 + k]);
+        };
+        auto B_ = [&](int j, int k) {
+            return double(staged ? Cs[j * (KC + 1) + k] : b[(j0 + j) * kdim + k0 + k]);
+        };
         for (int k = tid; k < kk; k += nth) {
             double a1 = 0.0, a2 = 0.0;
             for (int j = 0; j < nj; ++j) {
-                double v = double(b[(j0 + j) * kdim + k0 + k]);
+                double v = B_(j, k);
                 a1 = add_rn(a1, v);
                 a2 = add_rn(a2, mul_rn(double(j + 1), v));
             }
             rs1[k] = a1;
             rs2[k] = a2;
             double c = 0.0;
-            for (int i = 0; i < mi; ++i)
-                c = add_rn(c, mul_rn(double(i + 1), double(a[(i0 + i) * kdim + k0 + k])));
+            for (int i = 0; i < mi; ++i) c = add_rn(c, mul_rn(double(i + 1), A_(i, k)));
             c2[k] = c;
         }
         __syncthreads();
         for (int i = tid; i < mi; i += nth) {
             double a1 = 0.0, a2 = 0.0;
             for (int k = 0; k < kk; ++k) {
-                double v = double(a[(i0 + i) * kdim + k0 + k]);
+                double v = A_(i, k);
                 a1 = add_rn(a1, mul_rn(v, rs1[k]));
                 a2 = add_rn(a2, mul_rn(v, rs2[k]));
             }
@@ -156,8 +177,7 @@ __device__ void diagnose(const ExactParams &P, T *tile, int ts, double *s1, doub
         }
         for (int j = tid; j < nj; j += nth) {
             double s = ref2[j];
-            for (int k = 0; k < kk; ++k)
-                s = add_rn(s, mul_rn(c2[k], double(b[(j0 + j) * kdim + k0 + k])));
+            for (int k = 0; k < kk; ++k) s = add_rn(s, mul_rn(c2[k], B_(j, k)));
             ref2[j] = s;
         }
         __syncthreads();
@@ -449,7 +469,7 @@ __global__ void __launch_bounds__(exact_max_threads(TM)) exact_tile_kernel(Exact
             if (nviol) {
                 double delta = 0.0;
                 diagnose<T>(P, tile, ts, s1, rf1, s2, rf2, t1, t2, r1, r2, rs1, rs2, c2, ints,
-                            i0, mi, j0, nj, nbk - 1, tol, &delta);
+                            i0, mi, j0, nj, nbk - 1, tol, &delta, Xs, Cs, bm);
                 if (tid == 0) {
                     unsigned long long c = atomicAdd(P.ev_count, 1ull);
                     if (int64_t(c) < P.ev_cap) {
@@ -548,26 +568,26 @@ __global__ void exact_split_merge_kernel(const T *pv, const int32_t *pj, int gy,
 // bmax[bj] = max |y| over the rows of logical column block bj (_block_absmax)
 template <typename T>
 __global__ void block_absmax_kernel(const T *y, int64_t k, int64_t d, int64_t bn, double *bmax) {
+    // grid (column blocks, slices): each CTA takes a slice of its block's
+    // rows; the maximum of non-negative doubles is order-free, so the slices
+    // merge with an integer atomicMax on the bit pattern (bmax pre-zeroed)
     int64_t bj = blockIdx.x;
     int64_t j0 = bj * bn;
     int64_t nj = bn < k - j0 ? bn : k - j0;
+    const int64_t n = nj * d, per = (n + gridDim.y - 1) / gridDim.y;
+    const int64_t e0 = int64_t(blockIdx.y) * per, e1 = e0 + per < n ? e0 + per : n;
     double m = 0.0;
-    for (int64_t e = threadIdx.x; e < nj * d; e += blockDim.x) {
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         double v = fabs(double(y[j0 * d + e]));
         m = v > m ? v : m;
     }
-    __shared__ double sh[32];
     for (int off = 16; off; off >>= 1) {
         double o = __shfl_xor_sync(0xffffffffu, m, off);
         m = o > m ? o : m;
     }
-    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = m;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mm = 0.0;
-        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) mm = sh[w] > mm ? sh[w] : mm;
-        bmax[bj] = mm;
-    }
+    if ((threadIdx.x & 31) == 0 && m > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long *>(bmax + bj),
+                  static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
 // _row_sq_norms: s = x0*x0; s += xj*xj, left to right in dtype
@@ -718,11 +738,14 @@ int exact_run_m(ftk_ctx *ctx, int dtype, const void *x, const void *y, const voi
         double *bmax = static_cast<double *>(scratch(ctx, SLOT_BMAX, sizeof(double) * (nbj + 1), st));
         if (!bmax) return FTK_ERR_CUDA;
         if (nbj > 0) {
+            FTK_CUDA(cudaMemsetAsync(bmax, 0, sizeof(double) * nbj, st));
+            const int64_t per_block = std::min<int64_t>(bn, k) * d;
+            const unsigned sl = unsigned(std::max<int64_t>(1, std::min<int64_t>(64, per_block / 4096)));
             if (dtype == FTK_F32)
-                block_absmax_kernel<float><<<unsigned(nbj), 256, 0, st>>>(
+                block_absmax_kernel<float><<<dim3(unsigned(nbj), sl), 256, 0, st>>>(
                     static_cast<const float *>(y), k, d, bn, bmax);
             else
-                block_absmax_kernel<double><<<unsigned(nbj), 256, 0, st>>>(
+                block_absmax_kernel<double><<<dim3(unsigned(nbj), sl), 256, 0, st>>>(
                     static_cast<const double *>(y), k, d, bn, bmax);
             FTK_LAUNCHED("block_absmax_kernel");
         }

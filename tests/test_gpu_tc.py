@@ -12,6 +12,7 @@ pytestmark = pytest.mark.gpu
 
 P = pytest.importorskip("paper_2408_01391_b200")
 from paper_2408_01391_b200 import _engine as E  # noqa: E402
+from paper_2408_01391_b200 import gemm as G  # noqa: E402
 
 
 @pytest.fixture(autouse=True, scope="module")
@@ -126,7 +127,12 @@ def test_tc_checked_matches_reference_events(golden):
         entries = [FaultEntry(int(e[0]), (int(e[1]), int(e[2])), (int(e[3]), int(e[4])), int(e[5]))
                    for e in ent]
         h = ScheduledFaultHook(FaultSchedule(entries))
-        r2, rep2 = P.checked_assign(xx, yy, cfg=cfg, hook=h)
+        old = G.get_variant()
+        G.set_variant("tc")  # the tensor-core screen, whatever the variant table prefers
+        try:
+            r2, rep2 = P.checked_assign(xx, yy, cfg=cfg, hook=h)
+        finally:
+            G.set_variant(old)
         assert np.array_equal(r2.assignments, z[f"{n}_lab"]), n
         assert r2.min_dists.tobytes() == z[f"{n}_val"].tobytes(), n
         ev = np.array([[e.iteration, e.tile[0], e.tile[1],
