@@ -47,6 +47,14 @@ extern "C" {
 #define FTK_VARIANT_AUTO 0
 #define FTK_VARIANT_EXACT 1  /* SIMT, reference evaluation order, bit-exact   */
 #define FTK_VARIANT_TC 2     /* tcgen05 tf32 screen + certified exact refine  */
+/* Forced kernel families (variants.py VariantTable; the reference's
+ * TuneTable/select, tuner.py:230-351, chooses a CPU tile instead).  Each is
+ * bit-exact like every other variant; a family that does not apply to the
+ * dtype is FTK_ERR_ARG, a shape it cannot take FTK_ERR_UNSUPPORTED. */
+#define FTK_VARIANT_TC_PAIR 3    /* f32: CTA-pair tcgen05 screen (tc_pair.cu)   */
+#define FTK_VARIANT_TC_NARROW 4  /* f32: streamed-X narrow screen (tc_narrow.cu) */
+#define FTK_VARIANT_F64_DMMA 5   /* f64: DMMA screen (dscreen.cu)               */
+#define FTK_VARIANT_F64_DFMA 6   /* f64: DFMA SIMT screen (dscreen.cu)          */
 
 /* Scheduled injections for one kernel call: the eight arrays of
  * FaultHook.kernel_arrays (faults.py:261-277), as DEVICE pointers.  Entries
