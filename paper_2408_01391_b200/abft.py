@@ -125,6 +125,29 @@ def events_from_ring(raw, iteration_filter=None):
     return out
 
 
+def split_ranges(n_blocks, threads):
+    """Contiguous [lo, hi) row-block ranges, one per reference worker
+    (_kernels.py:615-619): each worker owns an event buffer of its own."""
+    threads = max(1, min(int(threads), n_blocks)) if n_blocks else 1
+    step = max(1, (n_blocks + threads - 1) // threads)
+    return [(lo, min(lo + step, n_blocks)) for lo in range(0, n_blocks, step)]
+
+
+def worker_overflow(raw, n_inj, nbi, threads):
+    """The reference's overflow rule (abft.py:280-316): every worker's buffer
+    holds n_inj + 64 events and ANY worker exceeding it raises.  The device
+    ring holds the sum of the worker capacities, so a ring overflow implies a
+    worker overflow, and otherwise every event is present to count per range."""
+    cap = n_inj + 64
+    ranges = split_ranges(nbi, threads)
+    if len(ranges) <= 1:
+        return len(raw) > cap
+    los = np.array([lo for lo, _ in ranges], np.int64)
+    bi = np.array([rec[1] for rec, _ in raw], np.int64)
+    per = np.bincount(np.searchsorted(los, bi, side="right") - 1, minlength=len(ranges))
+    return bool((per > cap).any())
+
+
 def _scheduled_tiles(inj):
     if inj is None or inj.n == 0:
         return set()
@@ -148,6 +171,11 @@ def _checked_run(a, b, cfg, thr, hook, iteration, threads, y_norms, materialize)
     a_t, b_t = E.to_dev(a), E.to_dev(b)
     events = E.DevEvents(cap)
     if m == 0:
+        if inj is not None:
+            inj.finish()
+        if hook is not None:
+            hook.absorb_kernel_results(iteration, *(inj.host[5:8] if inj is not None else
+                                                    (np.zeros(0, np.int64), np.zeros(0), np.zeros(0))))
         out = (np.empty((0, k), dt) if materialize
                else AssignResult(np.empty(0, np.int64), np.empty(0, dt)))
         return out, DetectionReport()
@@ -163,7 +191,7 @@ def _checked_run(a, b, cfg, thr, hook, iteration, threads, y_norms, materialize)
                                 checked=True, delta_rel=delta_rel, abs_tol=abs_tol,
                                 iteration=iteration, events=events)
     overflow, raw = events.read()
-    if overflow:
+    if overflow or worker_overflow(raw, n_inj, nbi, threads):
         raise RuntimeError("detection event buffer overflow; threshold likely miscalibrated")
     evs = events_from_ring(raw)
     report = DetectionReport(events=evs)

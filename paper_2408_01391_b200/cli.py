@@ -25,7 +25,7 @@ from .abft import Threshold
 from .errors import FormatError
 from .kmeans import KMeansConfig, lloyd
 from .matrix import mat_load, mat_load_pinned, mat_random, mat_store, precision_of
-from .tiles import parse_tile
+from .tiles import TileTable, parse_tile
 
 REPORT_SCHEMA_VERSION = 1
 
@@ -102,11 +102,16 @@ def cmd_cluster(args):
     if args.inject and args.inject != "none" and args.ft == "off":
         print("warning: faults injected without protection", file=sys.stderr)
     dtype = np.float32 if _precision(x) == "single" else np.float64
-    tile = "auto" if args.tile == "auto" else parse_tile(args.tile, dtype)
+    tune_table = TileTable.load(args.tune_table) if args.tune_table else None
+    tile = "auto"
+    if args.tile != "auto":
+        tile = parse_tile(args.tile, dtype)
+    elif tune_table is None:
+        print("warning: --tile auto with no tune table, using default config", file=sys.stderr)
     config = KMeansConfig(
         k=args.k, max_iters=args.max_iters, tol=args.tol, seed=args.seed, ft_mode=args.ft,
         init=args.init, tile=tile, threshold=Threshold(args.delta) if args.delta else None,
-        threads=args.threads, tune_table=None)
+        threads=args.threads, tune_table=tune_table)
     result = lloyd(x, config, fault_spec=args.inject)
     m, n = x.shape
     flops = 2.0 * m * n * args.k * (result.iters + 1)
@@ -165,7 +170,7 @@ def build_parser():
     c.add_argument("--tol", type=float, default=1e-4)
     c.add_argument("--tile", default="auto", help='"auto" or bm,bn,bk,sm,sn,sk')
     c.add_argument("--tune-table", default=None,
-                   help="accepted for compatibility (CPU tuner tables do not apply to the GPU tile)")
+                   help="reference tune-table CSV: picks the logical tile (fault grid, event coordinates)")
     c.add_argument("--delta", type=float, default=None, help="checksum threshold scale")
     c.add_argument("--init", choices=["kmeanspp", "random-sample"], default="kmeanspp")
     c.add_argument("--report", default=None, help="write a phase,metric,value CSV")

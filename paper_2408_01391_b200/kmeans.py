@@ -22,7 +22,7 @@ import numpy as np
 from . import _engine as E
 from . import _native as N
 from .abft import DetectionEvent, DetectionReport, Threshold, checked_assign, events_from_ring
-from .abft import _scheduled_tiles
+from .abft import _scheduled_tiles, worker_overflow
 from .errors import FaultEscalationError
 from .faults import NOOP_HOOK, FaultHook, FaultSpec, ScheduledFaultHook, plan_faults
 from .gemm import _as_operand, _dtype, _is_torch, fused_assign, get_variant, resolve_threads
@@ -290,7 +290,7 @@ class _DeviceAssign:
 
     def ev_cap(self, n_inj):
         """Event capacity of a pass with n_inj flips: the reference gives
-        every worker n_inj + 64 (abft.py)."""
+        every worker n_inj + 64 (abft.py); finish() applies the per-worker rule."""
         return (n_inj + 64) * max(1, min(self.threads, self.nbi))
 
     def finish(self, hook, iteration, inj, n_events=None, replayed=False):
@@ -299,10 +299,11 @@ class _DeviceAssign:
         iteration number of its capture; the records get the real one."""
         report = None
         if self.checked:
-            overflow, raw = self.events.read(n_events, cap=self.ev_cap(inj.n if inj else 0))
+            n_inj = inj.n if inj else 0
+            overflow, raw = self.events.read(n_events, cap=self.ev_cap(n_inj))
             if replayed:
                 raw = [((iteration,) + tuple(rec[1:]), d) for rec, d in raw]
-            if overflow:
+            if overflow or worker_overflow(raw, n_inj, self.nbi, self.threads):
                 raise RuntimeError("detection event buffer overflow; threshold likely "
                                    "miscalibrated")
             evs = events_from_ring(raw)

@@ -148,3 +148,44 @@ def test_config_validation():
         P.fused_assign(np.zeros((4, 3), np.float32), np.zeros((2, 5), np.float32))
     with pytest.raises(ValueError, match="dtypes"):
         P.fused_assign(np.zeros((4, 3), np.float32), np.zeros((2, 3), np.float64))
+
+
+def test_tile_table_reads_reference_tune_table(tmp_path):
+    """tiles.TileTable parses the reference's tune-table CSV (tuner.py:268-293)
+    and looks shapes up with its rule: exact key, else nearest (N, K) in log2
+    distance within the precision, else the default tiles."""
+    from paper_2408_01391_b200.tiles import TileTable, default_config, make_config
+
+    p = tmp_path / "tt.csv"
+    p.write_text("# M_bucket,N,K,precision,bm,bn,bk,sm,sn,sk,um,un,uk,gflops,reps\n"
+                 "65536,32,64,single,64,128,32,32,32,32,16,8,4,12.5,3\n"
+                 "65536,128,1024,single,32,256,16,32,64,16,16,8,4,40.0,3\n"
+                 "1024,64,256,double,128,64,16,32,32,16,8,8,4,3.0,2\n")
+    t = TileTable.load(str(p))
+    f32, f64 = np.float32, np.float64
+    assert t.lookup((100_000, 32, 64), f32) == make_config((64, 128, 32), (32, 32, 32), (16, 8, 4))
+    # nearest in (log2 N, log2 K): (100, 800) is closer to (128, 1024) than to (32, 64)
+    assert t.lookup((5, 100, 800), f32).block == (32, 256, 16)
+    assert t.lookup((5, 40, 50), f32).block == (64, 128, 32)
+    assert t.lookup((7, 3, 3), f64).block == (128, 64, 16)
+    assert TileTable().lookup((7, 3, 3), f64) == default_config(f64)
+    bad = tmp_path / "bad.csv"
+    bad.write_text("1,2,3,single,1\n")
+    with pytest.raises(ValueError, match="bad tune-table row"):
+        TileTable.load(str(bad))
+
+
+def test_event_overflow_is_per_worker():
+    """The reference raises when ANY worker's n_inj + 64 buffer overflows
+    (abft.py:280-316), not only when the total does."""
+    from paper_2408_01391_b200.abft import split_ranges, worker_overflow
+
+    assert split_ranges(10, 4) == [(0, 3), (3, 6), (6, 9), (9, 10)]
+    assert split_ranges(0, 8) == []
+    ev = lambda bi: ((0, bi, 0, 0, 0, 0, 0), 0.0)  # noqa: E731
+    burst = [ev(0)] * 65  # 65 events in worker 0's rows, total well under 4 * 64
+    assert worker_overflow(burst, 0, 10, 4)
+    assert not worker_overflow(burst, 1, 10, 4)
+    spread = [ev(b) for b in (0, 3, 6, 9)] * 64
+    assert not worker_overflow(spread, 0, 10, 4)
+    assert worker_overflow([ev(0)] * 65, 0, 10, 1)
