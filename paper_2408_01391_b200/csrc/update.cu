@@ -433,6 +433,148 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
     }
 }
 
+// ------------------------------------- warp-specialised ordered chains ----
+// The same ordered chains, with the gathers decoupled from the chain.  One
+// CTA per (cluster, slab of 32*VEC features = 512 bytes of a row): warp 0 is
+// the CONSUMER (each lane folds VEC = 16/sizeof(T) independent float64
+// chains, members in ascending sample order, from 16-byte shared reads);
+// warps 1..CS_LOADERS are LOADERS that take 16-member groups round-robin and
+// gather them into a ring of CS_NG slots with 16-byte cp.async (one
+// instruction per member row), signalling each slot's mbarrier through
+// cp.async.mbarrier.arrive.  A single warp's outstanding copies cap a
+// gather at ~10 GB/s per SM (measured: the 1-warp kernels above, with 8- and
+// 16-byte copies alike, run c4's update in 4.3 ms); seven loader warps keep
+// ~56 KB per CTA in flight, so the longest cluster's chain -- the kernel's
+// critical path -- is no longer fed by one warp.
+#ifndef FTK_CS_LOADERS
+#define FTK_CS_LOADERS 7
+#define FTK_CS_NG 8
+#endif
+constexpr int CS_GS = 16, CS_NG = FTK_CS_NG, CS_LOADERS = FTK_CS_LOADERS;
+constexpr size_t CS_SMEM = 256 + size_t(CS_NG) * CS_GS * 512;
+
+__device__ __forceinline__ void cs_cp16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cs_bar_init(uint64_t *bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(bar))), "r"(count));
+}
+__device__ __forceinline__ void cs_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void cs_cp_arrive(uint64_t *bar) {  // arrives when this thread's copies land
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(
+                     static_cast<unsigned>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+__device__ __forceinline__ void cs_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "CSW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra CSW_%=;\n\t}" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(bar))),
+        "r"(parity)
+        : "memory");
+}
+
+template <typename T, bool DMR>
+__global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
+    const T *x, int64_t d, int64_t nslab, const int32_t *perm, const int64_t *offsets, double *sums_a,
+    double *sums_b) {
+    constexpr int VEC = 16 / sizeof(T);
+    constexpr int W = 32 * VEC;  // features per slab (512 bytes)
+    extern __shared__ __align__(128) unsigned char cs_smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(cs_smem);
+    uint64_t *empty = full + CS_NG;
+    unsigned char *ring = cs_smem + 256;  // [CS_NG][CS_GS][512 bytes]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = int64_t(blockIdx.x) / nslab, s = int64_t(blockIdx.x) % nslab;
+    const int64_t f0 = s * W;
+    const int fw = int(d - f0 < W ? d - f0 : W);  // a multiple of VEC
+    const bool live = lane * VEC < fw;
+    const int64_t lo = offsets[c], n = offsets[c + 1] - lo;
+    const int64_t ngrp = (n + CS_GS - 1) / CS_GS;
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < CS_NG; ++g) {
+            cs_bar_init(&full[g], 32);  // the 32 lanes of one loader warp
+            cs_bar_init(&empty[g], 1);  // the consumer
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp > 0) {
+        // ------------------------------------------------ loaders --
+        const T *xs = x + f0 + lane * VEC;
+        const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring)) + lane * 16;
+        int64_t g = warp - 1;
+        int32_t rows = (g < ngrp && lane < CS_GS && g * CS_GS + lane < n) ? __ldg(perm + lo + g * CS_GS + lane) : 0;
+        for (; g < ngrp; g += CS_LOADERS) {
+            const int slot = int(g % CS_NG);
+            const int64_t gn = g + CS_LOADERS;  // this warp's next group: indices in flight early
+            const int32_t next = (gn < ngrp && lane < CS_GS && gn * CS_GS + lane < n)
+                                     ? __ldg(perm + lo + gn * CS_GS + lane) : 0;
+            cs_wait(&empty[slot], (uint32_t(g / CS_NG) & 1u) ^ 1u);
+            const int cnt = int(n - g * CS_GS < CS_GS ? n - g * CS_GS : CS_GS);
+            const uint32_t dst = rbase + uint32_t(slot) * (CS_GS * 512);
+            if (cnt == CS_GS) {
+#pragma unroll
+                for (int u = 0; u < CS_GS; ++u) {
+                    const int32_t row = __shfl_sync(0xffffffffu, rows, u);
+                    if (live) cs_cp16(dst + u * 512, xs + int64_t(row) * d);
+                }
+            } else {
+                for (int u = 0; u < cnt; ++u) {
+                    const int32_t row = __shfl_sync(0xffffffffu, rows, u);
+                    if (live) cs_cp16(dst + u * 512, xs + int64_t(row) * d);
+                }
+            }
+            cs_cp_arrive(&full[slot]);
+            rows = next;
+        }
+    } else {
+        // ----------------------------------------------- consumer --
+        double acc_a[VEC], acc_b[VEC];
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc_a[v] = acc_b[v] = 0.0;
+        const T *base = reinterpret_cast<const T *>(ring) + lane * VEC;
+        for (int64_t g = 0; g < ngrp; ++g) {
+            const int slot = int(g % CS_NG);
+            cs_wait(&full[slot], uint32_t(g / CS_NG) & 1u);
+            const int cnt = int(n - g * CS_GS < CS_GS ? n - g * CS_GS : CS_GS);
+            const T *sl = base + size_t(slot) * CS_GS * W;
+            if (live) {
+                auto fold = [&](int u) {
+                    T v[VEC];
+                    *reinterpret_cast<uint4 *>(v) = *reinterpret_cast<const uint4 *>(sl + u * W);
+#pragma unroll
+                    for (int e = 0; e < VEC; ++e) {
+                        acc_a[e] = __dadd_rn(acc_a[e], double(v[e]));
+                        if (DMR) acc_b[e] = __dadd_rn(acc_b[e], double(v[e]));
+                    }
+                };
+                if (cnt == CS_GS) {
+#pragma unroll
+                    for (int u = 0; u < CS_GS; ++u) fold(u);
+                } else {
+                    for (int u = 0; u < cnt; ++u) fold(u);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) cs_arrive(&empty[slot]);
+        }
+        if (live) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+                sums_a[c * d + f0 + lane * VEC + e] = acc_a[e];
+                if (DMR) sums_b[c * d + f0 + lane * VEC + e] = acc_b[e];
+            }
+        }
+    }
+}
+
 // ------------------------------------------------ certified segmented sums --
 // The reference's float64 chain is order-dependent only if some partial sum
 // rounds.  For a (cluster, feature) chain whose values are all multiples of
@@ -1164,6 +1306,26 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     const int64_t warps = k * ((d + 31) / 32);
     const int block = 256;
     const unsigned grid = unsigned((warps * 32 + block - 1) / block);
+    const int vec = dtype == FTK_F32 ? 4 : 2;
+    if (pipe_chains && d % vec == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+        !(getenv("FTK_UPD_CHAIN") && atoi(getenv("FTK_UPD_CHAIN")) == 0)) {
+        // ordered chains, 16-byte copies of 512-byte row slabs
+        const int64_t nslab = (d + 32 * vec - 1) / (32 * vec);
+        const unsigned g = unsigned(k * nslab);
+        if (dtype == FTK_F32) {
+            auto xx = static_cast<const float *>(x);
+            auto kern = dmr ? chain_spec_kernel<float, true> : chain_spec_kernel<float, false>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CS_SMEM)));
+            kern<<<g, 32 * (1 + CS_LOADERS), CS_SMEM, st>>>(xx, d, nslab, vals_out, offsets, sums_a, dmr ? sums_b : nullptr);
+        } else {
+            auto xx = static_cast<const double *>(x);
+            auto kern = dmr ? chain_spec_kernel<double, true> : chain_spec_kernel<double, false>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CS_SMEM)));
+            kern<<<g, 32 * (1 + CS_LOADERS), CS_SMEM, st>>>(xx, d, nslab, vals_out, offsets, sums_a, dmr ? sums_b : nullptr);
+        }
+        FTK_LAUNCHED("chain_spec_kernel");
+        return FTK_OK;
+    }
     if (pipe_chains) {
         // few long chains: the reference's ordered chain, latency-hidden
         const unsigned g = unsigned((nwarps + CH_WARPS - 1) / CH_WARPS);

@@ -352,6 +352,31 @@ def test_update_paths_bit_exact(m, d, k, dt, tiny):
     assert c.tobytes() == ref.tobytes()
 
 
+@pytest.mark.parametrize("m,d,k,dt,env", [
+    (50000, 64, 37, np.float64, {}),                          # bulk-copy chains, one 512-byte slab
+    (40000, 130, 5, np.float64, {}),                          # partial last slab (2 features)
+    (30000, 7, 5, np.float64, {}),                            # rows not 16-byte aligned: cp.async chains
+    (40000, 64, 37, np.float64, {"FTK_UPD_CHAIN": "0"}),      # cp.async chains forced
+    (40000, 200, 9, np.float32, {"FTK_UPD_PATH": "pipe"}),    # float32 data through the bulk chains
+])
+@pytest.mark.parametrize("dmr", [False, True])
+def test_ordered_chain_kernels_bit_exact(m, d, k, dt, env, dmr, monkeypatch):
+    """The ordered float64 chains (bulk-copy and cp.async kernels, with and
+    without the DMR duplicate) equal numpy.bincount's sums bit for bit."""
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    rng = np.random.default_rng(m + d + k)
+    x = np.ascontiguousarray(rng.standard_normal((m, d)) * 3.0, dtype=dt)
+    lab = rng.integers(0, k, m).astype(np.int64)
+    lab[: m // 2] = 1  # one long chain
+    lab[-5:] = k - 1
+    c, counts, ev = P.update_step(x, lab, k, ft_mode="abft+dmr" if dmr else "off")
+    ref, ref_counts = O.update_step(x, lab, k)
+    assert counts.tolist() == ref_counts.tolist()
+    assert c.tobytes() == ref.tobytes()
+    assert ev == []
+
+
 def test_candidate_overflow_rows_go_exact():
     """Rows whose pass-2 candidate set exceeds its cap (300 identical
     centroids tie for every row) are resolved by the exact row kernel."""
