@@ -51,7 +51,7 @@ extern "C" {
  * TuneTable/select, tuner.py:230-351, chooses a CPU tile instead).  Each is
  * bit-exact like every other variant; a family that does not apply to the
  * dtype is FTK_ERR_ARG, a shape it cannot take FTK_ERR_UNSUPPORTED. */
-#define FTK_VARIANT_TC_PAIR 3    /* f32: CTA-pair tcgen05 screen (tc_pair.cu)   */
+#define FTK_VARIANT_TC_PAIR 3    /* CTA-pair tcgen05 screen (tc_pair.cu; f64: tc64.cu) */
 #define FTK_VARIANT_TC_NARROW 4  /* f32: streamed-X narrow screen (tc_narrow.cu) */
 #define FTK_VARIANT_F64_DMMA 5   /* f64: DMMA screen (dscreen.cu)               */
 #define FTK_VARIANT_F64_DFMA 6   /* f64: DFMA SIMT screen (dscreen.cu)          */
@@ -106,6 +106,16 @@ int ftk_row_info(ftk_ctx *ctx, const float *x, int64_t m, int64_t d, float *info
  * modified while registered; pass x = NULL to unregister.  The reference has
  * no counterpart (its kernels recompute nothing across calls). */
 int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const float *info);
+/* Float64 data screened on the tf32 tensor cores (tc64.cu): x32 (m x d fp32,
+ * caller-allocated) receives fp32(x), info the row bounds measured against
+ * the float64 rows (|x|^2, |x - tf32(fp32(x))|^2, max|x|, 0).  Registering
+ * them (ftk_ctx_set_rows64) lets every float64 assignment of the fit reuse
+ * the copy; unregistered calls convert per call.  Replaces nothing in the
+ * reference (its float64 kernel, _kernels.py:432-475, has no screen). */
+int ftk_row_info64(ftk_ctx *ctx, const double *x, int64_t m, int64_t d, float *x32, float *info,
+                   void *stream);
+int ftk_ctx_set_rows64(ftk_ctx *ctx, const double *x, int64_t m, int64_t d, const float *x32,
+                       const float *info);
 /* Label hint for the next assignments on this context: labels (m int32,
  * device) of the previous Lloyd iteration.  The narrow screen (d > 256,
  * k + 4 <= 256) computes the exact reference value of the hinted centroid

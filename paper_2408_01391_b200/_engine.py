@@ -286,33 +286,46 @@ def row_sq_norms_dev(x_t):
 
 
 class RowInfo:
-    """Per-fit screening bounds of an fp32 data matrix (ftk_row_info),
-    registered on the context for the lifetime of a fit (ftk_ctx_set_rows);
-    ``close`` unregisters them before the data can be freed or modified."""
+    """Per-fit screening bounds of the data matrix (ftk_row_info; float64
+    data also keep the fp32 copy the tensor cores screen, ftk_row_info64),
+    registered on the context for the lifetime of a fit (ftk_ctx_set_rows /
+    ftk_ctx_set_rows64); ``close`` unregisters them before the data can be
+    freed or modified."""
 
     def __init__(self, x_t):
         t = _torch()
         self.x_t = x_t
         self.info = None
-        if x_t.dtype != t.float32 or x_t.shape[0] == 0:
+        self.x32 = None
+        if x_t.dtype not in (t.float32, t.float64) or x_t.shape[0] == 0:
             return
         m, d = x_t.shape
+        if x_t.dtype == t.float64:
+            if d % 4 or d > 256:  # no tensor-core screen for this shape (tc64.cu)
+                return
+            self.x32 = t.empty((m, d), dtype=t.float32, device=x_t.device)
         self.info = t.empty((m, 4), dtype=t.float32, device=x_t.device)
+        self._compute()
+
+    def _compute(self):
+        m, d = self.x_t.shape
         lib = N.load()
-        N.check(lib.ftk_row_info(ctx(), ptr(x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
-        N.check(lib.ftk_ctx_set_rows(ctx(), ptr(x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
-        _ROWS_OWNER[x_t.device.index] = id(self)
+        if self.x32 is None:
+            N.check(lib.ftk_row_info(ctx(), ptr(self.x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
+            N.check(lib.ftk_ctx_set_rows(ctx(), ptr(self.x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
+        else:
+            N.check(lib.ftk_row_info64(ctx(), ptr(self.x_t), m, d, ptr(self.x32), ptr(self.info), stream()),
+                    "ftk_row_info64")
+            N.check(lib.ftk_ctx_set_rows64(ctx(), ptr(self.x_t), m, d, ptr(self.x32), ptr(self.info)),
+                    "ftk_ctx_set_rows64")
+        _ROWS_OWNER[self.x_t.device.index] = id(self)
 
     def refresh(self):
         """Recompute the bounds in place after x_t's contents changed (same
         buffers, so captured graphs stay valid) and register them again."""
         if self.info is None:
             return
-        m, d = self.x_t.shape
-        lib = N.load()
-        N.check(lib.ftk_row_info(ctx(), ptr(self.x_t), m, d, ptr(self.info), stream()), "ftk_row_info")
-        N.check(lib.ftk_ctx_set_rows(ctx(), ptr(self.x_t), m, d, ptr(self.info)), "ftk_ctx_set_rows")
-        _ROWS_OWNER[self.x_t.device.index] = id(self)
+        self._compute()
 
     def close(self):
         if self.info is not None:
@@ -321,6 +334,7 @@ class RowInfo:
                 N.load().ftk_ctx_set_rows(ctx(), None, 0, 0, None)
                 _ROWS_OWNER.pop(dev, None)
             self.info = None
+            self.x32 = None
 
     def __del__(self):
         try:

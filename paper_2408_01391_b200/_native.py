@@ -45,6 +45,8 @@ PROTOTYPES = {
     "ftk_kpp_update": (_int, [_p, _int, _p, _i64, _i64, _i64, _p, _int, _p, _p, _i64, _p]),
     "ftk_kpp_search": (_int, [_p, _p, _i64, _dbl, _p, _p, _p]),
     "ftk_ctx_set_rows": (_int, [_p, _p, _i64, _i64, _p]),
+    "ftk_row_info64": (_int, [_p, _p, _i64, _i64, _p, _p, _p]),
+    "ftk_ctx_set_rows64": (_int, [_p, _p, _i64, _i64, _p, _p]),
     "ftk_ctx_generation": (_i64, [_p]),
     "ftk_ctx_set_label_hint": (_int, [_p, _p, _i64]),
     "ftk_ctx_set_option": (_int, [_p, _int, _i64]),

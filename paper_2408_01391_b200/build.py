@@ -24,6 +24,7 @@ SOURCES = {
     "tc.cu": [],
     "tc_pair.cu": [],
     "tc_narrow.cu": [],
+    "tc64.cu": [],
     "dscreen.cu": [],
     "kpp.cu": [],
     "h2d.cu": [],

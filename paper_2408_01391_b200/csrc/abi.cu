@@ -91,6 +91,11 @@ int tc_checked_run(ftk_ctx *, int, const void *, const void *, const void *, int
                    int64_t, int64_t, int64_t, int64_t, double, double, int64_t, int32_t *, void *,
                    const ftk_injection *, ftk_events *, cudaStream_t);
 int tc_supported(int dtype, int64_t m, int64_t k, int64_t d);
+bool tc64_supported(int64_t m, int64_t k, int64_t d);
+int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn, int64_t m,
+                    int64_t k, int64_t d, int32_t *out_idx, double *out_val, const TcFt *ft,
+                    cudaStream_t st);
+int row_info64_run(const double *x, int64_t m, int64_t d, float *x32, float *info, cudaStream_t st);
 int dscreen_run(ftk_ctx *, const double *, const double *, const double *, int64_t, int64_t,
                 int64_t, int32_t *, double *, const TcFt *, cudaStream_t);
 int tc_last_fallback(ftk_ctx *, unsigned *, cudaStream_t);
@@ -105,7 +110,7 @@ struct FamilyScope {
     FamilyScope(ftk_ctx *c, int dtype, int variant) : ctx(c) {
         int fam = 0;
         switch (variant) {
-            case FTK_VARIANT_TC_PAIR: fam = 1; break;
+            case FTK_VARIANT_TC_PAIR: fam = dtype == FTK_F64 ? 5 : 1; break;
             case FTK_VARIANT_TC_NARROW: fam = 2; break;
             case FTK_VARIANT_F64_DMMA: fam = 3; break;
             case FTK_VARIANT_F64_DFMA: fam = 4; break;
@@ -119,6 +124,14 @@ struct FamilyScope {
     }
     ~FamilyScope() { ctx->family = 0; }
 };
+// float64 through the tf32 CTA-pair screen: forced, or by default on shapes
+// large enough to amortise the per-call fp32 copy of the centroids
+static bool use_tc64(ftk_ctx *ctx, int64_t m, int64_t k, int64_t d) {
+    if (ctx->family == 5) return true;
+    if (ctx->family != 0) return false;
+    if (const char *e = getenv("FTK_F64_TC")) return atoi(e) != 0 && tc64_supported(m, k, d);
+    return m >= 65536 && tc64_supported(m, k, d);
+}
 static bool forced_tc(int v) { return v == FTK_VARIANT_TC || v == FTK_VARIANT_TC_PAIR || v == FTK_VARIANT_TC_NARROW; }
 static bool forced_any(int v) { return v != FTK_VARIANT_AUTO && v != FTK_VARIANT_EXACT; }
 
@@ -190,6 +203,24 @@ int ftk_ctx_set_rows(ftk_ctx *ctx, const void *x, int64_t m, int64_t d, const fl
     ctx->rows_m = x ? m : 0;
     ctx->rows_d = x ? d : 0;
     ctx->rows_info = x ? info : nullptr;
+    ctx->rows_x32 = nullptr;
+    return FTK_OK;
+}
+
+int ftk_row_info64(ftk_ctx *ctx, const double *x, int64_t m, int64_t d, float *x32, float *info,
+                   void *stream) {
+    if (!ctx || d < 1 || m < 0 || (m > 0 && (!x || !x32 || !info))) { set_error("bad ctx/shape"); return FTK_ERR_ARG; }
+    return row_info64_run(x, m, d, x32, info, as_stream(stream));
+}
+
+int ftk_ctx_set_rows64(ftk_ctx *ctx, const double *x, int64_t m, int64_t d, const float *x32,
+                       const float *info) {
+    if (!ctx) { set_error("bad ctx"); return FTK_ERR_ARG; }
+    ctx->rows_x = x;
+    ctx->rows_m = x ? m : 0;
+    ctx->rows_d = x ? d : 0;
+    ctx->rows_info = x ? info : nullptr;
+    ctx->rows_x32 = x ? x32 : nullptr;
     return FTK_OK;
 }
 
@@ -224,6 +255,13 @@ int ftk_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, const void *
     if (!fs.ok) return FTK_ERR_ARG;
     cudaStream_t st = as_stream(stream);
     bool has_inj = inj && inj->n > 0;
+    if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && !has_inj && use_tc64(ctx, m, k, d)) {
+        // float64 screened on the tf32 tensor cores, certified in float64 (tc64.cu)
+        int rc = tc64_assign_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
+                                 static_cast<const double *>(ynorms), m, k, d, out_idx,
+                                 static_cast<double *>(out_val), nullptr, st);
+        if (rc != FTK_ERR_UNSUPPORTED || ctx->family == 5) return rc;
+    }
     if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && !has_inj) {
         // float64: DMMA / DFMA screen + certified exact refine (dscreen.cu)
         int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
@@ -251,6 +289,14 @@ int ftk_checked_assign(ftk_ctx *ctx, int dtype, int variant, const void *x, cons
     FamilyScope fs(ctx, dtype, variant);
     if (!fs.ok) return FTK_ERR_ARG;
     cudaStream_t st = as_stream(stream);
+    if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && bn >= 1 && bm >= 1 &&
+        use_tc64(ctx, m, k, d)) {
+        TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
+        int rc = tc64_assign_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),
+                                 static_cast<const double *>(ynorms), m, k, d, out_idx,
+                                 static_cast<double *>(out_val), &ft, st);
+        if (rc != FTK_ERR_UNSUPPORTED || ctx->family == 5) return rc;
+    }
     if (dtype == FTK_F64 && variant != FTK_VARIANT_EXACT && bn >= 1 && bm >= 1) {
         TcFt ft{delta_rel, abs_tol, bm, bn, bk, iteration, inj, ev};
         int rc = dscreen_run(ctx, static_cast<const double *>(x), static_cast<const double *>(y),

@@ -49,6 +49,7 @@ struct ftk_ctx {
     const void *rows_x = nullptr;
     int64_t rows_m = 0, rows_d = 0;
     const float *rows_info = nullptr;  // m x 4: |x|^2, |x - tf32(x)|^2, max|x|, 0
+    const float *rows_x32 = nullptr;   // float64 data: the fp32 copy the tensor cores screen
     // diagnostics of the last screened assignment on this context
     unsigned last_fb[3] = {0, 0, 0};              // pass-1 uncertified, exact rows, ABFT flags
     int last_path = 0;                            // pass-1 kernel: 0 single-CTA, 1 CTA pair
@@ -62,7 +63,8 @@ struct ftk_ctx {
     const int32_t *hint = nullptr;
     int64_t hint_m = 0;
     int inj_replay = 1;  // FTK_OPT_INJ_REPLAY: replay blocks with scheduled flips exactly
-    int family = 0;      // forced kernel family of the current call (0 auto, 1 pair, 2 narrow, 3 dmma, 4 dfma)
+    int family = 0;      // forced kernel family of the current call (0 auto, 1 pair, 2 narrow, 3 dmma, 4 dfma,
+                         // 5 float64 through the tf32 CTA-pair screen)
 };
 
 namespace ftk {
@@ -99,6 +101,10 @@ enum ScratchSlot {
     SLOT_KPP = 23,          // k-means++: prefix scan of d2, counters, CUB temp
     SLOT_NARROW = 24,       // narrow screen: augmented centroids, tolerances, winner-pass rows
     SLOT_PAIR_FLAG = 25,    // CTA-pair screen: records of checksum-flagged rows
+    SLOT_TC64_X = 26,       // float64 via tf32: per-call fp32 copy of X + row bounds
+    SLOT_TC64_C = 27,       // float64 via tf32: fp32 centroids, norms, bounds, counters
+    SLOT_TC64_REC = 28,     // float64 via tf32: per-row (j1, T) records, fallback rows
+    SLOT_TC64_G = 29,       // float64 via tf32: gathered uncertified rows (DMMA pass 2)
 };
 
 // ------------------------------------------------------- float helpers --

@@ -892,6 +892,11 @@ static int prep_csum(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t 
     return FTK_OK;
 }
 
+int prep_csum_run(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb, int trunc,
+                  float **csum, float **camax, cudaStream_t st, float **csumw) {
+    return prep_csum(ctx, slot, y, k, d, nkb, trunc, csum, camax, st, csumw);
+}
+
 // Reference-identical handling of scheduled flips: the logical row blocks
 // that carry an injection are recomputed by the exact checked kernel (the
 // reference's detection / location / correction / events, bit for bit) and

@@ -1,0 +1,337 @@
+// tc64.cu -- float64 assignment screened on the tf32 tensor cores.
+//
+// The reference evaluates float64 distances as sequential chains of
+// separately rounded products and sums (_kernels.py:44-102).  Its labels only
+// depend on those values through the row argmin, and Gaussian-blob data keep
+// the argmin gap many orders above tf32 screening error, so the float64 path
+// need not run at FP64 tensor rate (DMMA: ~36 TF/s on a B200) to be
+// bit-exact: it is screened by the same CTA-pair tcgen05 kind::tf32 kernel as
+// float32 data (tc_pair.cu, ~500+ TF/s) and certified in float64.
+//
+//   1. X32 = fp32(X) once per fit (registered with ftk_ctx_set_rows64) with
+//      per-row bounds computed against the float64 rows: ||x||^2,
+//      ||x - tf32(fp32(x))||^2, max|x|.  C32 / yn32 per call, with
+//      max_j ||c_j||^2 and max_j ||c_j - tf32(fp32(c_j))||^2.
+//   2. Screen (tc_pair.cu, F64 mode): s_j = yn32_j - 2 acc_j (fp32 TMEM).
+//      |s_j - ref_j| <= A + B|s_j| with the float32 path's A plus the fp32
+//      rounding of the float64 norms (2^-23 cmax^2) and the reference's own
+//      float64 chain error (2 (D+2) 2^-53 |x| cmax).  Per row the kernel
+//      records (j1, T = m2 - A - B|m2| - 2^-21(|m1|+|m2|)) -- and, checked,
+//      verifies the row checksum against x~ . sum_j c~_j as in float32.
+//   3. Refine (tc64_refine_kernel): d1 = yn_j1 - (acc + acc), acc the
+//      reference's float64 chain; d1 < T proves j1 is the reference's strict
+//      argmin and d1 its min_dist bits.
+//   4. Rows no certificate covers (near ties, checksum flags, non-finite) go
+//      to the DMMA screen (dscreen.cu), whose own leftovers go exact.
+// Scheduled flips are replayed by the exact checked kernel over their logical
+// row blocks (reference-identical records), like the DMMA path.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+#include "tc_pair.cuh"
+
+namespace ftk {
+
+int make_tc_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols, uint32_t box_rows);
+int prep_csum_run(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb, int trunc,
+                  float **csum, float **camax, cudaStream_t st, float **csumw);
+int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn, int64_t m,
+                int64_t k, int64_t d, int32_t *out_idx, double *out_val, const TcFt *ft,
+                cudaStream_t st);
+
+constexpr int T64_KB = 32;
+
+// fp32 upper bound of a non-negative double
+__device__ __forceinline__ float up32(double v) { return __double2float_ru(v * (1.0 + 0x1p-40)); }
+
+// X32 = fp32(X) and the per-row screening bounds, one warp per row.
+__global__ void row_info64_kernel(const double *x, int64_t m, int64_t d, float *x32, float4 *info) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = w0; i < m; i += nw) {
+        double xx = 0.0, ee = 0.0, am = 0.0;
+        for (int64_t f = lane; f < d; f += 32) {
+            const double v = x[i * d + f];
+            const float v32 = __double2float_rn(v);
+            x32[i * d + f] = v32;
+            const double r = v - double(tf32_trunc(v32));
+            xx = fma(v, v, xx);
+            ee = fma(r, r, ee);
+            am = fmax(am, fabs(v));
+        }
+        for (int off = 16; off; off >>= 1) {
+            xx += __shfl_xor_sync(0xffffffffu, xx, off);
+            ee += __shfl_xor_sync(0xffffffffu, ee, off);
+            am = fmax(am, __shfl_xor_sync(0xffffffffu, am, off));
+        }
+        if (lane == 0) info[i] = make_float4(up32(xx), up32(ee), up32(am), 0.0f);
+    }
+}
+
+// C32 = fp32(C), yn32 = fp32(yn); bounds[0] >= max_j yn_j, bounds[1] >=
+// max_j ||c_j - tf32(fp32(c_j))||^2 (zeroed by the caller; non-negative
+// floats order like their bit patterns).
+__global__ void tc64_prep_kernel(const double *y, const double *yn, int64_t k, int64_t d, float *y32,
+                                 float *yn32, float *bounds) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    float mx = 0.0f, me = 0.0f;
+    for (int64_t j = w0; j < k; j += nw) {
+        double e = 0.0;
+        for (int64_t f = lane; f < d; f += 32) {
+            const double v = y[j * d + f];
+            const float v32 = __double2float_rn(v);
+            y32[j * d + f] = v32;
+            const double r = v - double(tf32_trunc(v32));
+            e = fma(r, r, e);
+        }
+        for (int off = 16; off; off >>= 1) e += __shfl_xor_sync(0xffffffffu, e, off);
+        me = fmaxf(me, up32(e));
+        mx = fmaxf(mx, up32(fabs(yn[j])));
+        if (lane == 0) yn32[j] = __double2float_rn(yn[j]);
+    }
+    if (lane == 0) {
+        atomicMax(reinterpret_cast<int *>(bounds), __float_as_int(mx));
+        atomicMax(reinterpret_cast<int *>(bounds + 1), __float_as_int(me));
+    }
+}
+
+// Certify each screened row in float64: the reference's chain for the
+// winner, d1 < T.  Uncertified rows are appended (warp-aggregated) to fb.
+__global__ void tc64_refine_kernel(const double *x, const double *y, const double *yn, int64_t m,
+                                   int64_t d, const int2 *rec, int32_t *out_idx, double *out_val,
+                                   int32_t *fb, unsigned *fb_count) {
+    const int lane = threadIdx.x & 31;
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < m; base += stride) {
+        const int64_t row = base + threadIdx.x;
+        bool need = false;
+        if (row < m) {
+            const int2 r = rec[row];
+            const int j = r.x;
+            bool ok = false;
+            double dval = 0.0;
+            if (j >= 0) {
+                const double *xr = x + row * d;
+                const double *cr = y + int64_t(j) * d;
+                double acc = 0.0;
+                int64_t f = 0;
+                if ((d & 1) == 0) {
+                    const double2 *x2 = reinterpret_cast<const double2 *>(xr);
+                    const double2 *c2 = reinterpret_cast<const double2 *>(cr);
+                    // 16 features per step: one 128-byte line of the row in flight at once
+                    for (; f + 16 <= d; f += 16) {
+                        double2 xv[8], cv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            xv[u] = __ldcs(x2 + f / 2 + u);  // streamed once
+                            cv[u] = __ldg(c2 + f / 2 + u);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            acc = __dadd_rn(acc, __dmul_rn(xv[u].x, cv[u].x));
+                            acc = __dadd_rn(acc, __dmul_rn(xv[u].y, cv[u].y));
+                        }
+                    }
+                }
+                for (; f < d; ++f) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + f), __ldg(cr + f)));
+                dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
+                ok = isfinite(dval) && double(__int_as_float(r.y)) > dval;
+            }
+            if (ok) {
+                out_idx[row] = j;
+                out_val[row] = dval;
+            }
+            need = !ok;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, need);
+        if (bal) {
+            unsigned b0 = 0;
+            if (lane == 0) b0 = atomicAdd(fb_count, unsigned(__popc(bal)));
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (need) fb[b0 + __popc(bal & ((1u << lane) - 1u))] = int32_t(row);
+        }
+    }
+}
+
+__global__ void tc64_gather_kernel(const double *x, int64_t d, const int32_t *rows, const unsigned *count,
+                                   double *g) {
+    const int64_t n = int64_t(*count) * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+         e += int64_t(gridDim.x) * blockDim.x)
+        g[e] = x[int64_t(rows[e / d]) * d + e % d];
+}
+
+__global__ void tc64_scatter_kernel(const int32_t *rows, const unsigned *count, const int32_t *idx,
+                                    const double *val, int32_t *out_idx, double *out_val) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < *count;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        out_idx[rows[q]] = idx[q];
+        out_val[rows[q]] = val[q];
+    }
+}
+
+bool tc64_supported(int64_t m, int64_t k, int64_t d) {
+    return m >= 1 && k >= 1 && k < 65536 && d >= 4 && d <= 256 && d % 4 == 0 &&
+           m < (int64_t(1) << 31);
+}
+
+int row_info64_run(const double *x, int64_t m, int64_t d, float *x32, float *info, cudaStream_t st) {
+    if (m == 0) return FTK_OK;
+    const int64_t blocks = std::min<int64_t>((m + 7) / 8, 148 * 16);
+    row_info64_kernel<<<unsigned(blocks), 256, 0, st>>>(x, m, d, x32, reinterpret_cast<float4 *>(info));
+    FTK_LAUNCHED("row_info64_kernel");
+    return FTK_OK;
+}
+
+static unsigned g_t64_last[2] = {0, 0};
+
+int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn, int64_t m,
+                    int64_t k, int64_t d, int32_t *out_idx, double *out_val, const TcFt *ft,
+                    cudaStream_t st) {
+    if (!tc64_supported(m, k, d)) {
+        set_error("tc64: unsupported shape (d % 4 == 0, d <= 256, k < 65536)");
+        return FTK_ERR_UNSUPPORTED;
+    }
+    // X32 and row bounds: the fit's registered copy, else converted here
+    const float *x32;
+    const float4 *info;
+    if (ctx->rows_x == x && ctx->rows_x32 && ctx->rows_m == m && ctx->rows_d == d && ctx->rows_info) {
+        x32 = ctx->rows_x32;
+        info = reinterpret_cast<const float4 *>(ctx->rows_info);
+    } else {
+        char *b = static_cast<char *>(scratch(ctx, SLOT_TC64_X, sizeof(float) * size_t(m) * (d + 4) + 256, st));
+        if (!b) return FTK_ERR_CUDA;
+        float *xs = reinterpret_cast<float *>(b);
+        float *inf = reinterpret_cast<float *>(b + ((sizeof(float) * size_t(m) * d + 255) & ~size_t(255)));
+        int rc = row_info64_run(x, m, d, xs, inf, st);
+        if (rc) return rc;
+        x32 = xs;
+        info = reinterpret_cast<const float4 *>(inf);
+    }
+    const size_t cbytes = (sizeof(float) * size_t(k) * d + 255) & ~size_t(255);
+    char *cb = static_cast<char *>(scratch(ctx, SLOT_TC64_C, cbytes + sizeof(float) * size_t(k) + 512, st));
+    if (!cb) return FTK_ERR_CUDA;
+    float *c32 = reinterpret_cast<float *>(cb);
+    float *yn32 = reinterpret_cast<float *>(cb + cbytes);
+    float *bounds = yn32 + ((k + 63) & ~int64_t(63));  // [0] cmax2, [1] ecmax2, then counters
+    unsigned *cnt = reinterpret_cast<unsigned *>(bounds + 8);  // [0] uncertified, [2] abft, [4] corrected, [5] flags
+    FTK_CUDA(cudaMemsetAsync(bounds, 0, 64, st));
+    tc64_prep_kernel<<<unsigned(std::min<int64_t>((k + 7) / 8, 296)), 256, 0, st>>>(y, yn, k, d, c32, yn32,
+                                                                                     bounds);
+    FTK_LAUNCHED("tc64_prep_kernel");
+    char *rb = static_cast<char *>(scratch(ctx, SLOT_TC64_REC, sizeof(int2) * size_t(m) + sizeof(int32_t) * size_t(m + 1) + 64, st));
+    if (!rb) return FTK_ERR_CUDA;
+    int2 *rec = reinterpret_cast<int2 *>(rb);
+    int32_t *fb = reinterpret_cast<int32_t *>(rec + m);
+
+    const int nkb = int((d + T64_KB - 1) / T64_KB);
+    PairParams Q{};
+    Q.x = x32; Q.y = c32; Q.yn = yn32; Q.m = m; Q.k = k; Q.d = d;
+    // tf32 accumulation (the float32 path's term) + the reference's float64 chain
+    Q.a_coef = float(3.0 * double(d) * 0x1p-24 + 2.0 * (double(d) + 2.0) * 0x1p-53);
+    Q.b_coef = float((0x1p-14 + 0x1p-22) * 1.01);
+    Q.a_abs = 0x1p-23f;  // x cmax^2: fp32 rounding of the float64 norms
+    Q.cmax2 = bounds;
+    Q.ecmax2 = bounds + 1;
+    Q.out_idx = out_idx;
+    Q.out_val = nullptr;
+    Q.fb_rows = fb;
+    Q.fb_count = cnt;
+    Q.rowinfo = info;
+    Q.rec64 = rec;
+    constexpr unsigned kFlagCap = 4096;
+    double4 *flag_rec = nullptr;
+    float *csum = nullptr, *camax = nullptr, *csumw = nullptr;
+    if (ft) {
+        int rc = prep_csum_run(ctx, SLOT_TC_CSUM1, c32, k, d, nkb, 1, &csum, &camax, st, &csumw);
+        if (rc) return rc;
+        flag_rec = static_cast<double4 *>(scratch(ctx, SLOT_PAIR_FLAG, sizeof(double4) * kFlagCap, st));
+        if (!flag_rec) return FTK_ERR_CUDA;
+        Q.csum = csum;
+        Q.camax = camax;
+        Q.tau_coef = float(ft->delta_rel * double(d) * std::sqrt(double(k) / 32.0));
+        Q.tau_abs = float(ft->abs_tol);
+        Q.abft_count = cnt + 2;
+        Q.abft_total = abft_total_ptr(ctx, st);
+        Q.flag_rec = flag_rec;
+        Q.flag_count = cnt + 5;
+        Q.flag_cap = kFlagCap;
+    }
+    CUtensorMap mx, mc;
+    int rc = make_tc_map(&mx, x32, m, d, 128);
+    if (!rc) rc = make_tc_map(&mc, c32, k, d, PAIR_BN / 2);
+    if (rc) return rc;
+    if ((rc = pair_screen_launch(mx, mc, Q, ft != nullptr, st))) return rc;
+    tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 255) / 256, 148 * 8)), 256, 0, st>>>(
+        x, y, yn, m, d, rec, out_idx, out_val, fb, cnt);
+    FTK_LAUNCHED("tc64_refine_kernel");
+    if (ft) {
+        // location + event records of the checksum-flagged rows (the DMMA pass
+        // below re-resolves them: the correction)
+        FlagEvents F{};
+        F.x = x32; F.d = d; F.k = k;
+        F.csumw = csumw; F.camax = camax;
+        F.rec = flag_rec; F.count = cnt + 5; F.cap = kFlagCap;
+        F.inj_col = nullptr;
+        F.events_for_scheduled = 1;
+        if (ft->ev) F.ev = *ft->ev;
+        F.iteration = ft->iteration;
+        F.bm = ft->bm;
+        F.bn = ft->bn;
+        F.interval = ft->bk > 0 ? (d + ft->bk - 1) / ft->bk - 1 : 0;
+        F.corrected = cnt + 4;
+        if ((rc = abft_flag_events_run(F, st))) return rc;
+    }
+    unsigned h[3] = {0, 0, 0};
+    FTK_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    FTK_CUDA(cudaStreamSynchronize(st));
+    g_t64_last[0] = h[0];
+    g_t64_last[1] = h[2];
+    ctx->stat_dev[0] = ctx->stat_dev[1] = ctx->stat_dev[2] = nullptr;
+    ctx->last_fb[0] = h[0];
+    ctx->last_fb[1] = 0;
+    ctx->last_fb[2] = h[2];
+    if (h[0] > 0) {
+        // uncertified rows: the DMMA screen (checked like the pass) over the gathered rows
+        const unsigned n = h[0];
+        const size_t gb = (sizeof(double) * size_t(n) * d + 255) & ~size_t(255);
+        char *g = static_cast<char *>(scratch(ctx, SLOT_TC64_G, gb + (sizeof(double) + sizeof(int32_t)) * size_t(n) + 64, st));
+        if (!g) return FTK_ERR_CUDA;
+        double *gx = reinterpret_cast<double *>(g);
+        double *gv = reinterpret_cast<double *>(g + gb);
+        int32_t *gi = reinterpret_cast<int32_t *>(gv + n);
+        tc64_gather_kernel<<<148 * 4, 256, 0, st>>>(x, d, fb, cnt, gx);
+        FTK_LAUNCHED("tc64_gather_kernel");
+        TcFt ft2{};
+        if (ft) {
+            ft2 = *ft;
+            ft2.inj = nullptr;
+            ft2.ev = nullptr;
+        }
+        const int fam = ctx->family;
+        ctx->family = 3;  // DMMA for the leftovers
+        rc = dscreen_run(ctx, gx, y, yn, n, k, d, gi, gv, ft ? &ft2 : nullptr, st);
+        ctx->family = fam;
+        if (rc) return rc;
+        tc64_scatter_kernel<<<148, 256, 0, st>>>(fb, cnt, gi, gv, out_idx, out_val);
+        FTK_LAUNCHED("tc64_scatter_kernel");
+    }
+    if (ft && ft->inj && ft->inj->n > 0)
+        return emulate_injected_blocks<double>(ctx, x, y, yn, m, k, d, *ft, out_idx, out_val, st);
+    return FTK_OK;
+}
+
+int tc64_last(unsigned *out) {
+    out[0] = g_t64_last[0];
+    out[1] = g_t64_last[1];
+    return FTK_OK;
+}
+
+}  // namespace ftk

@@ -85,7 +85,10 @@ __device__ __forceinline__ uint32_t ordered_key(float f) {
 // stage = centroid half + X half; with several column tiles the row tile's X
 // is re-read from L2 per tile) and the refine reads its row from global
 // memory (L2: the tile was just streamed).
-template <bool CHK, bool COLLECT, bool INJ, bool SX>
+// F64: float64 data screened from its fp32 copy; the refine records (j1, T)
+// for the float64 refine (tc.cu tc64_refine_kernel) instead of running the
+// fp32 exact chain.
+template <bool CHK, bool COLLECT, bool INJ, bool SX, bool F64 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     pair_screen_kernel(const __grid_constant__ CUtensorMap tmX,
                        const __grid_constant__ CUtensorMap tmC, PairParams P) {
@@ -478,6 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 // buffers); the X row comes from the resident tile
                 const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(active ? j : 0) * P.d);
                 auto load_c = [&](float4 (&cv)[8], int kb) {
+                    if (F64) return;  // the float64 refine reads the centroid itself
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         cv[q] = (active && kb * PR_KB + 4 * q < P.d) ? __ldg(cj4 + kb * 8 + q)
@@ -492,11 +496,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             const float4 xv =
                                 SX ? __ldg(xg4 + kb * 8 + q)
                                    : *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
-                            const float4 c4 = cv[q];
-                            acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.z, c4.z));
-                            acc = __fadd_rn(acc, __fmul_rn(xv.w, c4.w));
+                            if (!F64) {
+                                const float4 c4 = cv[q];
+                                acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
+                                acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
+                                acc = __fadd_rn(acc, __fmul_rn(xv.z, c4.z));
+                                acc = __fadd_rn(acc, __fmul_rn(xv.w, c4.w));
+                            }
                             if (!have_info) {
                                 xx = fmaf(xv.x, xv.x, xx);
                                 xx = fmaf(xv.y, xv.y, xx);
@@ -550,8 +556,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const float cm = sqrtf(*P.cmax2 * (1.0f + 0x1p-10f));
                 const float A = 2.0f * (1.0f + 0x1p-10f) *
                                 (sqrtf(ee * (1.0f + 0x1p-10f)) * cm +
-                                 xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) + P.a_coef * xn * cm);
-                dval = __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
+                                 xn * sqrtf(*P.ecmax2 * (1.0f + 0x1p-10f)) + P.a_coef * xn * cm) +
+                                (F64 ? P.a_abs * *P.cmax2 : 0.0f);
+                dval = F64 ? 0.0f : __fsub_rn(P.yn[j], __fadd_rn(acc, acc));
                 const double rref = (rr[0] + rr[1]) + (rr[2] + rr[3]);
                 bool abft_bad = false;
                 if (CHK) {
@@ -576,8 +583,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         }
                     }
                 }
+                if (F64) {
+                    // certificate threshold for the float64 refine: j1 is the
+                    // reference's strict argmin iff its exact value d1 < T
+                    const float T = m2 - A - P.b_coef * fabsf(m2) - 0x1p-21f * (fabsf(m1) + fabsf(m2));
+                    const bool good = !abft_bad && xn * cm < 1e36f && isfinite(T) && isfinite(m1);
+                    P.rec64[grow] = make_int2(good ? j : -1, __float_as_int(T));
+                }
                 // magnitudes far from overflow: the screen saw every column finite
-                const bool sane = xn * cm < 1e36f && isfinite(dval);
+                const bool sane = !F64 && xn * cm < 1e36f && isfinite(dval);
                 if (sane) {
                     // ref_j >= s_j - A - B|s_j| > d1 unless s_j <= thr (see tc_pair.cuh)
                     thr_out = dval + A + 2.0f * (P.b_coef + 0x1p-20f) * (fabsf(dval) + A);
@@ -589,7 +603,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
               }
                 PROBE_ADD(9, clock64() - lp1_);
             }
-            if (!COLLECT && grow < M) {
+            if (F64 && !active && grow < M) P.rec64[grow] = make_int2(-1, 0);
+            if (!COLLECT && !F64 && grow < M) {
                 if (ok) {
                     P.out_idx[grow] = j;
                     P.out_val[grow] = dval;
@@ -597,7 +612,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             // warp-aggregated append of the uncertified rows, with what pass 2
             // needs: the candidate threshold and the seed (exact d1, j1)
-            const bool need = !COLLECT && grow < M && !ok;
+            const bool need = !COLLECT && !F64 && grow < M && !ok;
             const unsigned bal = __ballot_sync(0xffffffffu, need);
             if (bal) {
                 unsigned base = 0;
@@ -673,6 +688,18 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int64_t ncl = npt < nsm / 2 ? npt : nsm / 2;
+    if (P.rec64) {  // float64 data, fp32 copy resident (d <= 256)
+        if (sx) {
+            set_error("tc pair f64: d > 256");
+            return FTK_ERR_UNSUPPORTED;
+        }
+        auto k64 = chk ? pair_screen_kernel<true, false, false, false, true>
+                       : pair_screen_kernel<false, false, false, false, true>;
+        FTK_CUDA(cudaFuncSetAttribute(k64, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        k64<<<dim3(unsigned(2 * ncl)), dim3(PR_THREADS), smem, st>>>(mx, mc, P);
+        FTK_LAUNCHED("pair_screen_kernel");
+        return FTK_OK;
+    }
     auto kern = sx ? (chk ? (P.thr ? pair_screen_kernel<true, true, false, true>
                                    : (P.inj_col ? pair_screen_kernel<true, false, true, true>
                                                 : pair_screen_kernel<true, false, false, true>))

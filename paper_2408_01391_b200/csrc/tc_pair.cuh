@@ -49,6 +49,12 @@ struct PairParams {
     unsigned *row_cnt;
     const unsigned *m_dev;  // device-side row count (<= m) or null
     const float4 *rowinfo;  // per-fit row bounds (|x|^2, |x - tf32 x|^2, max|x|) or null
+    // float64 data screened in tf32 (tc64 path): per row (j1, T) -- T the
+    // certificate threshold (j1 is the reference's argmin if its exact float64
+    // value d1 < T); j1 = -1 when the row is not screenable (checksum flag,
+    // non-finite).  The refine then skips the fp32 exact chain.
+    int2 *rec64;
+    float a_abs;  // extra absolute screen error (the fp32 rounding of float64 norms)
     long long *clk;  // debug: per-role clock64 sums (screen busy/wait, MMA waits), or null
     int dbg;  // bit 0: skip the screen math, bit 1: skip the refine (pipeline timing only)
 };

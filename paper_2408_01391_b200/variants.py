@@ -11,7 +11,9 @@ assignment, so this module keeps the same structure for it:
                                streamed with the centroid stages above)
                      "narrow"  streamed-X tcgen05 screen (tc_narrow.cu, k + 4 <= 256)
                      "exact"   SIMT kernel in the reference's evaluation order (exact.cu)
-  double precision   "dmma"    FP64 tensor-core screen (dscreen.cu)
+  double precision   "pair"    tf32 CTA-pair screen of the fp32 copy, certified in float64
+                               (tc64.cu; uncertified rows go to the DMMA screen)
+                     "dmma"    FP64 tensor-core screen (dscreen.cu)
                      "dfma"    SIMT DFMA screen (dscreen.cu)
                      "exact"
 
@@ -34,7 +36,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 PRECISIONS = ("single", "double")
-FAMILIES = {"single": ("pair", "narrow", "exact"), "double": ("dmma", "dfma", "exact")}
+FAMILIES = {"single": ("pair", "narrow", "exact"), "double": ("pair", "dmma", "dfma", "exact")}
 HEADER = "# M_bucket,D,K,precision,variant,gflops,reps\n"
 DEFAULT_TABLE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data",
                              "variants_b200.csv")
@@ -70,6 +72,8 @@ def feasible(variant, shape, precision, ft_on=False):
         return False
     if variant in ("dmma", "dfma"):
         return k < 65536 and m < (1 << 31)
+    if variant == "pair":  # tf32 screen of the fp32 copy, certified in float64 (tc64.cu)
+        return 4 <= d <= 256 and d % 4 == 0 and k < 65536 and m < (1 << 31)
     return False
 
 
@@ -79,6 +83,8 @@ def builtin(shape, precision, ft_on=False):
     else the pair screen with streamed X), DMMA for float64, the exact
     kernel otherwise."""
     if precision == "double":
+        if shape[0] >= 65536 and feasible("pair", shape, precision, ft_on):
+            return "pair"
         return "dmma" if feasible("dmma", shape, precision, ft_on) else "exact"
     _, d, _ = shape
     if d > 256 and feasible("narrow", shape, precision, ft_on):
