@@ -47,6 +47,8 @@ CONFIGS = {
     "c2": dict(rows=1_000_000, dim=128, k=1024, ft="abft",
                workload="c2: N=1e6 D=128 K=1024 fp32, ABFT on, per-tile-prob campaign sized for "
                         "~50 errors/s"),
+    "c4": dict(rows=10_000_000, dim=64, k=256, ft="abft",
+               workload="c4: N=1e7 D=64 K=256 fp64, ABFT on (FT-off interleaved for the overhead)"),
     "c5": dict(rows=100_000_000, dim=128, k=4096, ft="off",
                workload="c5: N=1e8 D=128 K=4096 fp32, FT off, rows sharded over the ranks"),
 }
@@ -169,7 +171,7 @@ def make_data(cfg, seed=0):
     return x
 
 
-def make_shard_dev(cfg, lo, hi, seed=0):
+def make_shard_dev(cfg, lo, hi, seed=0, dtype="float32"):
     """Rows [lo, hi) of a gaussian_mixture-shaped dataset generated on the
     device: the reference's centers (numpy default_rng(seed), rescaled to a
     minimum pairwise distance of 20 * spread, matrix.py:86-110), uniform
@@ -187,13 +189,13 @@ def make_shard_dev(cfg, lo, hi, seed=0):
         centers *= 20 * 0.25 / max(md, 1e-12)
     cen = torch.from_numpy(centers).cuda()
     g = torch.Generator(device="cuda").manual_seed(seed * 1_000_003 + lo)
-    x = torch.empty((hi - lo, d), dtype=torch.float32, device="cuda")
+    x = torch.empty((hi - lo, d), dtype=getattr(torch, dtype), device="cuda")
     ch = 1 << 22
     for r0 in range(0, hi - lo, ch):
         r1 = min(hi - lo, r0 + ch)
         lab = torch.randint(0, k, (r1 - r0,), generator=g, device="cuda")
         x[r0:r1] = (cen[lab] + 0.25 * torch.randn((r1 - r0, d), generator=g, device="cuda",
-                                                   dtype=torch.float64)).float()
+                                                   dtype=torch.float64)).to(x.dtype)
     # random-sample init (the first k rows of a seeded permutation of shard 0,
     # broadcast so every rank starts from the same centroids)
     return x, centers
@@ -541,6 +543,7 @@ def run_ours(args, rank, world):
         gc.collect()
         torch.cuda.empty_cache()
         c5 = c5_point(args)
+    c4 = c4_point(args) if world == 1 and args.c4 else None
     cpu = None
     if rank == 0 and world == 1:
         cpu = cpu_baseline_record(x, K, 3, "abft")
@@ -578,6 +581,7 @@ def run_ours(args, rank, world):
         "cpu_baseline": cpu,
         "e2e": e2e,
         "c5_1gpu": c5,
+        "c4_1gpu": c4,
     }
     print(json.dumps(line))
 
@@ -626,18 +630,79 @@ def c5_point(args):
             "data": "device-generated gaussian_mixture recipe (torch RNG), random-sample init"}
 
 
+def c4_point(args, reps=5, per=2):
+    """c4 (N=1e7, D=64, K=256 fp64, ABFT) on this GPU: an ABFT engine and an
+    FT-off engine from the same centroids, `per` steps each, interleaved
+    `reps` times (median ms per step of each), the overhead and the label
+    divergence between the two runs' final labels (fault-free ABFT is
+    bit-identical to FT off)."""
+    import torch
+
+    import paper_2408_01391_b200 as P
+    from paper_2408_01391_b200 import _engine as E
+    from paper_2408_01391_b200 import variants as V
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    cfg = CONFIGS["c4"]
+    x_t, _ = make_shard_dev(cfg, 0, cfg["rows"], dtype="float64")
+    c0 = x_t[:cfg["k"]].clone()
+    thr = P.Threshold.default_for(np.float64)
+    engs = {ft: LloydEngine(x_t, c0, cfg["k"], np.float64, P.default_config(np.float64), ft, thr, 64)
+            for ft in ("off", "abft")}
+    for eng in engs.values():  # warm-up: first iterations of a fit reshuffle many labels
+        for it in range(2):
+            eng.step(it)
+    times = {"off": [], "abft": []}
+    phase = {"off": [], "abft": []}
+    it = 2
+    for _ in range(reps):
+        for ft, eng in engs.items():
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for q in range(per):
+                eng.step(it + q)
+            s1.record()
+            torch.cuda.synchronize()
+            times[ft].append(s0.elapsed_time(s1) / per)
+            phase[ft].append((eng.assign_ms, eng.update_ms))
+        it += per
+    lab = {ft: E.to_host(eng.labels_view()) for ft, eng in engs.items()}
+    rep = engs["abft"].report
+    fb = E.tc_fallback_rows()
+    for eng in engs.values():
+        eng.close()
+    del engs, x_t
+    torch.cuda.empty_cache()
+    ms = {ft: float(np.median(v)) for ft, v in times.items()}
+    a_ms = float(np.median([p[0] for p in phase["abft"]]))
+    u_ms = float(np.median([p[1] for p in phase["abft"]]))
+    flops = 2.0 * cfg["rows"] * cfg["dim"] * cfg["k"]
+    return {"workload": cfg["workload"] + ", 1 GPU", "iter_per_s": 1e3 / ms["abft"],
+            "ms_per_step": ms["abft"], "ft_off_ms_per_step": ms["off"],
+            "ft_overhead_pct": 100.0 * (ms["abft"] / ms["off"] - 1.0),
+            "reps": reps, "steps_per_rep": per, "assign_ms": a_ms, "update_ms": u_ms,
+            "assign_tflops_f64_equiv": flops / (a_ms * 1e-3) / 1e12,
+            "variant": V.resolve((cfg["rows"], cfg["dim"], cfg["k"]), np.float64, True),
+            "uncertified_rows_last_pass": int(fb[0]),
+            "label_divergence": int((lab["off"] != lab["abft"]).sum()),
+            "detections": rep.detections, "false_alarms": rep.false_alarms,
+            "data": "device-generated gaussian_mixture recipe (torch RNG, float64), first-k-rows init"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="c2", choices=["c2", "c5"])
     ap.add_argument("--variant", default=None)
     ap.add_argument("--campaign-s", type=float, default=1.0,
                     help="seconds of ABFT iterations under ~50 injected errors/s (0: skip)")
     ap.add_argument("--reps", type=int, default=10, help="interleaved FT-off/on repetitions")
     ap.add_argument("--c5", type=int, default=1, help="also time c5 on one GPU (N=1 only)")
+    ap.add_argument("--c4", type=int, default=1, help="also time c4 (fp64) on one GPU (N=1 only)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))

@@ -48,28 +48,37 @@ constexpr int T64_KB = 32;
 // fp32 upper bound of a non-negative double
 __device__ __forceinline__ float up32(double v) { return __double2float_ru(v * (1.0 + 0x1p-40)); }
 
-// X32 = fp32(X) and the per-row screening bounds, one warp per row.
+// X32 = fp32(X) and the per-row screening bounds: one warp per group of 4
+// rows, all four rows' loads in flight together (HBM-bound, one pass).
 __global__ void row_info64_kernel(const double *x, int64_t m, int64_t d, float *x32, float4 *info) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t i = w0; i < m; i += nw) {
-        double xx = 0.0, ee = 0.0, am = 0.0;
+    for (int64_t i0 = w0 * 4; i0 < m; i0 += nw * 4) {
+        double xx[4] = {0.0, 0.0, 0.0, 0.0}, ee[4] = {0.0, 0.0, 0.0, 0.0}, am[4] = {0.0, 0.0, 0.0, 0.0};
         for (int64_t f = lane; f < d; f += 32) {
-            const double v = x[i * d + f];
-            const float v32 = __double2float_rn(v);
-            x32[i * d + f] = v32;
-            const double r = v - double(tf32_trunc(v32));
-            xx = fma(v, v, xx);
-            ee = fma(r, r, ee);
-            am = fmax(am, fabs(v));
+            double v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = i0 + u < m ? __ldcs(x + (i0 + u) * d + f) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float v32 = __double2float_rn(v[u]);
+                if (i0 + u < m) x32[(i0 + u) * d + f] = v32;
+                const double r = v[u] - double(tf32_trunc(v32));
+                xx[u] = fma(v[u], v[u], xx[u]);
+                ee[u] = fma(r, r, ee[u]);
+                am[u] = fmax(am[u], fabs(v[u]));
+            }
         }
-        for (int off = 16; off; off >>= 1) {
-            xx += __shfl_xor_sync(0xffffffffu, xx, off);
-            ee += __shfl_xor_sync(0xffffffffu, ee, off);
-            am = fmax(am, __shfl_xor_sync(0xffffffffu, am, off));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            for (int off = 16; off; off >>= 1) {
+                xx[u] += __shfl_xor_sync(0xffffffffu, xx[u], off);
+                ee[u] += __shfl_xor_sync(0xffffffffu, ee[u], off);
+                am[u] = fmax(am[u], __shfl_xor_sync(0xffffffffu, am[u], off));
+            }
+            if (lane == u && i0 + u < m) info[i0 + u] = make_float4(up32(xx[u]), up32(ee[u]), up32(am[u]), 0.0f);
         }
-        if (lane == 0) info[i] = make_float4(up32(xx), up32(ee), up32(am), 0.0f);
     }
 }
 
@@ -103,44 +112,59 @@ __global__ void tc64_prep_kernel(const double *y, const double *yn, int64_t k, i
 }
 
 // Certify each screened row in float64: the reference's chain for the
-// winner, d1 < T.  Uncertified rows are appended (warp-aggregated) to fb.
-__global__ void tc64_refine_kernel(const double *x, const double *y, const double *yn, int64_t m,
-                                   int64_t d, const int2 *rec, int32_t *out_idx, double *out_val,
-                                   int32_t *fb, unsigned *fb_count) {
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t base = int64_t(blockIdx.x) * blockDim.x; base < m; base += stride) {
-        const int64_t row = base + threadIdx.x;
+// winner, d1 < T.  One warp per 32-row tile, one lane per row; X streams in
+// 32-feature chunks: 16-byte coalesced loads (two rows per instruction) are
+// transposed through shared memory so each lane runs its row's sequential
+// chain, with its winner's centroid chunk (L2-resident) loaded alongside.
+// Uncertified rows are appended (warp-aggregated) to fb.
+constexpr int R64_WARPS = 4, R64_LD = 34;  // row stride in doubles (16-byte aligned rows)
+__global__ void __launch_bounds__(32 * R64_WARPS) tc64_refine_kernel(
+    const double *x, const double *y, const double *yn, int64_t m, int64_t d, const int2 *rec,
+    int32_t *out_idx, double *out_val, int32_t *fb, unsigned *fb_count) {
+    __shared__ __align__(16) double sx[R64_WARPS][32 * R64_LD];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *s = sx[w];
+    const int64_t ntile = (m + 31) / 32;
+    for (int64_t tile = int64_t(blockIdx.x) * R64_WARPS + w; tile < ntile;
+         tile += int64_t(gridDim.x) * R64_WARPS) {
+        const int64_t r0 = tile * 32, row = r0 + lane;
+        const int2 r = row < m ? rec[row] : make_int2(-1, 0);
+        const int j = r.x;
+        const double *cr = y + int64_t(j < 0 ? 0 : j) * d;
+        double acc = 0.0;
+        const int half = lane >> 4, q = lane & 15;  // x loads: row 2i + half, features 2q, 2q+1
+        for (int64_t f0 = 0; f0 < d; f0 += 32) {
+            const int fw = int(d - f0 < 32 ? d - f0 : 32);
+            double2 xv[16], cv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int64_t rr = r0 + 2 * i + half;
+                xv[i] = (rr < m && 2 * q < fw) ? __ldcs(reinterpret_cast<const double2 *>(x + rr * d + f0) + q)
+                                               : make_double2(0.0, 0.0);
+                cv[i] = (j >= 0 && 2 * i < fw) ? __ldg(reinterpret_cast<const double2 *>(cr + f0) + i)
+                                               : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i)
+                *reinterpret_cast<double2 *>(s + (2 * i + half) * R64_LD + 2 * q) = xv[i];
+            __syncwarp();
+            const double *sr = s + lane * R64_LD;
+            if (fw == 32) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    acc = __dadd_rn(acc, __dmul_rn(sr[2 * i], cv[i].x));
+                    acc = __dadd_rn(acc, __dmul_rn(sr[2 * i + 1], cv[i].y));
+                }
+            } else {
+                for (int f = 0; f < fw; ++f) acc = __dadd_rn(acc, __dmul_rn(sr[f], __ldg(cr + f0 + f)));
+            }
+            __syncwarp();  // the tile buffer is refilled by the next chunk
+        }
         bool need = false;
         if (row < m) {
-            const int2 r = rec[row];
-            const int j = r.x;
             bool ok = false;
             double dval = 0.0;
             if (j >= 0) {
-                const double *xr = x + row * d;
-                const double *cr = y + int64_t(j) * d;
-                double acc = 0.0;
-                int64_t f = 0;
-                if ((d & 1) == 0) {
-                    const double2 *x2 = reinterpret_cast<const double2 *>(xr);
-                    const double2 *c2 = reinterpret_cast<const double2 *>(cr);
-                    // 16 features per step: one 128-byte line of the row in flight at once
-                    for (; f + 16 <= d; f += 16) {
-                        double2 xv[8], cv[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            xv[u] = __ldcs(x2 + f / 2 + u);  // streamed once
-                            cv[u] = __ldg(c2 + f / 2 + u);
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            acc = __dadd_rn(acc, __dmul_rn(xv[u].x, cv[u].x));
-                            acc = __dadd_rn(acc, __dmul_rn(xv[u].y, cv[u].y));
-                        }
-                    }
-                }
-                for (; f < d; ++f) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + f), __ldg(cr + f)));
                 dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
                 ok = isfinite(dval) && double(__int_as_float(r.y)) > dval;
             }
@@ -184,7 +208,7 @@ bool tc64_supported(int64_t m, int64_t k, int64_t d) {
 
 int row_info64_run(const double *x, int64_t m, int64_t d, float *x32, float *info, cudaStream_t st) {
     if (m == 0) return FTK_OK;
-    const int64_t blocks = std::min<int64_t>((m + 7) / 8, 148 * 16);
+    const int64_t blocks = std::min<int64_t>((m + 31) / 32, 148 * 8);
     row_info64_kernel<<<unsigned(blocks), 256, 0, st>>>(x, m, d, x32, reinterpret_cast<float4 *>(info));
     FTK_LAUNCHED("row_info64_kernel");
     return FTK_OK;
@@ -269,7 +293,8 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     if (!rc) rc = make_tc_map(&mc, c32, k, d, PAIR_BN / 2);
     if (rc) return rc;
     if ((rc = pair_screen_launch(mx, mc, Q, ft != nullptr, st))) return rc;
-    tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 255) / 256, 148 * 8)), 256, 0, st>>>(
+    tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 32 * R64_WARPS - 1) / (32 * R64_WARPS), 148 * 6)),
+                         32 * R64_WARPS, 0, st>>>(
         x, y, yn, m, d, rec, out_idx, out_val, fb, cnt);
     FTK_LAUNCHED("tc64_refine_kernel");
     if (ft) {

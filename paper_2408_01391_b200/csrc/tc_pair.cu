@@ -53,6 +53,7 @@ constexpr int PR_BN = PAIR_BN;      // centroids per N tile (half per CTA)
 constexpr int PR_NBUF = 512 / PR_BN;  // TMEM accumulator buffers
 constexpr int PR_KB = 32;           // fp32 elements per 128-byte swizzle row
 constexpr int PR_MAX_KB = 8;        // k-blocks of the widest X row (d <= 256)
+constexpr int PR_MAX_NA = 4;        // X half-tile buffers (4 when few centroid k-blocks per row tile)
 constexpr int PR_THREADS = 480;     // 15 warps
 // Warp roles.  The SMSP arbiter favours the highest warp id, so the
 // latency-critical single-thread roles (MMA issue, TMA producers) take the
@@ -105,14 +106,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     float4 *css = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // ABFT checksum centroid [nkb * 8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
     uint64_t *full = bars, *empty = bars + S;
-    uint64_t *a_full = bars + 2 * S, *a_empty = a_full + 2;
-    uint64_t *t_full = a_full + 4, *t_empty = t_full + PR_NBUF;
+    uint64_t *a_full = bars + 2 * S, *a_empty = a_full + PR_MAX_NA;
+    uint64_t *t_full = a_full + 2 * PR_MAX_NA, *t_empty = t_full + PR_NBUF;
     uint64_t *p_full = t_empty + PR_NBUF, *p_empty = p_full + 2;
     // X k-block release, per buffer: the refine warps free each k-block of a
     // row tile's X half as soon as they have consumed it, so the next X half
     // streams in behind the refine instead of after it
-    uint64_t *a_kbe = p_empty + 2;  // [2][PR_MAX_KB]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_kbe + 2 * PR_MAX_KB);
+    uint64_t *a_kbe = p_empty + 2;  // [PR_MAX_NA][PR_MAX_KB]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(a_kbe + PR_MAX_NA * PR_MAX_KB);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -132,10 +133,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < PR_MAX_NA; ++a) {
             mbar_init(&a_full[a], rank == 0 ? 2 : 1);  // leader: own TMA + peer's forward
             mbar_init(&a_empty[a], 4);  // refine warps, done with the X half
             for (int kb = 0; kb < PR_MAX_KB; ++kb) mbar_init(&a_kbe[a * PR_MAX_KB + kb], 4);
+        }
+        for (int a = 0; a < 2; ++a) {
             mbar_init(&p_full[a], 8);
             mbar_init(&p_empty[a], 4);
         }
@@ -652,15 +655,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 size_t pair_smem_bytes(int nkb, int abufs, int stages, bool sx) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * (sx ? PR_B_HALF + PR_A_KB : PR_B_HALF) +
            2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 2 * PR_BN * sizeof(float) +
-           8 * 8 * sizeof(float4) + (2 * size_t(stages) + 8 + 2 * PR_NBUF + 2 * PR_MAX_KB) * 8 + 64;
+           8 * 8 * sizeof(float4) +
+           (2 * size_t(stages) + 2 * PR_MAX_NA + 4 + 2 * PR_NBUF + PR_MAX_NA * PR_MAX_KB) * 8 + 64;
 }
 
-int pair_plan(int64_t d, int *abufs, int *stages) {
+int pair_plan(int64_t d, int64_t k, int *abufs, int *stages) {
     const int nkb = int((d + PR_KB - 1) / PR_KB);
     const bool sx = nkb > PR_MAX_KB;  // X streamed through the stages
     const size_t cap = 227 * 1024;
     int na = sx ? 0 : 2;
     if (!sx && pair_smem_bytes(nkb, 2, 3, false) > cap) na = 1;
+    // few centroid k-blocks per row tile (small k and d): a row tile's MMAs are
+    // short, so the X half-tiles are the stream to keep in flight -- up to four
+    // X buffers, as long as four centroid stages remain
+    const int64_t kblocks = int64_t(nkb) * ((k + PR_BN - 1) / PR_BN);
+    if (!sx && kblocks <= 4 && !getenv("FTK_PAIR_NA2"))
+        for (int cand = PR_MAX_NA; cand > na; --cand)
+            if (pair_smem_bytes(nkb, cand, 4, false) <= cap) {
+                na = cand;
+                break;
+            }
     int s = 12;
     while (s >= 2 && pair_smem_bytes(nkb, na, s, sx) > cap) --s;
     if (s < 2) return -1;
@@ -671,7 +685,7 @@ int pair_plan(int64_t d, int *abufs, int *stages) {
 
 int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams P, bool chk,
                        cudaStream_t st) {
-    if (pair_plan(P.d, &P.abufs, &P.stages)) {
+    if (pair_plan(P.d, P.k, &P.abufs, &P.stages)) {
         set_error("tc pair: tile exceeds shared memory");
         return FTK_ERR_UNSUPPORTED;
     }

@@ -382,7 +382,6 @@ class LloydEngine:
         # scheduled flips, DMR, update-site hooks or multi-GPU.
         # (only the fp32 CTA-pair assignment is free of host synchronisation)
         self.use_graph = bool(graph) and (dist is None or dist.capturable) and \
-            ft_mode != "abft+dmr" and \
             update_hook is NOOP_HOOK and self.dtype == np.float32 and \
             _graphable_shape(x_t.shape[1], k) and self.A.variant in ("pair", "narrow", "tc")
         self.graphs = [None, None]
@@ -454,7 +453,10 @@ class LloydEngine:
             E.sq_dists_dev(A.md, self.xsq, self.sq)
             E.pairwise_sum_dev(self.sq, self.ctl_f64[0:1])
             E.labels_equal_dev(A.labels[self.slot], A.labels[1 - self.slot], self.ctl_i32[0:1])
-        sa, ca, _, _ = E.update_sums_dev(self.x_t, A.labels[self.slot], self.k, dmr=False)
+        dmr = self.ft_mode == "abft+dmr"
+        sa, ca, sb, cb = E.update_sums_dev(self.x_t, A.labels[self.slot], self.k, dmr=dmr)
+        if dmr:  # duplicated accumulators compared on the device; the host reads the flag
+            E.dmr_mismatch_dev(sa, ca, sb, cb, self.ctl_i32[2:3])
         if self.dist is not None:
             # row shards: ONE packed all-reduce of the partial sums, counts,
             # inertia and changed-label count (NCCL, captured in the graph)
@@ -634,6 +636,8 @@ class LloydEngine:
         if rep is not None:
             self.report.merge(rep)
         new_cent = self.cent_buf[1 - self.cbuf]
+        if self.ft_mode == "abft+dmr" and self._dmr_flagged():
+            self._dmr_retry(it, new_cent)
         if int(self.ctl_i32_host[1]):
             old = self.cent
             if self._ahead is not None:
@@ -653,6 +657,34 @@ class LloydEngine:
         self.cent = self.cent_buf[self.cbuf]
         self.slot = 1 - self.slot
         return max(0.0, float(self.ctl_host[0])), unchanged, float(self.ctl_host[1])
+
+    def _dmr_flagged(self):
+        """The graph step's device DMR compare flag (read after the step)."""
+        return bool(int(self.ctl_i32_host[2]))
+
+    def _dmr_retry(self, it, new_cent):
+        """A graph step's duplicated update disagreed (kmeans.py:176-189):
+        record the mismatch, drop the replay queued on its centroids, and
+        redo this iteration's update eagerly -- recomputed sums that disagree
+        again raise FaultEscalationError."""
+        t = self.t
+        if self._ahead is not None:
+            # the queued replay overwrote this step's input centroids: restore them
+            t.cuda.current_stream().synchronize()
+            self._ahead = None
+            self.cent.copy_(self._cent_prev)
+        self.report.events.append(DetectionEvent(iteration=it, tile=(0, 0), kind="dmr-mismatch",
+                                                 loc=(-1, -1), delta=0.0))
+        sa, ca, sb, cb = E.update_sums_dev(self.x_t, self.A.labels[self.slot], self.k, dmr=True)
+        E.dmr_mismatch_dev(sa, ca, sb, cb, self.ctl_i32[2:3])
+        if int(self.ctl_i32[2].item()):
+            raise FaultEscalationError(
+                f"update-phase DMR mismatch persisted after retry (iteration {it})")
+        E.finalize_dev(sa, ca, self.dtype, out=new_cent, n_empty=self.ctl_i32[1:2])
+        self.counts_buf.copy_(ca)
+        E.movement_dev(new_cent, self.cent, self.eps, self.ctl_f64[1:2])
+        self.ctl_host[1:2].copy_(self.ctl_f64[1:2])
+        self.ctl_i32_host[1:2].copy_(self.ctl_i32[1:2])
 
     def step(self, it, eager=False, more=None):
         """One Lloyd iteration; returns (inertia, unchanged, moved), and the

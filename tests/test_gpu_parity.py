@@ -14,6 +14,7 @@ import oracle as O
 pytestmark = pytest.mark.gpu
 
 P = pytest.importorskip("paper_2408_01391_b200")
+from paper_2408_01391_b200 import _engine as E  # noqa: E402
 from paper_2408_01391_b200 import gemm as G  # noqa: E402
 from paper_2408_01391_b200.faults import FaultEntry, FaultSchedule, ScheduledFaultHook  # noqa: E402
 from paper_2408_01391_b200.tiles import MICRO_SINGLE, make_config  # noqa: E402
@@ -274,6 +275,39 @@ def test_dmr_update_golden(golden):
         assert got.tobytes() == z[f"t{t}_got"].tobytes() == z[f"t{t}_clean"].tobytes()
         off, _, _ = P.update_step(x, lab, 5, hook=_hook([(0, (0, 0), (ci, cj), bit)]))
         assert off.tobytes() == z[f"t{t}_off"].tobytes()
+
+
+def test_dmr_graph_steps_match_and_retry():
+    """abft+dmr runs in the CUDA-graph steps (duplicated accumulators compared
+    on the device): same results as abft, and a flagged step redoes its update
+    eagerly (kmeans.py:176-189) without changing the outcome."""
+    from paper_2408_01391_b200.kmeans import LloydEngine
+
+    x, _, _ = P.gaussian_mixture(60000, 32, 16, 0.25, precision="single", seed=8)
+    cfg = dict(k=16, seed=1, max_iters=12, init="random-sample")
+    base = P.lloyd(x, P.KMeansConfig(ft_mode="abft", **cfg))
+    dmr = P.lloyd(x, P.KMeansConfig(ft_mode="abft+dmr", **cfg))
+    assert np.array_equal(base.assignments, dmr.assignments)
+    assert base.centroids.tobytes() == dmr.centroids.tobytes()
+    assert base.inertia_history == dmr.inertia_history
+    assert dmr.report.dmr_mismatches == 0
+    c0 = P.init_centroids(x, 16, seed=1, method="random-sample")
+    thr = P.Threshold.default_for(np.float32)
+    runs = []
+    for flag_at in (None, 3):
+        eng = LloydEngine(E.to_dev(x), c0, 16, np.float32, P.default_config(np.float32), "abft+dmr",
+                          thr, 1, graph=True)
+        assert eng.use_graph
+        hist = []
+        for it in range(6):
+            if it == flag_at:
+                eng._dmr_flagged = lambda: True
+            hist.append(eng.step(it, more=lambda: True))
+            eng.__dict__.pop("_dmr_flagged", None)
+        runs.append((hist, E.to_host(eng.cent).tobytes(), eng.report))
+        eng.close()
+    assert runs[0][0] == runs[1][0] and runs[0][1] == runs[1][1]
+    assert runs[1][2].dmr_mismatches == 1 and runs[0][2].dmr_mismatches == 0
 
 
 def test_dmr_persistent_escalates():

@@ -17,6 +17,8 @@ ap.add_argument("--out", default=os.path.join("paper_2408_01391_b200", "data", "
 ap.add_argument("--probe", type=int, default=1 << 18)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--quick", action="store_true")
+ap.add_argument("--only", choices=["single", "double"], default=None,
+                help="re-measure one precision and keep the other's rows of --out")
 a = ap.parse_args()
 
 from paper_2408_01391_b200 import variants as V  # noqa: E402
@@ -37,8 +39,14 @@ def show(shape, var, gf):
     print(f"{shape} {var:7s} {gf:9.1f} GFLOP/s  [{time.time() - t0:.0f} s]", flush=True)
 
 
-ts = V.select(single, "single", reps=a.reps, probe_m=a.probe, progress=show)
-td = V.select(double, "double", reps=a.reps, probe_m=a.probe, progress=show)
+keep = V.VariantTable.load(a.out) if a.only and os.path.exists(a.out) else V.VariantTable()
+ts = V.select(single, "single", reps=a.reps, probe_m=a.probe, progress=show) \
+    if a.only != "double" else V.VariantTable()
+td = V.select(double, "double", reps=a.reps, probe_m=a.probe, progress=show) \
+    if a.only != "single" else V.VariantTable()
+for key, e in keep.entries.items():
+    if key[3] != a.only:
+        ts.entries[key] = e
 ts.entries.update(td.entries)
 os.makedirs(os.path.dirname(a.out), exist_ok=True)
 ts.save(a.out)
