@@ -281,6 +281,15 @@ def test_dmr_graph_steps_match_and_retry():
     """abft+dmr runs in the CUDA-graph steps (duplicated accumulators compared
     on the device): same results as abft, and a flagged step redoes its update
     eagerly (kmeans.py:176-189) without changing the outcome."""
+    old = G.get_variant()
+    G.set_variant("pair")  # a graph-step family (the variant table may pick exact here)
+    try:
+        _dmr_graph_case()
+    finally:
+        G.set_variant(old)
+
+
+def _dmr_graph_case():
     from paper_2408_01391_b200.kmeans import LloydEngine
 
     x, _, _ = P.gaussian_mixture(60000, 32, 16, 0.25, precision="single", seed=8)
