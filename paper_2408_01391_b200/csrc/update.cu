@@ -451,7 +451,6 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
 #define FTK_CS_NG 8
 #endif
 constexpr int CS_GS = 16, CS_NG = FTK_CS_NG, CS_LOADERS = FTK_CS_LOADERS;
-constexpr size_t CS_SMEM = 256 + size_t(CS_NG) * CS_GS * 512;
 
 __device__ __forceinline__ void cs_cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -480,21 +479,24 @@ __device__ __forceinline__ void cs_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-template <typename T, bool DMR>
+// SLAB: bytes of a member row per CTA (512, 256 or 128; FTK_CS_SLAB): narrower
+// slabs split a cluster's features over more CTAs.
+template <typename T, bool DMR, int SLAB>
 __global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
     const T *x, int64_t d, int64_t nslab, const int32_t *perm, const int64_t *offsets, double *sums_a,
     double *sums_b) {
     constexpr int VEC = 16 / sizeof(T);
-    constexpr int W = 32 * VEC;  // features per slab (512 bytes)
+    constexpr int LPR = SLAB / 16;        // lanes per row (16 bytes each)
+    constexpr int RPI = 32 / LPR;         // rows per copy instruction
+    constexpr int W = SLAB / sizeof(T);   // features per slab
     extern __shared__ __align__(128) unsigned char cs_smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(cs_smem);
     uint64_t *empty = full + CS_NG;
-    unsigned char *ring = cs_smem + 256;  // [CS_NG][CS_GS][512 bytes]
+    unsigned char *ring = cs_smem + 256;  // [CS_NG][CS_GS][SLAB bytes]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c = int64_t(blockIdx.x) / nslab, s = int64_t(blockIdx.x) % nslab;
     const int64_t f0 = s * W;
     const int fw = int(d - f0 < W ? d - f0 : W);  // a multiple of VEC
-    const bool live = lane * VEC < fw;
     const int64_t lo = offsets[c], n = offsets[c + 1] - lo;
     const int64_t ngrp = (n + CS_GS - 1) / CS_GS;
     if (threadIdx.x == 0) {
@@ -507,8 +509,10 @@ __global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
     __syncthreads();
     if (warp > 0) {
         // ------------------------------------------------ loaders --
-        const T *xs = x + f0 + lane * VEC;
-        const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring)) + lane * 16;
+        const int ri = lane / LPR, ch = lane % LPR;  // row within the instruction, 16-byte chunk
+        const bool live = ch * VEC < fw;
+        const T *xs = x + f0 + ch * VEC;
+        const uint32_t rbase = static_cast<uint32_t>(__cvta_generic_to_shared(ring)) + ri * SLAB + ch * 16;
         int64_t g = warp - 1;
         int32_t rows = (g < ngrp && lane < CS_GS && g * CS_GS + lane < n) ? __ldg(perm + lo + g * CS_GS + lane) : 0;
         for (; g < ngrp; g += CS_LOADERS) {
@@ -518,17 +522,17 @@ __global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
                                      ? __ldg(perm + lo + gn * CS_GS + lane) : 0;
             cs_wait(&empty[slot], (uint32_t(g / CS_NG) & 1u) ^ 1u);
             const int cnt = int(n - g * CS_GS < CS_GS ? n - g * CS_GS : CS_GS);
-            const uint32_t dst = rbase + uint32_t(slot) * (CS_GS * 512);
+            const uint32_t dst = rbase + uint32_t(slot) * (CS_GS * SLAB);
             if (cnt == CS_GS) {
 #pragma unroll
-                for (int u = 0; u < CS_GS; ++u) {
-                    const int32_t row = __shfl_sync(0xffffffffu, rows, u);
-                    if (live) cs_cp16(dst + u * 512, xs + int64_t(row) * d);
+                for (int u = 0; u < CS_GS; u += RPI) {
+                    const int32_t row = __shfl_sync(0xffffffffu, rows, u + ri);
+                    if (live) cs_cp16(dst + u * SLAB, xs + int64_t(row) * d);
                 }
             } else {
-                for (int u = 0; u < cnt; ++u) {
-                    const int32_t row = __shfl_sync(0xffffffffu, rows, u);
-                    if (live) cs_cp16(dst + u * 512, xs + int64_t(row) * d);
+                for (int u = 0; u < cnt; u += RPI) {
+                    const int32_t row = __shfl_sync(0xffffffffu, rows, (u + ri) & 31);
+                    if (live && u + ri < cnt) cs_cp16(dst + u * SLAB, xs + int64_t(row) * d);
                 }
             }
             cs_cp_arrive(&full[slot]);
@@ -539,6 +543,7 @@ __global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
         double acc_a[VEC], acc_b[VEC];
 #pragma unroll
         for (int v = 0; v < VEC; ++v) acc_a[v] = acc_b[v] = 0.0;
+        const bool live = lane < LPR && lane * VEC < fw;
         const T *base = reinterpret_cast<const T *>(ring) + lane * VEC;
         for (int64_t g = 0; g < ngrp; ++g) {
             const int slot = int(g % CS_NG);
@@ -573,6 +578,28 @@ __global__ void __launch_bounds__(32 * (1 + CS_LOADERS)) chain_spec_kernel(
             }
         }
     }
+}
+
+template <typename T, bool DMR>
+static int chain_spec_launch(const T *x, int64_t d, int64_t k, const int32_t *perm, const int64_t *offsets,
+                             double *sums_a, double *sums_b, cudaStream_t st) {
+    // 512-byte slabs: narrower ones (more CTAs per cluster) measured no faster
+    // at c4 (2.2 / 2.2 / 2.4 ms for 512 / 256 / 128): the chains are bound by
+    // the random-row gather rate (~2.4 TB/s), not by one SM's share
+    int slab = 512;
+    const int64_t row_bytes = d * int64_t(sizeof(T));
+    if (const char *e = getenv("FTK_CS_SLAB")) {
+        const int v = atoi(e);
+        if (v == 128 || v == 256 || v == 512) slab = v;
+    }
+    const int64_t nslab = (row_bytes + slab - 1) / slab;
+    const size_t smem = 256 + size_t(CS_NG) * CS_GS * slab;
+    auto kern = slab == 512 ? chain_spec_kernel<T, DMR, 512>
+                            : (slab == 256 ? chain_spec_kernel<T, DMR, 256> : chain_spec_kernel<T, DMR, 128>);
+    FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<unsigned(k * nslab), 32 * (1 + CS_LOADERS), smem, st>>>(x, d, nslab, perm, offsets, sums_a, sums_b);
+    FTK_LAUNCHED("chain_spec_kernel");
+    return FTK_OK;
 }
 
 // ------------------------------------------------ certified segmented sums --
@@ -1309,22 +1336,16 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     const int vec = dtype == FTK_F32 ? 4 : 2;
     if (pipe_chains && d % vec == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
         !(getenv("FTK_UPD_CHAIN") && atoi(getenv("FTK_UPD_CHAIN")) == 0)) {
-        // ordered chains, 16-byte copies of 512-byte row slabs
-        const int64_t nslab = (d + 32 * vec - 1) / (32 * vec);
-        const unsigned g = unsigned(k * nslab);
-        if (dtype == FTK_F32) {
-            auto xx = static_cast<const float *>(x);
-            auto kern = dmr ? chain_spec_kernel<float, true> : chain_spec_kernel<float, false>;
-            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CS_SMEM)));
-            kern<<<g, 32 * (1 + CS_LOADERS), CS_SMEM, st>>>(xx, d, nslab, vals_out, offsets, sums_a, dmr ? sums_b : nullptr);
-        } else {
-            auto xx = static_cast<const double *>(x);
-            auto kern = dmr ? chain_spec_kernel<double, true> : chain_spec_kernel<double, false>;
-            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(CS_SMEM)));
-            kern<<<g, 32 * (1 + CS_LOADERS), CS_SMEM, st>>>(xx, d, nslab, vals_out, offsets, sums_a, dmr ? sums_b : nullptr);
-        }
-        FTK_LAUNCHED("chain_spec_kernel");
-        return FTK_OK;
+        // ordered chains: warp-specialised gathers of row slabs
+        if (dtype == FTK_F32)
+            return dmr ? chain_spec_launch<float, true>(static_cast<const float *>(x), d, k, vals_out, offsets,
+                                                        sums_a, sums_b, st)
+                       : chain_spec_launch<float, false>(static_cast<const float *>(x), d, k, vals_out, offsets,
+                                                         sums_a, nullptr, st);
+        return dmr ? chain_spec_launch<double, true>(static_cast<const double *>(x), d, k, vals_out, offsets,
+                                                     sums_a, sums_b, st)
+                   : chain_spec_launch<double, false>(static_cast<const double *>(x), d, k, vals_out, offsets,
+                                                      sums_a, nullptr, st);
     }
     if (pipe_chains) {
         // few long chains: the reference's ordered chain, latency-hidden

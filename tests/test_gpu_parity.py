@@ -396,15 +396,18 @@ def test_update_paths_bit_exact(m, d, k, dt, tiny):
 
 
 @pytest.mark.parametrize("m,d,k,dt,env", [
-    (50000, 64, 37, np.float64, {}),                          # bulk-copy chains, one 512-byte slab
+    (50000, 64, 37, np.float64, {}),                          # warp-specialised chains, one 512-byte slab
     (40000, 130, 5, np.float64, {}),                          # partial last slab (2 features)
     (30000, 7, 5, np.float64, {}),                            # rows not 16-byte aligned: cp.async chains
     (40000, 64, 37, np.float64, {"FTK_UPD_CHAIN": "0"}),      # cp.async chains forced
-    (40000, 200, 9, np.float32, {"FTK_UPD_PATH": "pipe"}),    # float32 data through the bulk chains
+    (40000, 200, 9, np.float32, {"FTK_UPD_PATH": "pipe"}),    # float32 data through the ordered chains
+    (40000, 100, 9, np.float64, {"FTK_CS_SLAB": "128"}),      # 128-byte slabs, partial last slab
+    (40000, 72, 9, np.float64, {"FTK_CS_SLAB": "256"}),       # 256-byte slabs
+    (30000, 36, 5, np.float32, {"FTK_UPD_PATH": "pipe", "FTK_CS_SLAB": "128"}),
 ])
 @pytest.mark.parametrize("dmr", [False, True])
 def test_ordered_chain_kernels_bit_exact(m, d, k, dt, env, dmr, monkeypatch):
-    """The ordered float64 chains (bulk-copy and cp.async kernels, with and
+    """The ordered float64 chains (warp-specialised and cp.async kernels, with and
     without the DMR duplicate) equal numpy.bincount's sums bit for bit."""
     for key, val in env.items():
         monkeypatch.setenv(key, val)
