@@ -1112,6 +1112,7 @@ int tc_assign_run(ftk_ctx *ctx, int dtype, const void *x, const void *y, const v
             Q.out_idx = out_idx; Q.out_val = outv; Q.fb_rows = rows1; Q.fb_count = cnt;
             Q.csum = P.csum; Q.camax = P.camax; Q.tau_coef = P.tau_coef; Q.tau_abs = P.tau_abs;
             Q.inj_col = P.inj_col; Q.inj_before = P.inj_before; Q.inj_after = P.inj_after;
+            Q.hint = (ctx->hint && ctx->hint_m == m && !getenv("FTK_PAIR_NOHINT")) ? ctx->hint : nullptr;
             Q.abft_count = P.abft_count;
             Q.abft_total = P.abft_total;
             if (ft) {

@@ -102,8 +102,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     unsigned char *sB = sA + size_t(NA) * A_BYTES;
     PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * STG);  // [2][2][128]
     double2 *psum = reinterpret_cast<double2 *>(part + 2 * 2 * PR_BM);         // [2][2][128] (sum, weighted)
-    float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);              // [2][PR_BN]
-    float4 *css = reinterpret_cast<float4 *>(yns + 2 * PR_BN);  // ABFT checksum centroid [nkb * 8]
+    float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);  // [8 screen warps][2][PR_BN / 2]
+    float4 *css = reinterpret_cast<float4 *>(yns + 8 * PR_BN);      // ABFT checksum centroid [nkb * 8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
     uint64_t *full = bars, *empty = bars + S;
     uint64_t *a_full = bars + 2 * S, *a_empty = a_full + PR_MAX_NA;
@@ -253,12 +253,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         constexpr int HALF = PR_BN / 2;
         uint32_t g = 0;
         int it = 0;
-        // centroid norms of the current tile, staged in shared memory one
-        // tile ahead by the 256 screen threads (named barrier 1)
+        // centroid norms of the current tile, staged one tile ahead
+#ifdef FTK_PAIR_YN_WARP
+        float *ywarp = yns + warp * PR_BN;  // [2][HALF]
+#else
+        // one [2][PR_BN] buffer staged by the 256 screen threads (named barrier 1);
+        // FTK_PAIR_YN_WARP (per-warp buffers, no barrier) measured 5% slower
         const int et = warp * 32 + lane;  // 0..255
+        float *ywarp = yns + wg * HALF;     // reads: ywarp + ybuf * PR_BN
+#endif
+        auto yn4_of = [&](int64_t cfirst) {  // this lane's 4 norms of the half starting at cfirst
+            float4 v;
+            const int64_t c = cfirst + lane * 4;
+            v.x = c < P.k ? __ldg(P.yn + c) : INFINITY;
+            v.y = c + 1 < P.k ? __ldg(P.yn + c + 1) : INFINITY;
+            v.z = c + 2 < P.k ? __ldg(P.yn + c + 2) : INFINITY;
+            v.w = c + 3 < P.k ? __ldg(P.yn + c + 3) : INFINITY;
+            return v;
+        };
         int ybuf = 0;
+#ifdef FTK_PAIR_YN_WARP
+        reinterpret_cast<float4 *>(ywarp)[lane] = yn4_of(wg * HALF);
+        __syncwarp();
+#else
         if (et < PR_BN) yns[et] = et < P.k ? __ldg(P.yn + et) : INFINITY;
         asm volatile("bar.sync 1, 256;" ::: "memory");
+#endif
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
@@ -280,14 +300,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const int buf = g % PR_NBUF;
                 const int64_t c0 = int64_t(t) * PR_BN + wg * HALF;  // first column of this half
                 // prefetch the next tile's norms (wrapping into the next row tile)
+#ifdef FTK_PAIR_YN_WARP
+                const float4 yn_next = yn4_of(int64_t((t + 1) % P.ntiles) * PR_BN + wg * HALF);
+#else
                 const int64_t cn = int64_t((t + 1) % P.ntiles) * PR_BN + et;
                 const float yn_next = (et < PR_BN && cn < P.k) ? __ldg(P.yn + cn) : INFINITY;
+#endif
                 PROBE_T(cw_); mbar_wait(&t_full[buf], (g / PR_NBUF) & 1); PROBE_T(cb_); PROBE_ADD(1, cb_ - cw_);
                 tc_fence_after();
                 float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
                 float s0 = 0.0f, s1 = 0.0f;
                 const uint32_t tbase = tmem + lane_base + uint32_t(buf * PR_BN + wg * HALF);
-                const float *ynt = yns + ybuf * PR_BN + wg * HALF;
+#ifdef FTK_PAIR_YN_WARP
+                const float *ynt = ywarp + ybuf * HALF;
+#else
+                const float *ynt = ywarp + ybuf * PR_BN;
+#endif
                 const bool inj_here = INJ && inj_c >= int(c0) && inj_c < int(c0) + HALF;
                 if (P.dbg & 4) {
                     // timing probe: TMEM drain only (values folded with one XOR per column)
@@ -409,8 +437,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 if (t1 < m1) tile1 = t;
                 m1 = fminf(m1, t1);
                 m2 = fminf(fminf(m2, t2), hi);
+#ifdef FTK_PAIR_YN_WARP
+                __syncwarp();  // every lane is done reading the other buffer's previous tile
+                reinterpret_cast<float4 *>(ywarp + (ybuf ^ 1) * HALF)[lane] = yn_next;
+                __syncwarp();
+#else
                 if (et < PR_BN) yns[(ybuf ^ 1) * PR_BN + et] = yn_next;
                 asm volatile("bar.sync 1, 256;" ::: "memory");
+#endif
                 ybuf ^= 1;
             }
             if (COLLECT && ncand) atomicAdd(P.row_cnt + grow, ncand);
@@ -435,6 +469,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             if (t < nkb * 8) css[t] = __ldg(reinterpret_cast<const float4 *>(P.csum) + t);
             asm volatile("bar.sync 3, 128;" ::: "memory");
         }
+        // centroid row of this thread's winner in 32-float k-blocks: two
+        // statically indexed register buffers, k-blocks 0 and 1 prefetched
+        // for the hinted label (previous iteration) while the previous row
+        // tile is still being screened
+        float4 cA[8], cB[8];
+        int pj = -1;  // centroid whose k-blocks 0 and 1 are in cA / cB
+        auto load_row = [&](float4 (&cv)[8], int row_j, int kb, bool live) {
+            if (F64 || COLLECT) return;  // the float64 refine reads the centroid itself
+#ifdef FTK_PAIR_PROBE
+            if (P.dbg & 8) live = false;  // timing probe: no centroid loads
+#endif
+            const float4 *c4 = reinterpret_cast<const float4 *>(P.y + int64_t(live ? row_j : 0) * P.d);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                cv[q] = (live && kb * PR_KB + 4 * q < P.d) ? __ldg(c4 + kb * 8 + q)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        };
+        auto prefetch = [&](int64_t ptn) {
+            pj = -1;
+            if (F64 || COLLECT || !P.hint || ptn >= npt) return;
+            const int64_t gn = ptn * 2 * PR_BM + int64_t(rank) * PR_BM + r;
+            if (gn >= M) return;
+            const int h = __ldg(P.hint + gn);
+            if (h < 0 || h >= P.k) return;
+            pj = h;
+            load_row(cA, h, 0, true);
+            if (nkb > 1) load_row(cB, h, 1, true);
+        };
+        prefetch(pt0);
         int it = 0;
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
@@ -458,6 +521,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const int j = take1 ? q1.j1 : q0.j1;
             const float m2 = fminf(fminf(q0.m2, q1.m2), fmaxf(q0.m1, q1.m1));
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
+            const int pjv = pj;  // the prefetched centroid (cA / cB are clobbered below)
+            pj = -1;
             if (!SX) mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // own X half resident + visible
             const unsigned char *sAt = sA + size_t(ab) * A_BYTES + uint32_t(r) * 128;
             bool ok = false;
@@ -479,17 +544,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     ee = ri.y;
                     amax = ri.z;
                 }
-                // centroid row of this thread's winner in 32-float k-blocks,
-                // the next k-block in flight (two statically indexed register
-                // buffers); the X row comes from the resident tile
-                const float4 *cj4 = reinterpret_cast<const float4 *>(P.y + int64_t(active ? j : 0) * P.d);
-                auto load_c = [&](float4 (&cv)[8], int kb) {
-                    if (F64) return;  // the float64 refine reads the centroid itself
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        cv[q] = (active && kb * PR_KB + 4 * q < P.d) ? __ldg(cj4 + kb * 8 + q)
-                                                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-                };
+                // the winner's centroid row; the X row comes from the resident tile
+                auto load_c = [&](float4 (&cv)[8], int kb) { load_row(cv, j, kb, active); };
                 auto consume = [&](const float4 (&cv)[8], int kb) {
                     const int k0 = kb * PR_KB;
                     const unsigned char *rowp = sAt + uint32_t(kb) * PR_A_KB;
@@ -499,7 +555,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             const float4 xv =
                                 SX ? __ldg(xg4 + kb * 8 + q)
                                    : *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
+#ifdef FTK_PAIR_PROBE
+                            if (!F64 && !(P.dbg & 16)) {  // timing probe: bit 16 skips the exact chain
+#else
                             if (!F64) {
+#endif
                                 const float4 c4 = cv[q];
                                 acc = __fadd_rn(acc, __fmul_rn(xv.x, c4.x));
                                 acc = __fadd_rn(acc, __fmul_rn(xv.y, c4.y));
@@ -539,19 +599,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     if (lane == 0) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
                 };
                 PROBE_T(lp0_);
-                float4 cA[8], cB[8];
-                load_c(cA, 0);
+                if (!(active && j == pjv)) {  // no (matching) prefetch: k-blocks 0 and 1 now
+                    load_c(cA, 0);
+                    if (nkb > 1) load_c(cB, 1);
+                }
                 for (int kb = 0; kb < nkb; kb += 2) {
-                    if (kb + 1 < nkb) load_c(cB, kb + 1);
                     consume(cA, kb);
                     release(kb);
+                    if (kb + 2 < nkb) load_c(cA, kb + 2);
                     if (kb + 1 < nkb) {
-                        if (kb + 2 < nkb) load_c(cA, kb + 2);
                         consume(cB, kb + 1);
                         release(kb + 1);
+                        if (kb + 3 < nkb) load_c(cB, kb + 3);
                     }
                 }
                 released = true;
+                prefetch(pt + pstride);  // the next row tile's hinted centroids, k-blocks 0 and 1
                 PROBE_T(lp1_);
                 PROBE_ADD(8, lp1_ - lp0_);
               if (active) {  // lanes without a live row only helped with the loads
@@ -654,7 +717,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 // ------------------------------------------------------------- host ------
 size_t pair_smem_bytes(int nkb, int abufs, int stages, bool sx) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * (sx ? PR_B_HALF + PR_A_KB : PR_B_HALF) +
-           2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 2 * PR_BN * sizeof(float) +
+           2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 8 * PR_BN * sizeof(float) +
            8 * 8 * sizeof(float4) +
            (2 * size_t(stages) + 2 * PR_MAX_NA + 4 + 2 * PR_NBUF + PR_MAX_NA * PR_MAX_KB) * 8 + 64;
 }

@@ -49,6 +49,10 @@ struct PairParams {
     unsigned *row_cnt;
     const unsigned *m_dev;  // device-side row count (<= m) or null
     const float4 *rowinfo;  // per-fit row bounds (|x|^2, |x - tf32 x|^2, max|x|) or null
+    // previous iteration's labels (m entries) or null: the refine prefetches
+    // the hinted centroid's first two k-blocks during the previous row tile
+    // (a speed hint only: a row whose winner differs reloads)
+    const int32_t *hint;
     // float64 data screened in tf32 (tc64 path): per row (j1, T) -- T the
     // certificate threshold (j1 is the reference's argmin if its exact float64
     // value d1 < T); j1 = -1 when the row is not screenable (checksum flag,
