@@ -427,11 +427,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const float t1 = fminf(a1, b1);  // b1 = b2 = inf: single chain
                 const float t2 = fminf(fminf(a2, b2), fmaxf(a1, b1));
                 if (CHK) {
-                    // the warpgroup's 128-column group g = 2t + wg has location
-                    // weight g + 1: one multiply per group, none per column
+                    // the warpgroup's columns lie in one 128-column group g (2t + wg
+                    // for 256-wide tiles), location weight g + 1: one multiply per
+                    // group, none per column
                     const double gs = double(s0 + s1);
                     rsum += gs;
-                    wsum += gs * double(2 * t + wg + 1);
+                    wsum += gs * double((t * PR_BN + wg * HALF) / 128 + 1);
                 }
                 const float hi = fmaxf(m1, t1);
                 if (t1 < m1) tile1 = t;

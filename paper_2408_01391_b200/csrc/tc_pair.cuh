@@ -11,7 +11,10 @@ namespace ftk {
 
 // centroids per accumulator tile (the TMEM holds 512 / PAIR_BN buffers);
 // each CTA of the pair loads PAIR_BN / 2 centroid rows per k-block
-constexpr int PAIR_BN = 256;
+#ifndef FTK_PAIR_BN  // A/B knob: 128 (four TMEM buffers) measured 40% slower at c2
+#define FTK_PAIR_BN 256
+#endif
+constexpr int PAIR_BN = FTK_PAIR_BN;
 
 struct PairParams {
     const float *x;  // rows (global, read by the refine warps)
