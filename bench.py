@@ -494,6 +494,40 @@ def run_ours(args, rank, world):
         e_ft.close()
         del e_off, e_ft
 
+    # ---- DMR on the update (abft+dmr vs abft, fault-free), interleaved: the
+    # duplicated accumulators and the device compare run inside the graph steps
+    dmr = None
+    if args.campaign_s > 0:
+        reps, per = 5, 20
+        e_a, e_d = engine("abft"), engine("abft+dmr")
+        for e in (e_a, e_d):
+            e.step(0)
+            e.warm_graphs(1)
+        barrier()
+        tms = {0: [], 1: []}
+        gc.collect()
+        gc.disable()
+        for r in range(reps):
+            for side, e in ((0, e_a), (1, e_d)):
+                its = range(1 + r * per, 1 + (r + 1) * per)
+                last = its[-1]
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record()
+                for it in its:
+                    e.step(it, more=(lambda it=it: it < last))
+                s1.record()
+                torch.cuda.synchronize()
+                tms[side].append(s0.elapsed_time(s1))
+        gc.enable()
+        over = [100.0 * (b / a - 1.0) for a, b in zip(tms[0], tms[1])]
+        dmr = {"reps": reps, "steps_per_rep": per, "overhead_pct_median": statistics.median(over),
+               "abft_ms_per_step": sum(tms[0]) / (reps * per), "dmr_ms_per_step": sum(tms[1]) / (reps * per),
+               "dmr_mismatches": e_d.report.dmr_mismatches, "graph_steps": bool(e_d.use_graph),
+               "labels_equal": bool((e_a.labels_view() == e_d.labels_view()).all().item())}
+        e_a.close()
+        e_d.close()
+        del e_a, e_d
+
     kern_ms = k_ft if k_ft else a_ft
     achieved = flops / (kern_ms * 1e-3) / 1e12
     traffic = None
@@ -575,6 +609,7 @@ def run_ours(args, rank, world):
         "faults": {"injected": injected, "detections": rep.detections,
                    "corrections": rep.corrections, "uncorrectable": rep.uncorrectable, "p_tile": p},
         "ft_campaign": campaign,
+        "dmr": dmr,
         "step_ms": {"ft_off": step_stats[0], "abft": step_stats[1]},
         "gpu_launches": launches,
         "clocks": clocks,

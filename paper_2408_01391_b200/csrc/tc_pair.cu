@@ -58,7 +58,11 @@ constexpr int PR_THREADS = 480;     // 15 warps
 // Warp roles.  The SMSP arbiter favours the highest warp id, so the
 // latency-critical single-thread roles (MMA issue, TMA producers) take the
 // top ids and are never starved by the screening warps.
-constexpr int W_REFINE0 = 8;        // warps 0..7 screen, 8..11 refine
+#ifdef FTK_PAIR_REFINE_LOW  // A/B: refine warps 0..3, screen warps 4..11
+constexpr int W_SCREEN0 = 4, W_REFINE0 = 0;
+#else
+constexpr int W_SCREEN0 = 0, W_REFINE0 = 8;  // warps 0..7 screen, 8..11 refine
+#endif
 constexpr int W_XPROD = 12;         // X half-tile producer (+ peer forwarding)
 constexpr int W_PROD = 13;          // centroid-stream TMA producer
 constexpr int W_MMA = 14;           // TMEM allocator; leader: MMA issuer
@@ -240,13 +244,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
             }
         }
-    } else if (warp < W_REFINE0) {
+    } else if (warp >= W_SCREEN0 && warp < W_SCREEN0 + 8) {
         // ----------------------------------------------------- screen --
         // Both warpgroups drain every accumulator tile: warpgroup wg takes
         // columns [128 wg, 128 wg + 128) of the 256-wide tile, so a TMEM
         // buffer is released after half a tile's worth of epilogue work.
-        const int wg = warp >> 2;
-        const int quad = warp & 3;
+        const int wg = (warp - W_SCREEN0) >> 2;
+        const int quad = warp & 3;  // TMEM lane quadrant: warp % 4
         const int r = quad * 32 + lane;
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
         const uint32_t t_empty_lead0 = mapa_shared(smem_u32(&t_empty[0]), 0);
@@ -255,11 +259,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         int it = 0;
         // centroid norms of the current tile, staged one tile ahead
 #ifdef FTK_PAIR_YN_WARP
-        float *ywarp = yns + warp * PR_BN;  // [2][HALF]
+        float *ywarp = yns + (warp - W_SCREEN0) * PR_BN;  // [2][HALF]
 #else
         // one [2][PR_BN] buffer staged by the 256 screen threads (named barrier 1);
         // FTK_PAIR_YN_WARP (per-warp buffers, no barrier) measured 5% slower
-        const int et = warp * 32 + lane;  // 0..255
+        const int et = (warp - W_SCREEN0) * 32 + lane;  // 0..255
         float *ywarp = yns + wg * HALF;     // reads: ywarp + ybuf * PR_BN
 #endif
         auto yn4_of = [&](int64_t cfirst) {  // this lane's 4 norms of the half starting at cfirst
@@ -461,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
         }
-    } else if (warp < W_XPROD) {
+    } else if (warp >= W_REFINE0 && warp < W_REFINE0 + 4) {
         // ----------------------------------------------------- refine --
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
@@ -532,6 +536,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             unsigned long long seed_out = ~0ull;  // (ordered d1, j1) key
             const bool active = !COLLECT && grow < M && m1 < INFINITY && !(P.dbg & 2);
             bool released = false;  // X k-blocks handed back (warp-uniform)
+#ifdef FTK_PAIR_PROBE
+            if ((P.dbg & 128) && !SX) {  // timing probe: hand X back at once (results invalid)
+                __syncwarp();
+                if (lane == 0)
+                    for (int kb = 0; kb < nkb; ++kb) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
+                released = true;
+            }
+#endif
             if (!COLLECT && !(P.dbg & 2) && __any_sync(0xffffffffu, active)) {
                 float acc = 0.0f, xx = 0.0f, ee = 0.0f, amax = 0.0f;
                 float rr[4] = {0.0f, 0.0f, 0.0f, 0.0f};  // ABFT reference x~ . csum (fp32)
@@ -553,9 +565,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 #pragma unroll
                     for (int q = 0; q < 8; ++q) {
                         if (k0 + 4 * q < P.d) {
+#ifdef FTK_PAIR_PROBE
+                            const float4 xv = (P.dbg & 32) ? make_float4(1.f, 1.f, 1.f, 1.f) :
+                                (SX ? __ldg(xg4 + kb * 8 + q)
+                                    : *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4)));
+#else
                             const float4 xv =
                                 SX ? __ldg(xg4 + kb * 8 + q)
                                    : *reinterpret_cast<const float4 *>(rowp + ((q ^ (r & 7)) << 4));
+#endif
 #ifdef FTK_PAIR_PROBE
                             if (!F64 && !(P.dbg & 16)) {  // timing probe: bit 16 skips the exact chain
 #else
@@ -585,7 +603,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                                              fmaxf(fabsf(xv.z), fabsf(xv.w))));
                             }
                             if (CHK) {
+#ifdef FTK_PAIR_PROBE
+                                const float4 sv = (P.dbg & 64) ? make_float4(1.f, 1.f, 1.f, 1.f) : cs4[kb * 8 + q];
+#else
                                 const float4 sv = cs4[kb * 8 + q];
+#endif
                                 rr[0] = fmaf(tf32_trunc(xv.x), sv.x, rr[0]);
                                 rr[1] = fmaf(tf32_trunc(xv.y), sv.y, rr[1]);
                                 rr[2] = fmaf(tf32_trunc(xv.z), sv.z, rr[2]);
@@ -595,7 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     }
                 };
                 auto release = [&](int kb) {  // this warp is done reading X k-block kb
-                    if (SX) return;
+                    if (SX || released) return;
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&a_kbe[ab * PR_MAX_KB + kb]);
                 };
@@ -702,7 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     }
 
 #ifdef FTK_PAIR_PROBE
-    if (P.clk && lane == 0 && (warp == 0 || warp == W_MMA || warp == W_REFINE0 || warp == W_XPROD))
+    if (P.clk && lane == 0 && (warp == W_SCREEN0 || warp == W_MMA || warp == W_REFINE0 || warp == W_XPROD))
         for (int q = 0; q < 10; ++q) atomicAdd(reinterpret_cast<unsigned long long *>(P.clk) + q,
                                               (unsigned long long)clk[q]);
 #endif

@@ -22,7 +22,7 @@ for it in range(4):
     eng.step(it)
 cent = eng.cent.clone()
 yn = E.row_sq_norms_dev(cent)
-for dbg in [0, 2, 1, 4, 3, 6, 0]:
+for dbg in ([int(v) for v in sys.argv[1:]] or [0, 2, 1, 4, 3, 6, 0]):
     os.environ["FTK_TC_DEBUG"] = str(dbg)
     ms = []
     for r in range(3):
