@@ -772,6 +772,27 @@ int make_tc_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
     return make_map(map, base, rows, cols, box_rows);
 }
 
+// float64 rows, box = 16 doubles (one 128-byte swizzle row) x box_rows, 128B swizzle
+int make_f64_map(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, uint32_t box_rows) {
+    PFN_encodeTiled enc = get_encode();
+    if (!enc) {
+        set_error("cuTensorMapEncodeTiled unavailable");
+        return FTK_ERR_CUDA;
+    }
+    cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows < 1 ? 1 : rows)};
+    cuuint64_t strides[1] = {cuuint64_t(cols) * sizeof(double)};
+    cuuint32_t box[2] = {16, box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (f64) failed (" + std::to_string(int(r)) + ")");
+        return FTK_ERR_CUDA;
+    }
+    return FTK_OK;
+}
+
 // Unswizzled 2-D map with an arbitrary box (cols * 4 bytes a multiple of 16).
 int make_plain_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols,
                    uint32_t box_cols, uint32_t box_rows) {

@@ -37,6 +37,7 @@
 namespace ftk {
 
 int make_tc_map(CUtensorMap *map, const float *base, int64_t rows, int64_t cols, uint32_t box_rows);
+int make_f64_map(CUtensorMap *map, const double *base, int64_t rows, int64_t cols, uint32_t box_rows);
 int prep_csum_run(ftk_ctx *ctx, int slot, const float *y, int64_t k, int64_t d, int nkb, int trunc,
                   float **csum, float **camax, cudaStream_t st, float **csumw);
 int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn, int64_t m,
@@ -184,6 +185,138 @@ __global__ void __launch_bounds__(32 * R64_WARPS) tc64_refine_kernel(
     }
 }
 
+// TMA-fed variant: a producer warp streams 32-row tiles of X (all d
+// features, 16-double x 32-row boxes with 128-byte swizzle) into one
+// shared-memory slot per consumer warp; four consumer warps take the tiles
+// round-robin, one lane per row running its winner's float64 chain from the
+// swizzled tile (16-byte reads, 4 wavefronts per warp) with the centroid chunk
+// from L2.  The copy engine, not a warp's outstanding loads, keeps X in flight.
+constexpr int RT_CONS = 4;  // consumer warps
+struct RtGeom {
+    int nbox;       // 16-double boxes per row (ceil(d / 16))
+    int stages;     // ring depth
+    size_t stage;   // bytes per stage (nbox * 4 KB)
+};
+__global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
+    const __grid_constant__ CUtensorMap tmx, const double *y, const double *yn, int64_t m, int64_t d,
+    int nbox, const int2 *rec, int32_t *out_idx, double *out_val, int32_t *fb,
+    unsigned *fb_count) {
+    extern __shared__ __align__(1024) unsigned char rt_raw[];
+    unsigned char *smem = rt_raw + ((1024u - (smem_u32(rt_raw) & 1023u)) & 1023u);
+    constexpr int stages = RT_CONS;  // slot w belongs to consumer w
+    const size_t stage_bytes = size_t(nbox) * 4096;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + size_t(stages) * stage_bytes);
+    uint64_t *empty = full + stages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntile = (m + 31) / 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    if (warp == RT_CONS) {
+        // ----------------------------------------------------- producer --
+        if (lane == 0) {
+            prefetch_tmap(&tmx);
+            int q = 0;
+            for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++q) {
+                const int s = q % stages;
+                mbar_wait(&empty[s], (uint32_t(q / stages) & 1u) ^ 1u);
+                mbar_expect_tx(&full[s], uint32_t(stage_bytes));
+                for (int b = 0; b < nbox; ++b)
+                    tma_load_2d(smem + size_t(s) * stage_bytes + size_t(b) * 4096, &tmx, &full[s], b * 16,
+                                int(tile * 32));
+            }
+        }
+        return;
+    }
+    // ------------------------------------------------------- consumers --
+    int q = warp;
+    for (int64_t tile = int64_t(blockIdx.x) + int64_t(warp) * gridDim.x; tile < ntile;
+         tile += int64_t(gridDim.x) * RT_CONS, q += RT_CONS) {
+        const int s = q % stages;
+        const int64_t row = tile * 32 + lane;
+        const int2 r = row < m ? rec[row] : make_int2(-1, 0);
+        const int j = r.x;
+        const double *cr = y + int64_t(j < 0 ? 0 : j) * d;
+        double cv[16];
+        auto load_c = [&](int f0) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const bool ok = j >= 0 && f0 + 2 * u + 1 < d;
+                const double2 c2 = ok ? __ldg(reinterpret_cast<const double2 *>(cr + f0) + u) : make_double2(0.0, 0.0);
+                cv[2 * u] = c2.x;
+                cv[2 * u + 1] = c2.y;
+            }
+        };
+        load_c(0);  // the first chunk's centroid values travel while the tile lands
+        mbar_wait(&full[s], uint32_t(q / stages) & 1u);
+        const unsigned char *tb = smem + size_t(s) * stage_bytes + lane * 128;
+        const int sw = lane & 7;
+        double acc = 0.0;
+        for (int b = 0; b < nbox; ++b) {
+            const int f0 = b * 16;
+            double cn[16];
+            const bool more = b + 1 < nbox;
+            if (more) {  // next chunk's centroid values in flight during this chunk's chain
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const bool ok = j >= 0 && f0 + 16 + 2 * u + 1 < d;
+                    const double2 c2 = ok ? __ldg(reinterpret_cast<const double2 *>(cr + f0 + 16) + u)
+                                          : make_double2(0.0, 0.0);
+                    cn[2 * u] = c2.x;
+                    cn[2 * u + 1] = c2.y;
+                }
+            }
+            const unsigned char *bx = tb + size_t(b) * 4096;
+            if (f0 + 16 <= d) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const double2 xv = *reinterpret_cast<const double2 *>(bx + ((u ^ sw) << 4));
+                    acc = __dadd_rn(acc, __dmul_rn(xv.x, cv[2 * u]));
+                    acc = __dadd_rn(acc, __dmul_rn(xv.y, cv[2 * u + 1]));
+                }
+            } else {
+                for (int f = f0; f < d; ++f) {
+                    const int fc = f - f0;
+                    const double xv = *reinterpret_cast<const double *>(bx + (((fc >> 1) ^ sw) << 4) + (fc & 1) * 8);
+                    acc = __dadd_rn(acc, __dmul_rn(xv, __ldg(cr + f)));
+                }
+            }
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < 16; ++u) cv[u] = cn[u];
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        bool need = false;
+        if (row < m) {
+            bool ok = false;
+            double dval = 0.0;
+            if (j >= 0) {
+                dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
+                ok = isfinite(dval) && double(__int_as_float(r.y)) > dval;
+            }
+            if (ok) {
+                out_idx[row] = j;
+                out_val[row] = dval;
+            }
+            need = !ok;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, need);
+        if (bal) {
+            unsigned b0 = 0;
+            if (lane == 0) b0 = atomicAdd(fb_count, unsigned(__popc(bal)));
+            b0 = __shfl_sync(0xffffffffu, b0, 0);
+            if (need) fb[b0 + __popc(bal & ((1u << lane) - 1u))] = int32_t(row);
+        }
+    }
+}
+
 __global__ void tc64_gather_kernel(const double *x, int64_t d, const int32_t *rows, const unsigned *count,
                                    double *g) {
     const int64_t n = int64_t(*count) * d;
@@ -293,10 +426,28 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     if (!rc) rc = make_tc_map(&mc, c32, k, d, PAIR_BN / 2);
     if (rc) return rc;
     if ((rc = pair_screen_launch(mx, mc, Q, ft != nullptr, st))) return rc;
-    tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 32 * R64_WARPS - 1) / (32 * R64_WARPS), 148 * 6)),
-                         32 * R64_WARPS, 0, st>>>(
-        x, y, yn, m, d, rec, out_idx, out_val, fb, cnt);
-    FTK_LAUNCHED("tc64_refine_kernel");
+    {
+        const int nbox = int((d + 15) / 16);
+        const size_t stage = size_t(nbox) * 4096;
+        const size_t ring = size_t(RT_CONS) * stage;  // one slot per consumer warp
+        CUtensorMap tx;
+        const bool tma = ring <= 200 * 1024 && !getenv("FTK_T64_REFINE_LDG") && !make_f64_map(&tx, x, m, d, 32);
+        if (tma) {
+            const int per_sm = int(std::min<size_t>(3, (200 * 1024) / ring));  // CTAs per SM
+            const size_t smem = ring + 16 * RT_CONS + 1024;
+            FTK_CUDA(cudaFuncSetAttribute(tc64_refine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(smem)));
+            const int64_t ntile = (m + 31) / 32;
+            tc64_refine_tma_kernel<<<unsigned(std::min<int64_t>(ntile, int64_t(148) * per_sm)),
+                                     32 * (RT_CONS + 1), smem, st>>>(tx, y, yn, m, d, nbox, rec, out_idx,
+                                                                     out_val, fb, cnt);
+            FTK_LAUNCHED("tc64_refine_tma_kernel");
+        } else {
+            tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 32 * R64_WARPS - 1) / (32 * R64_WARPS), 148 * 6)),
+                                 32 * R64_WARPS, 0, st>>>(x, y, yn, m, d, rec, out_idx, out_val, fb, cnt);
+            FTK_LAUNCHED("tc64_refine_kernel");
+        }
+    }
     if (ft) {
         // location + event records of the checksum-flagged rows (the DMMA pass
         // below re-resolves them: the correction)
