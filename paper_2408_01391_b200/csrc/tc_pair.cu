@@ -54,18 +54,20 @@ constexpr int PR_NBUF = 512 / PR_BN;  // TMEM accumulator buffers
 constexpr int PR_KB = 32;           // fp32 elements per 128-byte swizzle row
 constexpr int PR_MAX_KB = 8;        // k-blocks of the widest X row (d <= 256)
 constexpr int PR_MAX_NA = 4;        // X half-tile buffers (4 when few centroid k-blocks per row tile)
-constexpr int PR_THREADS = 480;     // 15 warps
+#ifndef FTK_PAIR_SWG
+#define FTK_PAIR_SWG 2
+#endif
+constexpr int PR_SWG = FTK_PAIR_SWG;  // screen warpgroups (each drains a column range of every tile)
+constexpr int PR_NCH = PR_BN / 32;    // 32-column chunks per tile
+constexpr int PR_THREADS = 32 * (4 * PR_SWG + 7);  // screen, 4 refine, X producer, C producer, MMA
 // Warp roles.  The SMSP arbiter favours the highest warp id, so the
 // latency-critical single-thread roles (MMA issue, TMA producers) take the
 // top ids and are never starved by the screening warps.
-#ifdef FTK_PAIR_REFINE_LOW  // A/B: refine warps 0..3, screen warps 4..11
-constexpr int W_SCREEN0 = 4, W_REFINE0 = 0;
-#else
-constexpr int W_SCREEN0 = 0, W_REFINE0 = 8;  // warps 0..7 screen, 8..11 refine
-#endif
-constexpr int W_XPROD = 12;         // X half-tile producer (+ peer forwarding)
-constexpr int W_PROD = 13;          // centroid-stream TMA producer
-constexpr int W_MMA = 14;           // TMEM allocator; leader: MMA issuer
+// warps 0..4*PR_SWG-1 screen, then 4 refine (refine on low ids measured +3 %)
+constexpr int W_SCREEN0 = 0, W_REFINE0 = 4 * PR_SWG;
+constexpr int W_XPROD = W_REFINE0 + 4;  // X half-tile producer (+ peer forwarding)
+constexpr int W_PROD = W_REFINE0 + 5;   // centroid-stream TMA producer
+constexpr int W_MMA = W_REFINE0 + 6;    // TMEM allocator; leader: MMA issuer
 constexpr uint32_t PR_A_KB = PR_BM * 128;         // bytes of one X k-block
 constexpr uint32_t PR_B_HALF = (PR_BN / 2) * 128;  // bytes of one centroid half k-block
 
@@ -105,8 +107,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     unsigned char *sA = smem;
     unsigned char *sB = sA + size_t(NA) * A_BYTES;
     PairPart *part = reinterpret_cast<PairPart *>(sB + size_t(S) * STG);  // [2][2][128]
-    double2 *psum = reinterpret_cast<double2 *>(part + 2 * 2 * PR_BM);         // [2][2][128] (sum, weighted)
-    float *yns = reinterpret_cast<float *>(psum + 2 * 2 * PR_BM);  // [8 screen warps][2][PR_BN / 2]
+    double2 *psum = reinterpret_cast<double2 *>(part + 2 * PR_SWG * PR_BM);  // [2][PR_SWG][128] (sum, weighted)
+    float *yns = reinterpret_cast<float *>(psum + 2 * PR_SWG * PR_BM);       // [2][PR_BN] (8 * PR_BN reserved)
     float4 *css = reinterpret_cast<float4 *>(yns + 8 * PR_BN);      // ABFT checksum centroid [nkb * 8]
     uint64_t *bars = reinterpret_cast<uint64_t *>(css + 8 * 8);
     uint64_t *full = bars, *empty = bars + S;
@@ -143,12 +145,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             for (int kb = 0; kb < PR_MAX_KB; ++kb) mbar_init(&a_kbe[a * PR_MAX_KB + kb], 4);
         }
         for (int a = 0; a < 2; ++a) {
-            mbar_init(&p_full[a], 8);
+            mbar_init(&p_full[a], 4 * PR_SWG);
             mbar_init(&p_empty[a], 4);
         }
         for (int b = 0; b < PR_NBUF; ++b) {
             mbar_init(&t_full[b], 1);
-            mbar_init(&t_empty[b], 16);                // 8 screen warps x 2 CTAs
+            mbar_init(&t_empty[b], 2 * 4 * PR_SWG);  // screen warps x 2 CTAs
         }
         fence_barrier_init();
     }
@@ -244,45 +246,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
             }
         }
-    } else if (warp >= W_SCREEN0 && warp < W_SCREEN0 + 8) {
+    } else if (warp >= W_SCREEN0 && warp < W_SCREEN0 + 4 * PR_SWG) {
         // ----------------------------------------------------- screen --
-        // Both warpgroups drain every accumulator tile: warpgroup wg takes
-        // columns [128 wg, 128 wg + 128) of the 256-wide tile, so a TMEM
-        // buffer is released after half a tile's worth of epilogue work.
+        // Every warpgroup drains every accumulator tile: warpgroup wg takes
+        // chunks [cb0, cb1) of the tile's PR_NCH 32-column chunks, so a TMEM
+        // buffer is released after 1/PR_SWG of a tile's epilogue work.
         const int wg = (warp - W_SCREEN0) >> 2;
         const int quad = warp & 3;  // TMEM lane quadrant: warp % 4
         const int r = quad * 32 + lane;
         const uint32_t lane_base = uint32_t(quad * 32) << 16;
         const uint32_t t_empty_lead0 = mapa_shared(smem_u32(&t_empty[0]), 0);
-        constexpr int HALF = PR_BN / 2;
+        const int cb0 = (PR_NCH * wg) / PR_SWG, cb1 = (PR_NCH * (wg + 1)) / PR_SWG;
+        const int cbeg = cb0 * 32, nch = cb1 - cb0, ncol = nch * 32;
+        // a warpgroup range crossing a 128-column group boundary (PR_SWG = 3)
+        // splits its checksum partial at chunk `split` (location weights)
+        const int split = (cb0 < 4 && cb1 > 4) ? 4 - cb0 : -1;
         uint32_t g = 0;
         int it = 0;
         // centroid norms of the current tile, staged one tile ahead
-#ifdef FTK_PAIR_YN_WARP
-        float *ywarp = yns + (warp - W_SCREEN0) * PR_BN;  // [2][HALF]
-#else
-        // one [2][PR_BN] buffer staged by the 256 screen threads (named barrier 1);
-        // FTK_PAIR_YN_WARP (per-warp buffers, no barrier) measured 5% slower
+        // one [2][PR_BN] buffer staged by the screen threads (named barrier 1);
+        // per-warp buffers without the barrier measured 5% slower
         const int et = (warp - W_SCREEN0) * 32 + lane;  // 0..255
-        float *ywarp = yns + wg * HALF;     // reads: ywarp + ybuf * PR_BN
-#endif
-        auto yn4_of = [&](int64_t cfirst) {  // this lane's 4 norms of the half starting at cfirst
-            float4 v;
-            const int64_t c = cfirst + lane * 4;
-            v.x = c < P.k ? __ldg(P.yn + c) : INFINITY;
-            v.y = c + 1 < P.k ? __ldg(P.yn + c + 1) : INFINITY;
-            v.z = c + 2 < P.k ? __ldg(P.yn + c + 2) : INFINITY;
-            v.w = c + 3 < P.k ? __ldg(P.yn + c + 3) : INFINITY;
-            return v;
-        };
+        float *ywarp = yns + cbeg;          // reads: ywarp + ybuf * PR_BN
         int ybuf = 0;
-#ifdef FTK_PAIR_YN_WARP
-        reinterpret_cast<float4 *>(ywarp)[lane] = yn4_of(wg * HALF);
-        __syncwarp();
-#else
         if (et < PR_BN) yns[et] = et < P.k ? __ldg(P.yn + et) : INFINITY;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-#endif
+        asm volatile("bar.sync 1, %0;" ::"n"(128 * PR_SWG) : "memory");
         for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
             const int pb = it & 1;
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
@@ -302,30 +290,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             }
             for (int t = 0; t < P.ntiles; ++t, ++g) {
                 const int buf = g % PR_NBUF;
-                const int64_t c0 = int64_t(t) * PR_BN + wg * HALF;  // first column of this half
+                const int64_t c0 = int64_t(t) * PR_BN + cbeg;  // first column of this warpgroup's range
                 // prefetch the next tile's norms (wrapping into the next row tile)
-#ifdef FTK_PAIR_YN_WARP
-                const float4 yn_next = yn4_of(int64_t((t + 1) % P.ntiles) * PR_BN + wg * HALF);
-#else
                 const int64_t cn = int64_t((t + 1) % P.ntiles) * PR_BN + et;
                 const float yn_next = (et < PR_BN && cn < P.k) ? __ldg(P.yn + cn) : INFINITY;
-#endif
                 PROBE_T(cw_); mbar_wait(&t_full[buf], (g / PR_NBUF) & 1); PROBE_T(cb_); PROBE_ADD(1, cb_ - cw_);
                 tc_fence_after();
                 float a1 = INFINITY, a2 = INFINITY, b1 = INFINITY, b2 = INFINITY;
                 float s0 = 0.0f, s1 = 0.0f;
-                const uint32_t tbase = tmem + lane_base + uint32_t(buf * PR_BN + wg * HALF);
-#ifdef FTK_PAIR_YN_WARP
-                const float *ynt = ywarp + ybuf * HALF;
-#else
+                const uint32_t tbase = tmem + lane_base + uint32_t(buf * PR_BN + cbeg);
                 const float *ynt = ywarp + ybuf * PR_BN;
-#endif
-                const bool inj_here = INJ && inj_c >= int(c0) && inj_c < int(c0) + HALF;
+                const bool inj_here = INJ && inj_c >= int(c0) && inj_c < int(c0) + ncol;
+                float gA = 0.0f;  // checksum partial before the group split
                 if (P.dbg & 4) {
                     // timing probe: TMEM drain only (values folded with one XOR per column)
                     uint32_t va[32], acc = 0;
 #pragma unroll 1
-                    for (int ch = 0; ch < HALF / 32; ++ch) {
+                    for (int ch = 0; ch < nch; ++ch) {
                         tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
                         tmem_ld_wait(va);
 #pragma unroll
@@ -338,7 +319,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     uint32_t va[32];
                     int nloc = 0, lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0;
 #pragma unroll 1
-                    for (int ch = 0; ch < HALF / 32; ++ch) {
+                    for (int ch = 0; ch < nch; ++ch) {
                         tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
                         tmem_ld_wait(va);
                         const float4 *yn4 = reinterpret_cast<const float4 *>(ynt + ch * 32);
@@ -396,31 +377,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     // skipped (a plain loop: the full-tile loop stays as is)
                     const int live = int(P.k - c0);
                     uint32_t va[32], vb[32];
-                    if (live >= HALF) {
+                    if (live >= ncol) {
                         tmem_ld32_issue(tbase, va);
                         tmem_ld_wait(va);
 #pragma unroll 1
-                        for (int ch = 0; ch < HALF / 32; ch += 2) {
-                            tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
+                        for (int ch = 0; ch < nch; ch += 2) {
+                            const bool two = ch + 1 < nch;
+                            if (two) tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
                             if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
                                 inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
-                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
-                            tmem_ld_wait(vb);
-                            if (ch + 2 < HALF / 32) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
-                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
-                                inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
-                            screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(wg * HALF + (ch + 1) * 32),
-                                           a1, a2, s0, s1);
-                            if (ch + 2 < HALF / 32) tmem_ld_wait(va);
+                            if (CHK && ch == split) { gA = s0 + s1; s0 = s1 = 0.0f; }
+                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(cbeg + ch * 32), a1, a2, s0, s1);
+                            if (two) {
+                                tmem_ld_wait(vb);
+                                if (ch + 2 < nch) tmem_ld32_issue(tbase + uint32_t((ch + 2) * 32), va);
+                                if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
+                                    inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                                if (CHK && ch + 1 == split) { gA = s0 + s1; s0 = s1 = 0.0f; }
+                                screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(cbeg + (ch + 1) * 32),
+                                               a1, a2, s0, s1);
+                                if (ch + 2 < nch) tmem_ld_wait(va);
+                            }
                         }
                     } else {
 #pragma unroll 1
-                        for (int ch = 0; ch * 32 < live; ++ch) {
+                        for (int ch = 0; ch < nch && ch * 32 < live; ++ch) {
                             tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
                             tmem_ld_wait(va);
                             if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
                                 inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
-                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(wg * HALF + ch * 32), a1, a2, s0, s1);
+                            if (CHK && ch == split) { gA = s0 + s1; s0 = s1 = 0.0f; }
+                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(cbeg + ch * 32), a1, a2, s0, s1);
                         }
                     }
                 }
@@ -431,25 +418,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const float t1 = fminf(a1, b1);  // b1 = b2 = inf: single chain
                 const float t2 = fminf(fminf(a2, b2), fmaxf(a1, b1));
                 if (CHK) {
-                    // the warpgroup's columns lie in one 128-column group g (2t + wg
-                    // for 256-wide tiles), location weight g + 1: one multiply per
-                    // group, none per column
+                    // the warpgroup's columns lie in one 128-column group g (two when
+                    // its range crosses a group boundary: gA before, the rest
+                    // after), location weight g + 1: one multiply per group
+                    const int gf = (t * PR_BN + cbeg) / 128;
                     const double gs = double(s0 + s1);
-                    rsum += gs;
-                    wsum += gs * double((t * PR_BN + wg * HALF) / 128 + 1);
+                    rsum += double(gA) + gs;
+                    wsum += double(gA) * double(gf + 1) + gs * double(gf + 1 + (split >= 0 ? 1 : 0));
                 }
                 const float hi = fmaxf(m1, t1);
                 if (t1 < m1) tile1 = t;
                 m1 = fminf(m1, t1);
                 m2 = fminf(fminf(m2, t2), hi);
-#ifdef FTK_PAIR_YN_WARP
-                __syncwarp();  // every lane is done reading the other buffer's previous tile
-                reinterpret_cast<float4 *>(ywarp + (ybuf ^ 1) * HALF)[lane] = yn_next;
-                __syncwarp();
-#else
                 if (et < PR_BN) yns[(ybuf ^ 1) * PR_BN + et] = yn_next;
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-#endif
+                asm volatile("bar.sync 1, %0;" ::"n"(128 * PR_SWG) : "memory");
                 ybuf ^= 1;
             }
             if (COLLECT && ncand) atomicAdd(P.row_cnt + grow, ncand);
@@ -460,8 +442,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             pp.j1 = tile1 * PR_BN + int(__float_as_uint(m1) & 0xFFu);
             pp.m2 = m2;
             pp.pad = 0.0f;
-            part[(pb * 2 + wg) * PR_BM + r] = pp;
-            if (CHK) psum[(pb * 2 + wg) * PR_BM + r] = make_double2(rsum, wsum);
+            part[(pb * PR_SWG + wg) * PR_BM + r] = pp;
+            if (CHK) psum[(pb * PR_SWG + wg) * PR_BM + r] = make_double2(rsum, wsum);
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[pb]);
         }
@@ -511,20 +493,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             mbar_wait(&p_full[pb], uint32_t(it >> 1) & 1);
             PROBE_T(rw1_);
             PROBE_ADD(6, rw1_ - rw0_);
-            const PairPart q0 = part[(pb * 2 + 0) * PR_BM + r];
-            const PairPart q1 = part[(pb * 2 + 1) * PR_BM + r];
+            // merge the warpgroups' partials (ascending column ranges: a tie
+            // keeps the earlier range, the reference's lowest index)
+            float m1 = INFINITY, m2 = INFINITY;
+            int j = 0;
             double rsum = 0.0, wsum = 0.0;
-            if (CHK) {
-                const double2 u0 = psum[(pb * 2 + 0) * PR_BM + r], u1 = psum[(pb * 2 + 1) * PR_BM + r];
-                rsum = u0.x + u1.x;
-                wsum = u0.y + u1.y;
+#pragma unroll
+            for (int w = 0; w < PR_SWG; ++w) {
+                const PairPart q = part[(pb * PR_SWG + w) * PR_BM + r];
+                const float hi = fmaxf(m1, q.m1);
+                if (q.m1 < m1) j = q.j1;
+                m1 = fminf(m1, q.m1);
+                m2 = fminf(fminf(m2, q.m2), hi);
+                if (CHK) {
+                    const double2 u = psum[(pb * PR_SWG + w) * PR_BM + r];
+                    rsum += u.x;
+                    wsum += u.y;
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_empty[pb]);
-            const bool take1 = q1.m1 < q0.m1;
-            const float m1 = take1 ? q1.m1 : q0.m1;
-            const int j = take1 ? q1.j1 : q0.j1;
-            const float m2 = fminf(fminf(q0.m2, q1.m2), fmaxf(q0.m1, q1.m1));
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
             const int pjv = pj;  // the prefetched centroid (cA / cB are clobbered below)
             pj = -1;
@@ -740,7 +728,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
 // ------------------------------------------------------------- host ------
 size_t pair_smem_bytes(int nkb, int abufs, int stages, bool sx) {
     return 1024 + size_t(abufs) * PR_A_KB * nkb + size_t(stages) * (sx ? PR_B_HALF + PR_A_KB : PR_B_HALF) +
-           2 * 2 * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 8 * PR_BN * sizeof(float) +
+           2 * PR_SWG * PR_BM * (sizeof(PairPart) + sizeof(double2)) + 8 * PR_BN * sizeof(float) +
            8 * 8 * sizeof(float4) +
            (2 * size_t(stages) + 2 * PR_MAX_NA + 4 + 2 * PR_NBUF + PR_MAX_NA * PR_MAX_KB) * 8 + 64;
 }
