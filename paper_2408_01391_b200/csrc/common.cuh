@@ -68,6 +68,13 @@ struct ftk_ctx {
 };
 
 namespace ftk {
+// SM count of the CURRENT device (each rank of a multi-GPU run drives its own)
+inline int current_sm_count() {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    return nsm;
+}
 // Returns a device buffer of at least `bytes` for `slot` of this context.
 void *scratch(ftk_ctx *ctx, int slot, size_t bytes, cudaStream_t st);
 // The context's cumulative row-checksum flag counter (allocated and zeroed

@@ -547,7 +547,7 @@ int dscreen_run(ftk_ctx *ctx, const double *x, const double *y, const double *yn
     }
     const int64_t nrt = (m + DS_BM - 1) / DS_BM;
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    nsm = current_sm_count();
     const unsigned grid = unsigned(std::min<int64_t>(nrt, int64_t(nsm)));
     const char *se = getenv("FTK_F64_SIMT");
     if (ctx->family == 4 || (ctx->family != 3 && se && atoi(se))) {  // DFMA SIMT screen

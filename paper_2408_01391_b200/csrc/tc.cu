@@ -841,7 +841,7 @@ static int launch_screen(TcParams P, const CUtensorMap &mx, const CUtensorMap &m
     const int64_t ntm = (P.m + TC_BM - 1) / TC_BM;
     if (ntm == 0) return FTK_OK;
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    nsm = current_sm_count();
     const int64_t grid = ntm < nsm ? ntm : nsm;
     auto kern = tc_screen_kernel<BN, SPLIT, CHK>;
     FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

@@ -774,7 +774,7 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     const int64_t npt = (P.m + 2 * PR_BM - 1) / (2 * PR_BM);
     if (npt == 0) return FTK_OK;
     int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    nsm = current_sm_count();
     const int64_t ncl = npt < nsm / 2 ? npt : nsm / 2;
     if (P.rec64) {  // float64 data, fp32 copy resident (d <= 256)
         if (sx) {
