@@ -59,7 +59,16 @@ constexpr int PR_MAX_NA = 4;        // X half-tile buffers (4 when few centroid 
 #endif
 constexpr int PR_SWG = FTK_PAIR_SWG;  // screen warpgroups (each drains a column range of every tile)
 constexpr int PR_NCH = PR_BN / 32;    // 32-column chunks per tile
+#ifdef FTK_PAIR_SETMAXNREG
+// register rebalancing (setmaxnreg, warpgroup-wide): the control warpgroup
+// (X producer, C producer, MMA, one idle warp) gives registers to the screen.
+// The pool is the CTA's launch allocation (threads x launch registers): the
+// three counts must satisfy 384 S + 128 R + 128 C <= 640 x 96, else the
+// increases wait forever.
+constexpr int PR_THREADS = 32 * (4 * PR_SWG + 8);
+#else
 constexpr int PR_THREADS = 32 * (4 * PR_SWG + 7);  // screen, 4 refine, X producer, C producer, MMA
+#endif
 // Warp roles.  The SMSP arbiter favours the highest warp id, so the
 // latency-critical single-thread roles (MMA issue, TMA producers) take the
 // top ids and are never starved by the screening warps.
@@ -159,6 +168,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     cluster_sync_all();  // barriers of both CTAs initialised before any remote use
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+#ifdef FTK_PAIR_SETMAXNREG
+    // warpgroup-uniform: the control warpgroup gives up registers here, the
+    // screen warpgroups take them at the top of their branch
+    if (warp >= W_REFINE0 + 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(FTK_PAIR_CTRL_REGS));
+#endif
 
     if (warp == W_PROD) {
         // ------------------------------------------------ TMA producer --
@@ -248,6 +262,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         }
     } else if (warp >= W_SCREEN0 && warp < W_SCREEN0 + 4 * PR_SWG) {
         // ----------------------------------------------------- screen --
+#ifdef FTK_PAIR_SETMAXNREG
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FTK_PAIR_SCREEN_REGS));
+#endif
         // Every warpgroup drains every accumulator tile: warpgroup wg takes
         // chunks [cb0, cb1) of the tile's PR_NCH 32-column chunks, so a TMEM
         // buffer is released after 1/PR_SWG of a tile's epilogue work.
@@ -449,6 +466,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         }
     } else if (warp >= W_REFINE0 && warp < W_REFINE0 + 4) {
         // ----------------------------------------------------- refine --
+#ifdef FTK_PAIR_SETMAXNREG
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(FTK_PAIR_REFINE_REGS));
+#endif
         const int quad = warp & 3;
         const int r = quad * 32 + lane;
         if (CHK && !SX) {

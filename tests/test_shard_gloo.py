@@ -109,13 +109,14 @@ def test_shard_bounds_aligned_and_covering():
 
 
 def _engine_run(x, c0, k, steps, dist=None, graph=False):
+    dt = x.dtype.type
     from paper_2408_01391_b200 import _engine as E
     from paper_2408_01391_b200.kmeans import LloydEngine
     from paper_2408_01391_b200.tiles import default_config
     from paper_2408_01391_b200.abft import Threshold
 
-    eng = LloydEngine(E.to_dev(x), c0, k, np.float32, default_config(np.float32), "abft",
-                      Threshold.default_for(np.float32), 8, dist=dist, graph=graph)
+    eng = LloydEngine(E.to_dev(x), c0, k, dt, default_config(dt), "abft",
+                      Threshold.default_for(dt), 8, dist=dist, graph=graph)
     hist = []
     for it in range(steps):
         inertia, _, moved = eng.step(it, more=(lambda it=it: it + 1 < steps))
@@ -126,23 +127,23 @@ def _engine_run(x, c0, k, steps, dist=None, graph=False):
     return labels, cent, hist, inertia
 
 
-def _engine_data():
+def _engine_data(dtype=np.float32):
     rng = np.random.default_rng(11)
     centers = rng.random((40, 24)) * 10
     lab = rng.integers(0, 40, 60_000)
-    x = (centers[lab] + 0.3 * rng.standard_normal((60_000, 24))).astype(np.float32)
+    x = (centers[lab] + 0.3 * rng.standard_normal((60_000, 24))).astype(dtype)
     c0 = np.ascontiguousarray(x[rng.choice(len(x), 40, replace=False)])
     return x, c0
 
 
-def _engine_worker(rank, port, backend, world, out):
+def _engine_worker(rank, port, backend, world, out, dtype_name="float32"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         from paper_2408_01391_b200.shard import ShardComm
 
-        x, c0 = _engine_data()
+        x, c0 = _engine_data(np.dtype(dtype_name).type)
         lo, hi = ShardComm.shard_bounds(len(x), world, rank)
         comm = ShardComm(lo)
         labels, cent, hist, inertia = _engine_run(x[lo:hi], c0, 40, 10, dist=comm,
@@ -157,8 +158,9 @@ def _cuda_ok():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("backend,world", [("gloo", 2), ("nccl", 1)])
-def test_sharded_engine_matches_single_process(backend, world):
+@pytest.mark.parametrize("backend,world,dtype_name", [("gloo", 2, "float32"), ("nccl", 1, "float32"),
+                                                      ("gloo", 2, "float64")])
+def test_sharded_engine_matches_single_process(backend, world, dtype_name):
     """LloydEngine(dist=ShardComm): gloo world 2 (eager steps, both ranks on
     cuda:0) and NCCL world 1 (the packed all-reduce captured in the step
     graphs) reproduce the single-process engine: labels identical,
@@ -166,12 +168,13 @@ def test_sharded_engine_matches_single_process(backend, world):
     (world 1)."""
     if not _cuda_ok():
         pytest.skip("needs a CUDA device")
-    x, c0 = _engine_data()
+    x, c0 = _engine_data(np.dtype(dtype_name).type)
     ref_lab, ref_c, ref_hist, ref_inertia = _engine_run(x, c0, 40, 10, graph=True)
     ctx = mp.get_context("spawn")
     with ctx.Manager() as mgr:
         out = mgr.dict()
-        mp.spawn(_engine_worker, args=(_free_port(), backend, world, out), nprocs=world, join=True)
+        mp.spawn(_engine_worker, args=(_free_port(), backend, world, out, dtype_name), nprocs=world,
+                 join=True)
         res = dict(out)
     labels = np.concatenate([res[r][1] for r in range(world)])
     assert np.array_equal(labels, ref_lab)
