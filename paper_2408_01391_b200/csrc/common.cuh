@@ -112,6 +112,7 @@ enum ScratchSlot {
     SLOT_TC64_C = 27,       // float64 via tf32: fp32 centroids, norms, bounds, counters
     SLOT_TC64_REC = 28,     // float64 via tf32: per-row (j1, T) records, fallback rows
     SLOT_TC64_G = 29,       // float64 via tf32: gathered uncertified rows (DMMA pass 2)
+    SLOT_TC64_P2 = 30,      // float64 via tf32: pass-2 thresholds, fp32 rows, candidates, keys
 };
 
 // ------------------------------------------------------- float helpers --

@@ -112,6 +112,51 @@ __global__ void tc64_prep_kernel(const double *y, const double *yn, int64_t k, i
     }
 }
 
+// Outputs of one row's float64 certificate (both refine kernels): certified
+// rows write the reference's (j1, d1); the rest are appended to fb with the
+// pass-2 candidate threshold thr = d1 + A + 2(B + 2^-20)(|d1| + A) (screen
+// units, rounded up): a centroid can beat d1 only if its screened value is
+// <= thr.  Rows with no usable screen (j1 < 0, non-finite d1) get -inf.
+__device__ __forceinline__ void t64_finish(int64_t row, int64_t m, int j, float T, double acc,
+                                           const double *yn, const float *a64, int32_t *out_idx,
+                                           double *out_val, int32_t *fb, unsigned *fb_count,
+                                           float *fb_thr) {
+    const int lane = threadIdx.x & 31;
+    bool need = false;
+    float thr = -INFINITY;
+    if (row < m) {
+        bool ok = false;
+        double dval = 0.0;
+        if (j >= 0) {
+            dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
+            ok = isfinite(dval) && double(T) > dval;
+        }
+        if (ok) {
+            out_idx[row] = j;
+            out_val[row] = dval;
+        } else if (j >= 0 && isfinite(dval) && a64) {
+            const double A = double(__ldg(a64 + row));
+            if (A >= 0.0) {
+                double t = dval + A + 2.0 * (double((0x1p-14 + 0x1p-22) * 1.01) + 0x1p-20) * (fabs(dval) + A);
+                t += fabs(t) * 0x1p-20;
+                thr = __double2float_ru(t);
+            }
+        }
+        need = !ok;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, need);
+    if (bal) {
+        unsigned b0 = 0;
+        if (lane == 0) b0 = atomicAdd(fb_count, unsigned(__popc(bal)));
+        b0 = __shfl_sync(0xffffffffu, b0, 0);
+        if (need) {
+            const unsigned pos = b0 + __popc(bal & ((1u << lane) - 1u));
+            fb[pos] = int32_t(row);
+            if (fb_thr) fb_thr[pos] = thr;
+        }
+    }
+}
+
 // Certify each screened row in float64: the reference's chain for the
 // winner, d1 < T.  One warp per 32-row tile, one lane per row; X streams in
 // 32-feature chunks: 16-byte coalesced loads (two rows per instruction) are
@@ -121,7 +166,7 @@ __global__ void tc64_prep_kernel(const double *y, const double *yn, int64_t k, i
 constexpr int R64_WARPS = 4, R64_LD = 34;  // row stride in doubles (16-byte aligned rows)
 __global__ void __launch_bounds__(32 * R64_WARPS) tc64_refine_kernel(
     const double *x, const double *y, const double *yn, int64_t m, int64_t d, const int2 *rec,
-    int32_t *out_idx, double *out_val, int32_t *fb, unsigned *fb_count) {
+    const float *a64, int32_t *out_idx, double *out_val, int32_t *fb, unsigned *fb_count, float *fb_thr) {
     __shared__ __align__(16) double sx[R64_WARPS][32 * R64_LD];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double *s = sx[w];
@@ -161,27 +206,7 @@ __global__ void __launch_bounds__(32 * R64_WARPS) tc64_refine_kernel(
             }
             __syncwarp();  // the tile buffer is refilled by the next chunk
         }
-        bool need = false;
-        if (row < m) {
-            bool ok = false;
-            double dval = 0.0;
-            if (j >= 0) {
-                dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
-                ok = isfinite(dval) && double(__int_as_float(r.y)) > dval;
-            }
-            if (ok) {
-                out_idx[row] = j;
-                out_val[row] = dval;
-            }
-            need = !ok;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, need);
-        if (bal) {
-            unsigned b0 = 0;
-            if (lane == 0) b0 = atomicAdd(fb_count, unsigned(__popc(bal)));
-            b0 = __shfl_sync(0xffffffffu, b0, 0);
-            if (need) fb[b0 + __popc(bal & ((1u << lane) - 1u))] = int32_t(row);
-        }
+        t64_finish(row, m, j, __int_as_float(r.y), acc, yn, a64, out_idx, out_val, fb, fb_count, fb_thr);
     }
 }
 
@@ -199,8 +224,8 @@ struct RtGeom {
 };
 __global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
     const __grid_constant__ CUtensorMap tmx, const double *y, const double *yn, int64_t m, int64_t d,
-    int nbox, const int2 *rec, int32_t *out_idx, double *out_val, int32_t *fb,
-    unsigned *fb_count) {
+    int nbox, const int2 *rec, const float *a64, int32_t *out_idx, double *out_val, int32_t *fb,
+    unsigned *fb_count, float *fb_thr) {
     extern __shared__ __align__(1024) unsigned char rt_raw[];
     unsigned char *smem = rt_raw + ((1024u - (smem_u32(rt_raw) & 1023u)) & 1023u);
     constexpr int stages = RT_CONS;  // slot w belongs to consumer w
@@ -293,27 +318,7 @@ __global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
-        bool need = false;
-        if (row < m) {
-            bool ok = false;
-            double dval = 0.0;
-            if (j >= 0) {
-                dval = __dsub_rn(__ldg(yn + j), __dadd_rn(acc, acc));
-                ok = isfinite(dval) && double(__int_as_float(r.y)) > dval;
-            }
-            if (ok) {
-                out_idx[row] = j;
-                out_val[row] = dval;
-            }
-            need = !ok;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, need);
-        if (bal) {
-            unsigned b0 = 0;
-            if (lane == 0) b0 = atomicAdd(fb_count, unsigned(__popc(bal)));
-            b0 = __shfl_sync(0xffffffffu, b0, 0);
-            if (need) fb[b0 + __popc(bal & ((1u << lane) - 1u))] = int32_t(row);
-        }
+        t64_finish(row, m, j, __int_as_float(r.y), acc, yn, a64, out_idx, out_val, fb, fb_count, fb_thr);
     }
 }
 
@@ -331,6 +336,99 @@ __global__ void tc64_scatter_kernel(const int32_t *rows, const unsigned *count, 
          q += int64_t(gridDim.x) * blockDim.x) {
         out_idx[rows[q]] = idx[q];
         out_val[rows[q]] = val[q];
+    }
+}
+
+// ---------------------------------------------- pass 2 (candidates) -----
+// The rows the float64 certificate left open: their fp32 rows are re-screened
+// (CTA-pair COLLECT mode) against their own threshold, and every centroid
+// that can still beat the row's exact d1 is evaluated in float64 in the
+// reference's order; the row's result is the smallest value, then the
+// smallest index (the reference's first strict minimum).
+__device__ __forceinline__ unsigned long long ord64(double v) {
+    const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+    return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unord64(unsigned long long k) {
+    const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double(static_cast<long long>(u));
+}
+
+__global__ void t64p2_gather_kernel(const float *x32, int64_t d, const int32_t *rows, const unsigned *count,
+                                    float *g, unsigned *row_cnt, unsigned long long *key, int32_t *kidx) {
+    const unsigned n = *count;
+    const int64_t tot = int64_t(n) * d;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t q = e / d, f = e % d;
+        g[e] = x32[int64_t(rows[q]) * d + f];
+        if (f == 0) {
+            row_cnt[q] = 0u;
+            key[q] = ~0ull;
+            kidx[q] = 0x7FFFFFFF;
+        }
+    }
+}
+
+// one thread per candidate (gathered row q, centroid j): the exact value
+__global__ void t64p2_value_kernel(const double *x, const double *y, const double *yn, int64_t d,
+                                   const int32_t *rows, const int2 *cand, const unsigned *count, unsigned cap,
+                                   const unsigned *row_cnt, unsigned row_cap, double *cval,
+                                   unsigned long long *key) {
+    const unsigned n = min(*count, cap);
+    for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        const int2 e = cand[c];
+        if (row_cnt[e.x] > row_cap) continue;
+        const double *xr = x + int64_t(rows[e.x]) * d;
+        const double *cr = y + int64_t(e.y) * d;
+        double acc = 0.0;
+        int64_t f = 0;
+        if ((d & 1) == 0) {
+            const double2 *x2 = reinterpret_cast<const double2 *>(xr);
+            const double2 *c2 = reinterpret_cast<const double2 *>(cr);
+            for (; f < d / 2; ++f) {
+                const double2 a = __ldg(x2 + f), b = __ldg(c2 + f);
+                acc = __dadd_rn(acc, __dmul_rn(a.x, b.x));
+                acc = __dadd_rn(acc, __dmul_rn(a.y, b.y));
+            }
+        } else {
+            for (; f < d; ++f) acc = __dadd_rn(acc, __dmul_rn(__ldg(xr + f), __ldg(cr + f)));
+        }
+        const double v = __dsub_rn(__ldg(yn + e.y), __dadd_rn(acc, acc));
+        cval[c] = v;
+        if (v < INFINITY) atomicMin(key + e.x, ord64(v));
+    }
+}
+
+// the smallest index among the candidates holding the row's minimum
+__global__ void t64p2_index_kernel(const int2 *cand, const unsigned *count, unsigned cap, const unsigned *row_cnt,
+                                   unsigned row_cap, const double *cval, const unsigned long long *key,
+                                   int32_t *kidx) {
+    const unsigned n = min(*count, cap);
+    for (unsigned c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+        const int2 e = cand[c];
+        if (row_cnt[e.x] > row_cap) continue;
+        const double v = cval[c];
+        if (v < INFINITY && ord64(v) == key[e.x]) atomicMin(kidx + e.x, e.y);
+    }
+}
+
+// resolved rows write their outputs; the rest (no screen, too many
+// candidates, list overflow) go on to the DMMA screen
+__global__ void t64p2_finalize_kernel(const int32_t *rows, const unsigned *n_rows, const unsigned *row_cnt,
+                                      unsigned row_cap, const unsigned *count, unsigned cap,
+                                      const unsigned long long *key, const int32_t *kidx, int32_t *out_idx,
+                                      double *out_val, int32_t *rows2, unsigned *n2) {
+    const unsigned n = *n_rows;
+    const bool over = *count > cap;
+    for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < n; q += gridDim.x * blockDim.x) {
+        const int32_t row = rows[q];
+        if (over || row_cnt[q] > row_cap || key[q] == ~0ull) {
+            rows2[atomicAdd(n2, 1u)] = row;
+            continue;
+        }
+        out_idx[row] = kidx[q];
+        out_val[row] = unord64(key[q]);
     }
 }
 
@@ -383,10 +481,14 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     tc64_prep_kernel<<<unsigned(std::min<int64_t>((k + 7) / 8, 296)), 256, 0, st>>>(y, yn, k, d, c32, yn32,
                                                                                      bounds);
     FTK_LAUNCHED("tc64_prep_kernel");
-    char *rb = static_cast<char *>(scratch(ctx, SLOT_TC64_REC, sizeof(int2) * size_t(m) + sizeof(int32_t) * size_t(m + 1) + 64, st));
+    char *rb = static_cast<char *>(scratch(ctx, SLOT_TC64_REC, sizeof(int2) * size_t(m) + sizeof(int32_t) * size_t(m + 1) +
+                                                                   2 * sizeof(float) * size_t(m + 1) + 64, st));
     if (!rb) return FTK_ERR_CUDA;
     int2 *rec = reinterpret_cast<int2 *>(rb);
     int32_t *fb = reinterpret_cast<int32_t *>(rec + m);
+    float *a64 = reinterpret_cast<float *>(fb + (m + 1));   // per-row screen bound
+    float *fb_thr = a64 + (m + 1);                          // per uncertified row: pass-2 threshold
+    const bool p2 = !getenv("FTK_T64_NO_P2");
 
     const int nkb = int((d + T64_KB - 1) / T64_KB);
     PairParams Q{};
@@ -403,6 +505,7 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     Q.fb_count = cnt;
     Q.rowinfo = info;
     Q.rec64 = rec;
+    Q.a64 = p2 ? a64 : nullptr;
     constexpr unsigned kFlagCap = 4096;
     double4 *flag_rec = nullptr;
     float *csum = nullptr, *camax = nullptr, *csumw = nullptr;
@@ -439,12 +542,14 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
                                           int(smem)));
             const int64_t ntile = (m + 31) / 32;
             tc64_refine_tma_kernel<<<unsigned(std::min<int64_t>(ntile, int64_t(148) * per_sm)),
-                                     32 * (RT_CONS + 1), smem, st>>>(tx, y, yn, m, d, nbox, rec, out_idx,
-                                                                     out_val, fb, cnt);
+                                     32 * (RT_CONS + 1), smem, st>>>(tx, y, yn, m, d, nbox, rec,
+                                                                     p2 ? a64 : nullptr, out_idx, out_val,
+                                                                     fb, cnt, p2 ? fb_thr : nullptr);
             FTK_LAUNCHED("tc64_refine_tma_kernel");
         } else {
             tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 32 * R64_WARPS - 1) / (32 * R64_WARPS), 148 * 6)),
-                                 32 * R64_WARPS, 0, st>>>(x, y, yn, m, d, rec, out_idx, out_val, fb, cnt);
+                                 32 * R64_WARPS, 0, st>>>(x, y, yn, m, d, rec, p2 ? a64 : nullptr, out_idx,
+                                                          out_val, fb, cnt, p2 ? fb_thr : nullptr);
             FTK_LAUNCHED("tc64_refine_kernel");
         }
     }
@@ -474,16 +579,69 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     ctx->last_fb[0] = h[0];
     ctx->last_fb[1] = 0;
     ctx->last_fb[2] = h[2];
-    if (h[0] > 0) {
-        // uncertified rows: the DMMA screen (checked like the pass) over the gathered rows
-        const unsigned n = h[0];
+    int32_t *dm_rows = fb;        // rows for the DMMA screen
+    const unsigned *dm_cnt = cnt;
+    unsigned n_dm = h[0];
+    if (h[0] > 0 && p2) {
+        // pass 2: COLLECT re-screen of the uncertified rows' fp32 copies, float64
+        // evaluation of every candidate that can still beat the row's d1
+        const unsigned n1 = h[0];
+        const unsigned row_cap = 256;
+        const unsigned cap = unsigned(std::min<int64_t>(int64_t(n1) * 16 + 65536, int64_t(1) << 30));
+        const size_t gbytes = (sizeof(float) * size_t(n1) * d + 255) & ~size_t(255);
+        const size_t need = gbytes + sizeof(int2) * cap + sizeof(double) * cap + 8 * size_t(n1) +
+                            4 * size_t(n1) * 3 + 256;
+        char *b2 = static_cast<char *>(scratch(ctx, SLOT_TC64_P2, need, st));
+        if (!b2) return FTK_ERR_CUDA;
+        float *g32 = reinterpret_cast<float *>(b2);
+        int2 *cand = reinterpret_cast<int2 *>(b2 + gbytes);
+        double *cval = reinterpret_cast<double *>(cand + cap);
+        unsigned long long *key = reinterpret_cast<unsigned long long *>(cval + cap);
+        int32_t *kidx = reinterpret_cast<int32_t *>(key + n1);
+        unsigned *row_cnt = reinterpret_cast<unsigned *>(kidx + n1);
+        int32_t *rows2 = reinterpret_cast<int32_t *>(row_cnt + n1);
+        unsigned *cc = cnt + 8;  // [0] candidates, [1] rows for the DMMA screen
+        FTK_CUDA(cudaMemsetAsync(cc, 0, 2 * sizeof(unsigned), st));
+        t64p2_gather_kernel<<<148 * 4, 256, 0, st>>>(x32, d, fb, cnt, g32, row_cnt, key, kidx);
+        FTK_LAUNCHED("t64p2_gather_kernel");
+        CUtensorMap mg, mc2;
+        if ((rc = make_tc_map(&mg, g32, n1, d, 128)) || (rc = make_tc_map(&mc2, c32, k, d, PAIR_BN / 2)))
+            return rc;
+        PairParams R{};
+        R.x = g32; R.y = c32; R.yn = yn32; R.m = n1; R.k = k; R.d = d;
+        R.cmax2 = bounds;
+        R.ecmax2 = bounds + 1;
+        R.thr = fb_thr;
+        R.cand = cand;
+        R.cand_count = cc;
+        R.cand_cap = cap;
+        R.row_cnt = row_cnt;
+        if ((rc = pair_screen_launch(mg, mc2, R, false, st))) return rc;
+        t64p2_value_kernel<<<148 * 8, 256, 0, st>>>(x, y, yn, d, fb, cand, cc, cap, row_cnt, row_cap, cval, key);
+        FTK_LAUNCHED("t64p2_value_kernel");
+        t64p2_index_kernel<<<148 * 4, 256, 0, st>>>(cand, cc, cap, row_cnt, row_cap, cval, key, kidx);
+        FTK_LAUNCHED("t64p2_index_kernel");
+        t64p2_finalize_kernel<<<148, 256, 0, st>>>(fb, cnt, row_cnt, row_cap, cc, cap, key, kidx, out_idx, out_val,
+                                                   rows2, cc + 1);
+        FTK_LAUNCHED("t64p2_finalize_kernel");
+        unsigned h2 = 0;
+        FTK_CUDA(cudaMemcpyAsync(&h2, cc + 1, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        FTK_CUDA(cudaStreamSynchronize(st));
+        dm_rows = rows2;
+        dm_cnt = cc + 1;
+        n_dm = h2;
+        ctx->last_fb[1] = h2;
+    }
+    if (n_dm > 0) {
+        // rows left: the DMMA screen (checked like the pass) over the gathered rows
+        const unsigned n = n_dm;
         const size_t gb = (sizeof(double) * size_t(n) * d + 255) & ~size_t(255);
         char *g = static_cast<char *>(scratch(ctx, SLOT_TC64_G, gb + (sizeof(double) + sizeof(int32_t)) * size_t(n) + 64, st));
         if (!g) return FTK_ERR_CUDA;
         double *gx = reinterpret_cast<double *>(g);
         double *gv = reinterpret_cast<double *>(g + gb);
         int32_t *gi = reinterpret_cast<int32_t *>(gv + n);
-        tc64_gather_kernel<<<148 * 4, 256, 0, st>>>(x, d, fb, cnt, gx);
+        tc64_gather_kernel<<<148 * 4, 256, 0, st>>>(x, d, dm_rows, dm_cnt, gx);
         FTK_LAUNCHED("tc64_gather_kernel");
         TcFt ft2{};
         if (ft) {
@@ -496,7 +654,7 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
         rc = dscreen_run(ctx, gx, y, yn, n, k, d, gi, gv, ft ? &ft2 : nullptr, st);
         ctx->family = fam;
         if (rc) return rc;
-        tc64_scatter_kernel<<<148, 256, 0, st>>>(fb, cnt, gi, gv, out_idx, out_val);
+        tc64_scatter_kernel<<<148, 256, 0, st>>>(dm_rows, dm_cnt, gi, gv, out_idx, out_val);
         FTK_LAUNCHED("tc64_scatter_kernel");
     }
     if (ft && ft->inj && ft->inj->n > 0)

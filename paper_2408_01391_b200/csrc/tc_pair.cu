@@ -686,6 +686,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     const float T = m2 - A - P.b_coef * fabsf(m2) - 0x1p-21f * (fabsf(m1) + fabsf(m2));
                     const bool good = !abft_bad && xn * cm < 1e36f && isfinite(T) && isfinite(m1);
                     P.rec64[grow] = make_int2(good ? j : -1, __float_as_int(T));
+                    if (P.a64) P.a64[grow] = good ? A : -1.0f;  // the screen bound (pass-2 threshold)
                 }
                 // magnitudes far from overflow: the screen saw every column finite
                 const bool sane = !F64 && xn * cm < 1e36f && isfinite(dval);

@@ -61,6 +61,7 @@ struct PairParams {
     // value d1 < T); j1 = -1 when the row is not screenable (checksum flag,
     // non-finite).  The refine then skips the fp32 exact chain.
     int2 *rec64;
+    float *a64;   // optional: per-row screen bound A (the float64 pass-2 candidate threshold)
     float a_abs;  // extra absolute screen error (the fp32 rounding of float64 norms)
     long long *clk;  // debug: per-role clock64 sums (screen busy/wait, MMA waits), or null
     int dbg;  // bit 0: skip the screen math, bit 1: skip the refine (pipeline timing only)
