@@ -119,3 +119,19 @@ def test_tc64_lloyd_matches_oracle(pair64):
     assert res.centroids.tobytes() == ref["centroids"].tobytes()
     assert res.inertia == ref["inertia"]
     assert res.iters == ref["iters"]
+
+
+def test_tc64_candidate_overflow_goes_to_dmma(pair64):
+    """Rows whose pass-2 candidate set exceeds its cap (300 identical
+    centroids tie for every row) fall through to the DMMA screen; rows with a
+    few close centroids are resolved by the float64 candidate pass."""
+    rng = np.random.default_rng(12)
+    base = rng.standard_normal((1, 64))
+    y = np.ascontiguousarray(np.vstack([np.repeat(base, 300, axis=0), rng.standard_normal((20, 64)) * 5]))
+    x = np.ascontiguousarray(np.vstack([base + 1e-3 * rng.standard_normal((700, 64)),
+                                        y[300:310] + 1e-9 * rng.standard_normal((10, 64))]))
+    r = P.fused_assign(x, y)
+    lab, val = O.assign(x, y)
+    assert np.array_equal(r.assignments, lab)
+    assert r.min_dists.tobytes() == val.tobytes()
+    assert E.tc_fallback_rows()[1] > 0  # rows reached the DMMA screen
