@@ -9,6 +9,8 @@
 // queues the DMA; the next chunk's memcpy overlaps that DMA.  The caller's
 // stream then waits on every thread's last DMA, so work queued after the
 // upload is ordered behind it without a host synchronisation.
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -18,24 +20,23 @@
 namespace ftk {
 
 struct H2DStage {
-    static constexpr int T = 6;                    // copy threads
+    static constexpr int T = 16;                   // max copy threads (FTK_H2D_THREADS, default 6)
     static constexpr size_t CH = size_t(8) << 20;  // bytes per chunk
     void *buf[T][2] = {};
     cudaEvent_t ev[T][2] = {};
     cudaStream_t st[T] = {};
-    bool ready = false;
+    int ready = 0;  // threads whose buffers, events and stream exist
 };
 
-static int stage_init(H2DStage &S) {
-    if (S.ready) return FTK_OK;
-    for (int t = 0; t < H2DStage::T; ++t) {
+static int stage_init(H2DStage &S, int nt) {
+    for (int t = S.ready; t < nt; ++t) {
         FTK_CUDA(cudaStreamCreateWithFlags(&S.st[t], cudaStreamNonBlocking));
         for (int b = 0; b < 2; ++b) {
             FTK_CUDA(cudaHostAlloc(&S.buf[t][b], H2DStage::CH, cudaHostAllocDefault));
             FTK_CUDA(cudaEventCreateWithFlags(&S.ev[t][b], cudaEventDisableTiming));
         }
+        S.ready = t + 1;
     }
-    S.ready = true;
     return FTK_OK;
 }
 
@@ -56,13 +57,15 @@ int h2d_pageable_run(ftk_ctx *ctx, void *dst, const void *src, size_t n, cudaStr
     if (n == 0) return FTK_OK;
     if (!ctx->h2d) ctx->h2d = new H2DStage();
     H2DStage &S = *static_cast<H2DStage *>(ctx->h2d);
-    if (int rc = stage_init(S)) return rc;
+    int want = 6;
+    if (const char *e = getenv("FTK_H2D_THREADS")) want = std::max(1, std::min(H2DStage::T, atoi(e)));
     // the upload may overwrite memory the caller's stream still reads
     cudaEvent_t start;
     FTK_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
     FTK_CUDA(cudaEventRecord(start, st));
     const size_t nch = (n + H2DStage::CH - 1) / H2DStage::CH;
-    const int nt = int(std::min<size_t>(H2DStage::T, nch));
+    const int nt = int(std::min<size_t>(size_t(want), nch));
+    if (int rc = stage_init(S, nt)) return rc;
     std::vector<int> rc(nt, FTK_OK);
     std::vector<std::string> err(nt);
     auto work = [&](int t) {
