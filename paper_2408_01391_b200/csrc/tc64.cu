@@ -506,6 +506,7 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
     Q.rowinfo = info;
     Q.rec64 = rec;
     Q.a64 = p2 ? a64 : nullptr;
+    if (const char *e = getenv("FTK_TC_DEBUG")) Q.dbg = atoi(e);  // timing probe (results invalid)
     constexpr unsigned kFlagCap = 4096;
     double4 *flag_rec = nullptr;
     float *csum = nullptr, *camax = nullptr, *csumw = nullptr;
