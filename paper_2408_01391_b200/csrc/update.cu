@@ -450,7 +450,13 @@ __global__ void __launch_bounds__(32 * CH_WARPS) chain_pipe_kernel(
 #define FTK_CS_LOADERS 7
 #define FTK_CS_NG 8
 #endif
-constexpr int CS_GS = 16, CS_NG = FTK_CS_NG, CS_LOADERS = FTK_CS_LOADERS;
+#ifndef FTK_CS_GS
+#define FTK_CS_GS 16
+#endif
+constexpr int CS_GS = FTK_CS_GS, CS_NG = FTK_CS_NG, CS_LOADERS = FTK_CS_LOADERS;
+// a loader's next group reuses a slot at most one phase ahead only if there
+// are more slots than loaders (parity waits cannot tell phases two apart)
+static_assert(CS_LOADERS < CS_NG, "chain ring needs more slots than loader warps");
 
 __device__ __forceinline__ void cs_cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
