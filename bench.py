@@ -360,6 +360,7 @@ def run_ours(args, rank, world):
         return float(t.item())
 
     step_stats = []
+    upd_ms = []
 
     def time_steps(eng, steps, warmup):
         """W warm-up steps, one eager step (phase timings + the screen's own
@@ -370,6 +371,7 @@ def run_ours(args, rank, world):
             eng.step(it)
         eng.step(warmup, eager=True)
         a_ms, k_ms = eng.assign_ms, E.tc_last_kernel_ms()
+        upd_ms.append(eng.update_ms)  # the update phase of the eager step (CUDA events)
         eng.warm_graphs(warmup + 1)
         barrier()
         evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
@@ -528,6 +530,7 @@ def run_ours(args, rank, world):
         e_d.close()
         del e_a, e_d
 
+    B_u = (hi - lo) * DIM * 4 + (hi - lo) * 8 + K * DIM * 8 + K * 8
     kern_ms = k_ft if k_ft else a_ft
     achieved = flops / (kern_ms * 1e-3) / 1e12
     traffic = None
@@ -604,6 +607,11 @@ def run_ours(args, rank, world):
                      "traffic_note": "dram read+write bytes per launch, ncu --set full "
                                      "(profiles/traffic.json)"},
         "assign_ms": a_ft, "assign_tflops": flops / (a_ft * 1e-3) / 1e12,
+        "update_roofline": {"bound": "hbm", "unit": "GB/s", "peak": hbm, "ms": upd_ms[-1],
+                            "bytes": B_u, "achieved": B_u / (upd_ms[-1] * 1e-3) / 1e9,
+                            "frac": B_u / (upd_ms[-1] * 1e-3) / 1e9 / hbm,
+                            "note": "SURVEY 8(d) B_u = N*D*s + N*8 + K*D*8 + K*8 over the whole update phase "
+                                    "(sort, certified segment sums, fold, finalize) of one eager step"},
         "ft_off_kernel_ms": k_off, "ft_off_ms_per_step": ms_off,
         "ft_overhead_pct": 100.0 * (ms_ft / ms_off - 1.0),
         "faults": {"injected": injected, "detections": rep.detections,
