@@ -135,3 +135,28 @@ def test_tc64_candidate_overflow_goes_to_dmma(pair64):
     assert np.array_equal(r.assignments, lab)
     assert r.min_dists.tobytes() == val.tobytes()
     assert E.tc_fallback_rows()[1] > 0  # rows reached the DMMA screen
+
+
+@pytest.mark.parametrize("m,d,k", [(70000, 4, 1), (66000, 8, 5), (70000, 6, 33), (70000, 300, 40)])
+def test_tc64_auto_edge_shapes(m, d, k):
+    """The default family choice for float64 at edge shapes (k = 1, tiny d,
+    d % 4 != 0 and d > 256 -- the last two outside the tf32 path) stays
+    bit-exact."""
+    rng = np.random.default_rng(m + d + k)
+    x = np.ascontiguousarray(rng.standard_normal((m, d)) * 2.0)
+    y = np.ascontiguousarray(x[rng.choice(m, k, replace=False)] + 0.01)
+    r = P.fused_assign(x, y)
+    lab, val = O.assign(x, y)
+    assert np.array_equal(r.assignments, lab)
+    assert r.min_dists.tobytes() == val.tobytes()
+
+
+def test_tc64_estimator_fit_matches_oracle():
+    """FTKMeans on float64 data (default variant selection, ABFT) against the
+    oracle's restatement of the reference lloyd."""
+    x, _ = _blobs(90000, 32, 64, seed=21)
+    km = P.FTKMeans(n_clusters=64, init="random-sample", max_iter=6, random_state=3, ft_mode="abft").fit(x)
+    ref = O.lloyd(x, 64, max_iters=6, seed=3, init="random-sample", ft_mode="abft")
+    assert np.array_equal(km.labels_, ref["assignments"])
+    assert km.cluster_centers_.tobytes() == ref["centroids"].tobytes()
+    assert km.inertia_ == ref["inertia"]
