@@ -104,6 +104,9 @@ __device__ __forceinline__ uint32_t ordered_key(float f) {
 // F64: float64 data screened from its fp32 copy; the refine records (j1, T)
 // for the float64 refine (tc.cu tc64_refine_kernel) instead of running the
 // fp32 exact chain.
+#ifndef FTK_PAIR_COLLECT_SPLIT
+#define FTK_PAIR_COLLECT_SPLIT 1  // pass 2: one work item per (row pair-tile, column tile)
+#endif
 template <bool CHK, bool COLLECT, bool INJ, bool SX, bool F64 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     pair_screen_kernel(const __grid_constant__ CUtensorMap tmX,
@@ -139,6 +142,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     // on the host (pass 2 over the rows pass 1 left uncertified)
     const int64_t M = P.m_dev ? (int64_t(*P.m_dev) < P.m ? int64_t(*P.m_dev) : P.m) : P.m;
     const int64_t npt = (M + 2 * PR_BM - 1) / (2 * PR_BM);  // row pair-tiles
+    // work items: a row pair-tile with all its column tiles, or (COLLECT: the
+    // few rows of pass 2) one column tile, so pass 2 spreads over every SM
+    const bool csplit = COLLECT && FTK_PAIR_COLLECT_SPLIT;
+    const int TPS = csplit ? P.ntiles : 1;   // items per row pair-tile
+    const int TPW = csplit ? 1 : P.ntiles;   // column tiles per item
+    const int64_t nwi = npt * TPS;
     const int64_t pt0 = cluster_id_x(), pstride = ncluster_x();
 
     if (warp == W_PROD && lane == 0) {
@@ -180,9 +189,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+            for (int64_t wi = pt0; wi < nwi; wi += pstride, ++it) {
+                const int64_t pt = wi / TPS;
+                const int tb = int(wi % TPS) * TPW, te = tb + TPW < P.ntiles ? tb + TPW : P.ntiles;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
-                for (int t = 0; t < P.ntiles; ++t) {
+                for (int t = tb; t < te; ++t) {
                     const int c0 = t * PR_BN + int(rank) * (PR_BN / 2);
                     for (int kb = 0; kb < nkb; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
@@ -206,7 +217,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             uint32_t phase = 0;
             uint32_t g = 0;
             int it = 0;
-            for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+            for (int64_t wi = pt0; wi < nwi; wi += pstride, ++it) {
+                const int64_t pt = wi / TPS;
+                const int tb = int(wi % TPS) * TPW, te = tb + TPW < P.ntiles ? tb + TPW : P.ntiles;
                 const int ab = SX ? 0 : it % NA;
                 if (!SX) {
                     PROBE_T(c0_);
@@ -215,7 +228,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 }
                 tc_fence_after();
                 const uint32_t a_base = smem_u32(sA) + uint32_t(ab) * A_BYTES;
-                for (int t = 0; t < P.ntiles; ++t, ++g) {
+                for (int t = tb; t < te; ++t, ++g) {
                     const int buf = g % PR_NBUF;
                     { PROBE_T(c0_); mbar_wait(&t_empty[buf], ((g / PR_NBUF) & 1) ^ 1); PROBE_ADD(2, clock64() - c0_); }
                     tc_fence_after();
@@ -243,7 +256,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         if (lane == 0 && !SX) {
             int it = 0;
             const uint32_t lead = mapa_shared(smem_u32(&a_full[0]), 0);
-            for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+            for (int64_t wi = pt0; wi < nwi; wi += pstride, ++it) {
+                const int64_t pt = wi / TPS;
+                const int tb = int(wi % TPS) * TPW, te = tb + TPW < P.ntiles ? tb + TPW : P.ntiles;
                 const int ab = it % NA;
                 unsigned char *a_dst = sA + size_t(ab) * A_BYTES;
                 const int row0 = int(pt * 2 * PR_BM + rank * PR_BM);
@@ -286,9 +301,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         const int et = (warp - W_SCREEN0) * 32 + lane;  // 0..255
         float *ywarp = yns + cbeg;          // reads: ywarp + ybuf * PR_BN
         int ybuf = 0;
-        if (et < PR_BN) yns[et] = et < P.k ? __ldg(P.yn + et) : INFINITY;
+        {
+            const int64_t c = int64_t((pt0 % TPS) * TPW) * PR_BN + et;  // the first item's first tile
+            if (et < PR_BN) yns[et] = c < P.k ? __ldg(P.yn + c) : INFINITY;
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(128 * PR_SWG) : "memory");
-        for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+        for (int64_t wi = pt0; wi < nwi; wi += pstride, ++it) {
+                const int64_t pt = wi / TPS;
+                const int tb = int(wi % TPS) * TPW, te = tb + TPW < P.ntiles ? tb + TPW : P.ntiles;
             const int pb = it & 1;
             const int64_t grow = pt * 2 * PR_BM + int64_t(rank) * PR_BM + r;
             float m1 = INFINITY, m2 = INFINITY;
@@ -305,11 +325,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     inj_a = P.inj_after[grow];
                 }
             }
-            for (int t = 0; t < P.ntiles; ++t, ++g) {
+            for (int t = tb; t < te; ++t, ++g) {
                 const int buf = g % PR_NBUF;
                 const int64_t c0 = int64_t(t) * PR_BN + cbeg;  // first column of this warpgroup's range
                 // prefetch the next tile's norms (wrapping into the next row tile)
-                const int64_t cn = int64_t((t + 1) % P.ntiles) * PR_BN + et;
+                const int tn = t + 1 < te ? t + 1 : int(((wi + pstride) % TPS) * TPW);  // next item's first tile
+                const int64_t cn = int64_t(tn) * PR_BN + et;
                 const float yn_next = (et < PR_BN && cn < P.k) ? __ldg(P.yn + cn) : INFINITY;
                 PROBE_T(cw_); mbar_wait(&t_full[buf], (g / PR_NBUF) & 1); PROBE_T(cb_); PROBE_ADD(1, cb_ - cw_);
                 tc_fence_after();
@@ -519,7 +540,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
         const float k_camax0 = (F64 && CHK && !COLLECT) ? P.camax[0] : 0.0f;
         const float k_camax2 = (F64 && CHK && !COLLECT) ? P.camax[2] : 0.0f;
         int it = 0;
-        for (int64_t pt = pt0; pt < npt; pt += pstride, ++it) {
+        for (int64_t wi = pt0; wi < nwi; wi += pstride, ++it) {
+                const int64_t pt = wi / TPS;
+                const int tb = int(wi % TPS) * TPW, te = tb + TPW < P.ntiles ? tb + TPW : P.ntiles;
             const int pb = it & 1;
             const int ab = SX ? 0 : it % NA;
             PROBE_T(rw0_);
@@ -550,7 +573,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             const int pjv = pj;  // the prefetched centroid (cA / cB are clobbered below)
             pj = -1;
             const float4 ri_cur = ri_next;
-            if (F64) ri_next = load_info(pt + pstride);
+            if (F64) ri_next = load_info((wi + pstride) / TPS);
             if (!SX) mbar_wait(&a_full[ab], uint32_t(it / NA) & 1);  // own X half resident + visible
             const unsigned char *sAt = sA + size_t(ab) * A_BYTES + uint32_t(r) * 128;
             bool ok = false;
@@ -660,7 +683,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     }
                 }
                 released = true;
-                prefetch(pt + pstride);  // the next row tile's hinted centroids, k-blocks 0 and 1
+                prefetch((wi + pstride) / TPS);  // the next row tile's hinted centroids, k-blocks 0 and 1
                 PROBE_T(lp1_);
                 PROBE_ADD(8, lp1_ - lp0_);
               if (active) {  // lanes without a live row only helped with the loads
@@ -811,7 +834,8 @@ int pair_screen_launch(const CUtensorMap &mx, const CUtensorMap &mc, PairParams 
     if (npt == 0) return FTK_OK;
     int nsm = 148;
     nsm = current_sm_count();
-    const int64_t ncl = npt < nsm / 2 ? npt : nsm / 2;
+    const int64_t nwork = (P.thr && FTK_PAIR_COLLECT_SPLIT) ? npt * P.ntiles : npt;  // COLLECT: one item per (row tile, column tile)
+    const int64_t ncl = nwork < nsm / 2 ? nwork : nsm / 2;
     if (P.rec64) {  // float64 data, fp32 copy resident (d <= 256)
         if (sx) {
             set_error("tc pair f64: d > 256");
