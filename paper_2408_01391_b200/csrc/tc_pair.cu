@@ -885,7 +885,33 @@ __global__ void cand_exact_kernel(const float *g, const float *y, const float *y
         const float *cr = y + int64_t(e.y) * d;
         float acc = 0.0f;
         int64_t f = 0;
-        if ((d & 3) == 0) {
+        if ((d & 31) == 0 && ((reinterpret_cast<uintptr_t>(xr) | reinterpret_cast<uintptr_t>(cr)) & 15) == 0) {
+            // the chain is sequential (the reference's order); the loads are
+            // not: 8-vector batches, the next batch in flight while the
+            // current one is chained (one L2 round trip per 32 features
+            // instead of one per 4)
+            const float4 *x4 = reinterpret_cast<const float4 *>(xr);
+            const float4 *c4 = reinterpret_cast<const float4 *>(cr);
+            const int64_t nb = d / 32;
+            float4 xa[8], ca[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) { xa[u] = __ldg(x4 + u); ca[u] = __ldg(c4 + u); }
+            for (int64_t b = 0; b < nb; ++b) {
+                float4 xn[8], cn[8];
+                const int64_t o = (b + 1 < nb ? b + 1 : b) * 8;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { xn[u] = __ldg(x4 + o + u); cn[u] = __ldg(c4 + o + u); }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    acc = __fadd_rn(acc, __fmul_rn(xa[u].x, ca[u].x));
+                    acc = __fadd_rn(acc, __fmul_rn(xa[u].y, ca[u].y));
+                    acc = __fadd_rn(acc, __fmul_rn(xa[u].z, ca[u].z));
+                    acc = __fadd_rn(acc, __fmul_rn(xa[u].w, ca[u].w));
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { xa[u] = xn[u]; ca[u] = cn[u]; }
+            }
+        } else if ((d & 3) == 0) {
             const float4 *x4 = reinterpret_cast<const float4 *>(xr);
             const float4 *c4 = reinterpret_cast<const float4 *>(cr);
             for (; f < d / 4; ++f) {
@@ -940,12 +966,23 @@ __global__ void pass2_gather_kernel(const float *x, int64_t d, const int32_t *ro
                                     const unsigned long long *seed, float *g,
                                     unsigned long long *key, unsigned *row_cnt) {
     const unsigned n = min(*count, cap_rows);
-    const int64_t tot = int64_t(n) * d;
-    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < tot;
-         e += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t q = e / d, f = e % d;
-        g[e] = x[int64_t(rows[q]) * d + f];
-        if (f == 0) {
+    // one warp per row (16-byte copies when the rows are aligned): no
+    // per-element 64-bit division
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    const bool v4 = (d & 3) == 0 && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(g)) & 15) == 0;
+    for (int64_t q = w0; q < n; q += nw) {
+        const float *src = x + int64_t(rows[q]) * d;
+        float *dst = g + q * d;
+        if (v4) {
+            const float4 *s4 = reinterpret_cast<const float4 *>(src);
+            float4 *d4 = reinterpret_cast<float4 *>(dst);
+            for (int64_t f = lane; f < d / 4; f += 32) d4[f] = __ldg(s4 + f);
+        } else {
+            for (int64_t f = lane; f < d; f += 32) dst[f] = __ldg(src + f);
+        }
+        if (lane == 0) {
             key[q] = seed[q];
             row_cnt[q] = 0u;
         }

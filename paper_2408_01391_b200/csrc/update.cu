@@ -251,8 +251,11 @@ __device__ void block_exclusive_scan(F val, int64_t k, int64_t *out) {
 constexpr int SEG_MEMBERS = 256;  // == SEG (segment length of the certified update)
 
 __global__ void offsets_segs_kernel(const int64_t *counts, int64_t k, int64_t *offsets,
-                                    int64_t *seg_base, int32_t *seg_cl, unsigned *zero) {
+                                    int64_t *seg_base, int32_t *seg_cl, unsigned *zero,
+                                    unsigned *done = nullptr) {
     if (zero && threadIdx.x == 0) *zero = 0u;
+    if (done)
+        for (int64_t c = threadIdx.x; c < k; c += blockDim.x) done[c] = 0u;
     block_exclusive_scan([&](int64_t i) { return counts[i]; }, k, offsets);
     if (!seg_base) return;
     block_exclusive_scan([&](int64_t i) { return (counts[i] + SEG_MEMBERS - 1) / SEG_MEMBERS; }, k,
@@ -653,10 +656,33 @@ __device__ __forceinline__ void fvec_load(const float *p, float (&v)[V]) {
     }
 }
 
-template <bool DMR, int V>
+// The certificate of one (cluster, feature) chain from its segment summaries
+// (seg_fold_kernel and the fused fold below): values multiples of 2^q and
+// sum |v| < 2^(53+q); the bound's own rounding stays far below the margin.
+__device__ __forceinline__ bool chain_exact(double bnd, int q) {
+    return q == INT_MAX || (q > -1000 && bnd * (1.0 + 0x1p-20) < ldexp(1.0, 53 + q));
+}
+
+// FOLD: the block that completes a cluster's last segment (per-cluster
+// arrival counter) folds that cluster's chains -- the separate fold pass and
+// its launch disappear.  Threads split into nsub = 256/d sub-lanes per feature
+// (adjacent lanes, combined by shuffles); any association is exact when the
+// certificate holds, failing chains are queued for seg_replay_kernel.
+// Surplus blocks (the grid is sized for the largest segment count) write the
+// zero sums of empty clusters.
+template <bool DMR>
+struct SegFold {
+    double *sums_a, *sums_b;
+    int64_t *fail_list;
+    unsigned *fail_count;
+    unsigned *done;  // per-cluster arrivals, zeroed by offsets_segs_kernel
+};
+
+template <bool DMR, int V, bool FOLD = false>
 __global__ void __launch_bounds__(256) seg_partials_kernel(
     const float *x, int64_t d, const int32_t *perm, const int64_t *offsets, const int64_t *seg_base,
-    const int32_t *seg_cl, int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q) {
+    const int32_t *seg_cl, int64_t k, double *ps_a, double *ps_b, double *ps_abs, int32_t *ps_q,
+    SegFold<DMR> fo = SegFold<DMR>{}) {
     // The segment partial is only used when the whole chain is certified
     // exact (then any association gives the reference's bits), so the
     // members of a segment are split across `nph` thread phases and the
@@ -665,7 +691,18 @@ __global__ void __launch_bounds__(256) seg_partials_kernel(
     __shared__ double red_a[256 * V], red_b[DMR ? 256 * V : 1];
     __shared__ uint32_t red_mx[256 * V], red_mn[256 * V];
     const int64_t s = blockIdx.x;
-    if (s >= seg_base[k]) return;  // launched for the largest possible segment count
+    if (s >= seg_base[k]) {  // launched for the largest possible segment count
+        if (FOLD) {
+            const int64_t extra = int64_t(gridDim.x) - seg_base[k];
+            for (int64_t c = s - seg_base[k]; c < k; c += extra)
+                if (offsets[c + 1] == offsets[c])
+                    for (int64_t f = threadIdx.x; f < d; f += blockDim.x) {
+                        fo.sums_a[c * d + f] = 0.0;
+                        if (DMR) fo.sums_b[c * d + f] = 0.0;
+                    }
+        }
+        return;
+    }
     const int64_t c = seg_cl[s];
     const int64_t beg = offsets[c] + (s - seg_base[c]) * SEG;
     const int64_t end = offsets[c + 1];
@@ -753,6 +790,51 @@ __global__ void __launch_bounds__(256) seg_partials_kernel(
             ps_q[s * d + ff] = q;
         }
     }
+    if (!FOLD) return;
+    __shared__ int is_last;
+    __threadfence();  // this block's partials are visible before its arrival
+    __syncthreads();
+    if (threadIdx.x == 0)
+        is_last = atomicAdd(fo.done + c, 1u) == unsigned(seg_base[c + 1] - seg_base[c] - 1);
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    const int64_t s0 = seg_base[c], s1 = seg_base[c + 1];
+    int nsub = 1;
+    while (nsub < 32 && int64_t(nsub) * 2 * d <= int64_t(blockDim.x)) nsub *= 2;
+    const int sub = int(threadIdx.x) & (nsub - 1);
+    const int64_t fstride = int64_t(blockDim.x) / nsub;
+    // whole warps iterate together (the shuffles): the trip count follows the
+    // warp's first feature
+    const int64_t fw = int64_t(threadIdx.x & ~31u) / nsub;
+    for (int64_t r = 0; fw + r * fstride < d; ++r) {
+        const int64_t f0 = int64_t(threadIdx.x) / nsub + r * fstride;
+        const bool live = f0 < d;
+        const int64_t f = live ? f0 : 0;
+        double a = 0.0, b = 0.0, bnd = 0.0;
+        int q = INT_MAX;
+        if (live)
+            for (int64_t t = s0 + sub; t < s1; t += nsub) {
+                a = __dadd_rn(a, __ldcg(ps_a + t * d + f));
+                if (DMR) b = __dadd_rn(b, __ldcg(ps_b + t * d + f));
+                bnd = __dadd_rn(bnd, __ldcg(ps_abs + t * d + f));
+                q = min(q, __ldcg(ps_q + t * d + f));
+            }
+        for (int off = nsub / 2; off; off >>= 1) {
+            a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, off, nsub));
+            if (DMR) b = __dadd_rn(b, __shfl_xor_sync(0xffffffffu, b, off, nsub));
+            bnd = __dadd_rn(bnd, __shfl_xor_sync(0xffffffffu, bnd, off, nsub));
+            q = min(q, __shfl_xor_sync(0xffffffffu, q, off, nsub));
+        }
+        if (!live || sub != 0) continue;
+        const int64_t e = c * d + f;
+        if (chain_exact(bnd, q)) {
+            fo.sums_a[e] = a;
+            if (DMR) fo.sums_b[e] = b;
+        } else {
+            fo.fail_list[atomicAdd(fo.fail_count, 1u)] = e;
+        }
+    }
 }
 
 // Fold one (cluster, feature) chain.  If every value of the chain is a
@@ -795,8 +877,7 @@ __global__ void seg_fold_kernel(const int64_t *seg_base, int64_t k, int64_t d,
             q = min(q, __shfl_xor_sync(0xffffffffu, q, off, lanes));
         }
         if (!live || sub != 0) continue;
-        const bool exact = q == INT_MAX || (q > -1000 && bnd * (1.0 + 0x1p-20) < ldexp(1.0, 53 + q));
-        if (exact) {
+        if (chain_exact(bnd, q)) {
             sums_a[e] = a;
             if (DMR) sums_b[e] = b;
         } else {
@@ -817,27 +898,38 @@ __device__ __forceinline__ int lowbit_exp(double s) {
 
 // One block per failing chain.  The leading segments whose partial sums
 // provably join the running sum exactly (per-segment certificate against the
-// running sum's lowest set bit) are folded directly; from the first segment
-// that fails on, the block stages member values in shared memory and one
-// thread runs the reference's sequential float64 chain.
+// running sum's lowest set bit) are folded directly.  At the first segment
+// that fails, the block gathers a WINDOW of up to RW segments' member values
+// into shared memory in one parallel pass (one gather latency instead of one
+// per segment) and summarises them in 32-member sub-segments; one thread then
+// walks the window: a segment that certifies against the running sum is
+// added whole, else each of its sub-segments that certifies, else its members
+// one by one -- the reference's sequential float64 chain wherever a partial
+// sum can round.
+constexpr int RW = 8;  // segments per staged window (8 KB of member values)
+
+__device__ __forceinline__ bool joins_exactly(double a, double part_abs, int qpart) {
+    const int qa = lowbit_exp(a);
+    const int q = qa < qpart ? qa : qpart;
+    return q > -1000 && fabs(a) + part_abs * (1.0 + 0x1p-20) < ldexp(1.0, 53 + q);
+}
+
 template <bool DMR>
 __global__ void __launch_bounds__(256) seg_replay_kernel(
     const float *x, int64_t d, const int32_t *perm, const int64_t *offsets,
     const int64_t *seg_base, const double *ps_a, const double *ps_b, const double *ps_abs,
     const int32_t *ps_q, const int64_t *fail_list, const unsigned *fail_count, double *sums_a,
     double *sums_b) {
-    // One thread walks the chain's segment summaries (staged 256 at a time):
-    // a segment whose partial provably joins the running sum exactly
-    // (certificate against the running sum's lowest set bit) is added whole;
-    // at a segment that fails, the block gathers that segment's member values
-    // and the thread sums them one by one, the reference's sequential float64
-    // chain.  Only failing segments touch X.
     constexpr int SB = 256;  // summaries staged per round (== blockDim.x)
-    __shared__ __align__(16) float vals[SEG];
+    constexpr int NSUB = RW * SEG / 32;
+    __shared__ __align__(16) float vals[RW * SEG];
+    __shared__ double sub_a[NSUB], sub_abs[NSUB];
+    __shared__ int sub_q[NSUB];
     __shared__ double sp_a[SB], sp_b[DMR ? SB : 1], sp_abs[SB];
     __shared__ int32_t sp_q[SB];
     __shared__ double run[2];
     __shared__ int next;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const unsigned nfail = *fail_count;
     for (unsigned w = blockIdx.x; w < nfail; w += gridDim.x) {
         const int64_t e = fail_list[w];
@@ -861,12 +953,8 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
                 if (threadIdx.x == 0) {
                     double a = run[0], b = run[1];
                     for (; j < cnt; ++j) {
-                        const int qseg = sp_q[j];
-                        if (qseg == INT_MAX) continue;  // all-zero segment
-                        const int qa = lowbit_exp(a);
-                        const int q = qa < qseg ? qa : qseg;
-                        const double bound = fabs(a) + sp_abs[j] * (1.0 + 0x1p-20);
-                        if (!(q > -1000 && bound < ldexp(1.0, 53 + q)) || (DMR && a != b)) break;
+                        if (sp_q[j] == INT_MAX) continue;  // all-zero segment
+                        if (!joins_exactly(a, sp_abs[j], sp_q[j]) || (DMR && a != b)) break;
                         a = __dadd_rn(a, sp_a[j]);
                         if (DMR) b = __dadd_rn(b, sp_b[j]);
                     }
@@ -877,33 +965,85 @@ __global__ void __launch_bounds__(256) seg_replay_kernel(
                 __syncthreads();
                 j = next;
                 if (j >= cnt) break;
-                // gather the failing segment's members (one per thread)
+                // stage the window's member values (segments j .. j+nw-1)
+                const int nw = cnt - j < RW ? cnt - j : RW;
                 const int64_t t0 = m0 + (sb + j - s0) * SEG;
-                const int n = int(m1 - t0 < SEG ? m1 - t0 : SEG);
-                if (int(threadIdx.x) < n) vals[threadIdx.x] = x[int64_t(perm[t0 + threadIdx.x]) * d + f];
+                const int64_t tend = m1 - t0 < int64_t(nw) * SEG ? m1 : t0 + int64_t(nw) * SEG;
+                const int n = int(tend - t0);
+#pragma unroll 4
+                for (int t = threadIdx.x; t < n; t += 256) vals[t] = x[int64_t(perm[t0 + t]) * d + f];
+                __syncthreads();
+                // 32-member sub-segment summaries (warp w: sub-segments w, w+8, ...)
+                for (int sj = wid; sj * 32 < n; sj += 8) {
+                    const float v = sj * 32 + lane < n ? vals[sj * 32 + lane] : 0.0f;
+                    double ps = double(v);
+                    uint32_t mx = __float_as_uint(v) & 0x7FFFFFFFu, mn = mx - 1u;
+                    for (int off = 16; off; off >>= 1) {
+                        ps = __dadd_rn(ps, __shfl_xor_sync(0xffffffffu, ps, off));
+                        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+                        mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, off));
+                    }
+                    if (lane == 0) {
+                        sub_a[sj] = ps;
+                        sub_abs[sj] = 32.0 * double(__uint_as_float(mx));
+                        int q = INT_MAX;
+                        if (mn != 0xFFFFFFFFu) {
+                            const int ex = int((mn + 1u) >> 23);
+                            q = (ex == 0 ? 1 : ex) - 150;
+                        }
+                        sub_q[sj] = q;
+                    }
+                }
                 __syncthreads();
                 if (threadIdx.x == 0) {
                     double a = run[0], b = run[1];
-                    const float4 *v4 = reinterpret_cast<const float4 *>(vals);
-                    int t = 0;
-                    for (; t + 8 <= n; t += 8) {
-                        const float4 p = v4[t / 4], r = v4[t / 4 + 1];
-                        const float vv[8] = {p.x, p.y, p.z, p.w, r.x, r.y, r.z, r.w};
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            a = __dadd_rn(a, double(vv[u]));
-                            if (DMR) b = __dadd_rn(b, double(vv[u]));
+                    for (int g = 0; g < nw; ++g) {
+                        const int jj = j + g;
+                        if (sp_q[jj] == INT_MAX) continue;
+                        if (joins_exactly(a, sp_abs[jj], sp_q[jj]) && (!DMR || a == b)) {
+                            a = __dadd_rn(a, sp_a[jj]);
+                            if (DMR) b = __dadd_rn(b, sp_b[jj]);
+                            continue;
                         }
-                    }
-                    for (; t < n; ++t) {
-                        a = __dadd_rn(a, double(vals[t]));
-                        if (DMR) b = __dadd_rn(b, double(vals[t]));
+                        const int te = min(n, (g + 1) * SEG);
+                        for (int sj = g * (SEG / 32); sj * 32 < te; ++sj) {
+                            if (sub_q[sj] == INT_MAX) continue;  // all-zero sub-segment
+                            if (joins_exactly(a, sub_abs[sj], sub_q[sj]) && (!DMR || a == b)) {
+                                a = __dadd_rn(a, sub_a[sj]);
+                                if (DMR) b = __dadd_rn(b, sub_a[sj]);
+                                continue;
+                            }
+                            const int ue = min(te, sj * 32 + 32);
+                            if (ue == sj * 32 + 32) {
+                                // a whole sub-segment: its 32 values loaded up
+                                // front (8 x LDS.128), then the dependent chain
+                                const float4 *v4 = reinterpret_cast<const float4 *>(vals + sj * 32);
+                                float4 r[8];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) r[u] = v4[u];
+#pragma unroll
+                                for (int u = 0; u < 8; ++u) {
+                                    const float vv[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                                    for (int h = 0; h < 4; ++h) {
+                                        a = __dadd_rn(a, double(vv[h]));
+                                        if (DMR) b = __dadd_rn(b, double(vv[h]));
+                                    }
+                                }
+                                continue;
+                            }
+                            for (int t = sj * 32; t < ue; ++t) {
+                                a = __dadd_rn(a, double(vals[t]));
+                                if (DMR) b = __dadd_rn(b, double(vals[t]));
+                            }
+                        }
                     }
                     run[0] = a;
                     run[1] = b;
+                    next = j + nw;
                 }
-                ++j;
                 __syncthreads();
+                j = next;
             }
         }
         if (threadIdx.x == 0) {
@@ -1281,11 +1421,18 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
     if (use_seg) {
         seg_base = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_BASE, sizeof(int64_t) * (k + 2) +
                                                                           sizeof(int32_t) * max_seg, st));
-        fail_list = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_FB, sizeof(int64_t) * (k * d + 2), st));
+        fail_list = static_cast<int64_t *>(scratch(ctx, SLOT_SEG_FB, sizeof(int64_t) * (k * d + 2) +
+                                                                        sizeof(unsigned) * (k + 2), st));
         if (!seg_base || !fail_list) return FTK_ERR_CUDA;
         seg_cl = reinterpret_cast<int32_t *>(seg_base + (k + 2));
         fail_count = reinterpret_cast<unsigned *>(fail_list + k * d);
     }
+    // fused fold (seg_partials_kernel<FOLD>: the last segment block of a
+    // cluster folds its chains, no separate fold pass) -- an A/B knob, off by default: measured slower at c2 (partials 93 -> 124 us
+    // against the 15 us fold pass it removes, profiles/r6_ab_experiments.txt)
+    bool fused_fold = false;
+    if (const char *e = getenv("FTK_UPD_FUSED_FOLD")) fused_fold = use_seg && atoi(e) != 0;
+    unsigned *done = fused_fold ? reinterpret_cast<unsigned *>(fail_list + k * d + 2) : nullptr;
     // stable sort of (label, index) -> member lists in ascending sample order
     int bits = 1;
     while ((int64_t(1) << bits) < k) ++bits;
@@ -1307,7 +1454,7 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         FTK_LAUNCHED("cs_hist_kernel");
         cs_binscan_kernel<<<unsigned((k * 32 + 255) / 256), 256, 0, st>>>(hist, nb, k, counts_a);
         FTK_LAUNCHED("cs_binscan_kernel");
-        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count, done);
         FTK_LAUNCHED("offsets_segs_kernel");
         const size_t smw = sizeof(int32_t) * size_t(nw) * k;
         if (smw > 48 * 1024)
@@ -1330,10 +1477,10 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         boundary_count_kernel<<<grid_for(m, 256), 256, 0, st>>>(
             keys_out, m, k, reinterpret_cast<unsigned long long *>(counts_a));
         FTK_LAUNCHED("boundary_count_kernel");
-        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count, done);
         FTK_LAUNCHED("offsets_segs_kernel");
     } else {
-        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count);
+        offsets_segs_kernel<<<1, 1024, 0, st>>>(counts_a, k, offsets, seg_base, seg_cl, fail_count, done);
         FTK_LAUNCHED("offsets_segs_kernel");
     }
     const int64_t warps = k * ((d + 31) / 32);
@@ -1390,26 +1537,44 @@ int update_sums_run(ftk_ctx *ctx, int dtype, const void *x, const int32_t *label
         while (lanes < 32 && int64_t(lanes) * k < max_seg) lanes *= 2;
         const unsigned fgrid = grid_for(k * d * lanes, 128);
         if (dmr) {
-            auto kp = d % 4 == 0 ? seg_partials_kernel<true, 4>
-                      : (d % 2 == 0 ? seg_partials_kernel<true, 2> : seg_partials_kernel<true, 1>);
-            kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
-                                                  ps_b, ps_abs, ps_q);
-            FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<true><<<fgrid, 128, 0, st>>>(
-                seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count, lanes);
-            FTK_LAUNCHED("seg_fold_kernel");
+            const SegFold<true> fo{sums_a, sums_b, fail_list, fail_count, done};
+            if (fused_fold) {
+                auto kp = d % 4 == 0 ? seg_partials_kernel<true, 4, true>
+                          : (d % 2 == 0 ? seg_partials_kernel<true, 2, true> : seg_partials_kernel<true, 1, true>);
+                kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                      ps_b, ps_abs, ps_q, fo);
+                FTK_LAUNCHED("seg_partials_kernel");
+            } else {
+                auto kp = d % 4 == 0 ? seg_partials_kernel<true, 4>
+                          : (d % 2 == 0 ? seg_partials_kernel<true, 2> : seg_partials_kernel<true, 1>);
+                kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                      ps_b, ps_abs, ps_q, fo);
+                FTK_LAUNCHED("seg_partials_kernel");
+                seg_fold_kernel<true><<<fgrid, 128, 0, st>>>(
+                    seg_base, k, d, ps_a, ps_b, ps_abs, ps_q, sums_a, sums_b, fail_list, fail_count, lanes);
+                FTK_LAUNCHED("seg_fold_kernel");
+            }
             seg_replay_kernel<true><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
                                                           ps_b, ps_abs, ps_q, fail_list, fail_count,
                                                           sums_a, sums_b);
         } else {
-            auto kp = d % 4 == 0 ? seg_partials_kernel<false, 4>
-                      : (d % 2 == 0 ? seg_partials_kernel<false, 2> : seg_partials_kernel<false, 1>);
-            kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
-                                                  nullptr, ps_abs, ps_q);
-            FTK_LAUNCHED("seg_partials_kernel");
-            seg_fold_kernel<false><<<fgrid, 128, 0, st>>>(
-                seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count, lanes);
-            FTK_LAUNCHED("seg_fold_kernel");
+            const SegFold<false> fo{sums_a, nullptr, fail_list, fail_count, done};
+            if (fused_fold) {
+                auto kp = d % 4 == 0 ? seg_partials_kernel<false, 4, true>
+                          : (d % 2 == 0 ? seg_partials_kernel<false, 2, true> : seg_partials_kernel<false, 1, true>);
+                kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                      nullptr, ps_abs, ps_q, fo);
+                FTK_LAUNCHED("seg_partials_kernel");
+            } else {
+                auto kp = d % 4 == 0 ? seg_partials_kernel<false, 4>
+                          : (d % 2 == 0 ? seg_partials_kernel<false, 2> : seg_partials_kernel<false, 1>);
+                kp<<<unsigned(max_seg), 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, seg_cl, k, ps_a,
+                                                      nullptr, ps_abs, ps_q, fo);
+                FTK_LAUNCHED("seg_partials_kernel");
+                seg_fold_kernel<false><<<fgrid, 128, 0, st>>>(
+                    seg_base, k, d, ps_a, nullptr, ps_abs, ps_q, sums_a, nullptr, fail_list, fail_count, lanes);
+                FTK_LAUNCHED("seg_fold_kernel");
+            }
             seg_replay_kernel<false><<<rgrid, 256, 0, st>>>(xx, d, vals_out, offsets, seg_base, ps_a,
                                                            nullptr, ps_abs, ps_q, fail_list,
                                                            fail_count, sums_a, nullptr);

@@ -423,6 +423,29 @@ def test_ordered_chain_kernels_bit_exact(m, d, k, dt, env, dmr, monkeypatch):
     assert ev == []
 
 
+@pytest.mark.parametrize("fused", ["0", "1"])
+@pytest.mark.parametrize("dmr", [False, True])
+def test_update_fused_fold_bit_exact(fused, dmr, monkeypatch):
+    """The segment fold fused into the partials kernel (the last segment block
+    of a cluster folds its chains) and the separate fold pass give
+    numpy.bincount's bits, with empty clusters (zero sums written by the
+    surplus blocks), one long chain, and tiny values whose chains the replay
+    walks in 32-member sub-segments."""
+    monkeypatch.setenv("FTK_UPD_FUSED_FOLD", fused)
+    rng = np.random.default_rng(77)
+    m, d, k = 50000, 128, 1024
+    x = rng.standard_normal((m, d)) * 3.0 + 20.0
+    x[rng.integers(0, m, 300), rng.integers(0, d, 300)] = 1e-9
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    lab = 2 * rng.integers(0, k // 2, m).astype(np.int64)  # odd clusters empty
+    lab[: m // 4] = 6  # one long chain (49 segments)
+    c, counts, ev = P.update_step(x, lab, k, ft_mode="abft+dmr" if dmr else "off")
+    ref, ref_counts = O.update_step(x, lab, k)
+    assert counts.tolist() == ref_counts.tolist()
+    assert c.tobytes() == ref.tobytes()
+    assert ev == []
+
+
 def test_candidate_overflow_rows_go_exact():
     """Rows whose pass-2 candidate set exceeds its cap (300 identical
     centroids tie for every row) are resolved by the exact row kernel."""
