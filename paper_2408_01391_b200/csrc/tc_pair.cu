@@ -340,6 +340,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 const float *ynt = ywarp + ybuf * PR_BN;
                 const bool inj_here = INJ && inj_c >= int(c0) && inj_c < int(c0) + ncol;
                 float gA = 0.0f;  // checksum partial before the group split
+                bool early_rel = false;  // FTK_PAIR_X2R: buffer released inside the drain
                 if (P.dbg & 4) {
                     // timing probe: TMEM drain only (values folded with one XOR per column)
                     uint32_t va[32], acc = 0;
@@ -415,6 +416,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     // skipped (a plain loop: the full-tile loop stays as is)
                     const int live = int(P.k - c0);
                     uint32_t va[32], vb[32];
+#ifndef FTK_PAIR_NOX2
+                    // both chunks of a pair loaded, ONE wait, then the two
+                    // tournaments in one basic block: twice the independent
+                    // work per warp, no load in flight during the math
+                    // (measured faster than keeping the next chunk's load in
+                    // flight: c2 kernel 0.531 -> 0.519 ms, FT-off 0.498 ->
+                    // 0.482, profiles/r6_ab_experiments.txt; FTK_PAIR_NOX2
+                    // builds the software-pipelined drain)
+                    if (live >= ncol && (nch & 1) == 0) {
+#pragma unroll 1
+                        for (int ch = 0; ch < nch; ch += 2) {
+#ifdef FTK_PAIR_X64
+                            tmem_ld64_issue(tbase + uint32_t(ch * 32), va, vb);
+#else
+                            tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
+                            tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
+#endif
+                            tmem_ld_wait(va);
+                            tmem_pin(vb);
+#ifdef FTK_PAIR_X2R
+                            if (ch + 2 >= nch) {  // the tile's last values are in registers: release the buffer
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_remote(t_empty_lead0 + uint32_t(buf) * 8u);
+                                early_rel = true;
+                            }
+#endif
+                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch)
+                                inject_into(va, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                            if (INJ && inj_here && (inj_c - int(c0)) >> 5 == ch + 1)
+                                inject_into(vb, (inj_c - int(c0)) & 31, inj_b, inj_a);
+                            if (CHK && ch == split) { gA = s0 + s1; s0 = s1 = 0.0f; }
+                            float t0s = 0.0f, t1s = 0.0f, bL = INFINITY, bM = INFINITY;
+                            screen32t<CHK>(va, ynt + ch * 32, uint32_t(cbeg + ch * 32), a1, a2, s0, s1);
+                            screen32t<CHK>(vb, ynt + (ch + 1) * 32, uint32_t(cbeg + (ch + 1) * 32), bL, bM,
+                                           t0s, t1s);
+                            if (CHK && ch + 1 == split) { gA = s0 + s1; s0 = t0s; s1 = t1s; }
+                            else if (CHK) { s0 += t0s; s1 += t1s; }
+                            a2 = fminf(fminf(a2, bM), bL == bL ? fmaxf(a1, bL) : INFINITY);
+                            a1 = fminf(a1, bL);
+                        }
+                    } else
+#endif
                     if (live >= ncol) {
                         tmem_ld32_issue(tbase, va);
                         tmem_ld_wait(va);
@@ -449,9 +493,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         }
                     }
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(t_empty_lead0 + uint32_t(buf) * 8u); PROBE_ADD(0, clock64() - cb_); PROBE_ADD(5, 1);
+                if (!early_rel) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(t_empty_lead0 + uint32_t(buf) * 8u);
+                }
+                PROBE_ADD(0, clock64() - cb_); PROBE_ADD(5, 1);
                 // merge the two chains into the tile's top-2, then the running top-2
                 const float t1 = fminf(a1, b1);  // b1 = b2 = inf: single chain
                 const float t2 = fminf(fminf(a2, b2), fmaxf(a1, b1));
