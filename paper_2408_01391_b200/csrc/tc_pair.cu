@@ -355,17 +355,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 } else if (COLLECT) {
                     // pass 2: every column whose screened value can still beat
                     // the row's threshold becomes an exact-evaluation candidate
-                    uint32_t va[32], vb[32];
+                    uint32_t va[32];
                     int nloc = 0, lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0;
-                    auto collect32 = [&](const uint32_t (&vv)[32], int ch) {
+#pragma unroll 1
+                    for (int ch = 0; ch < nch; ++ch) {
+                        tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
+                        tmem_ld_wait(va);
                         const float4 *yn4 = reinterpret_cast<const float4 *>(ynt + ch * 32);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const float4 yv = yn4[q];
                             float d[4];
-                            ffma2_m2(__uint_as_float(vv[4 * q]), __uint_as_float(vv[4 * q + 1]), yv.x,
+                            ffma2_m2(__uint_as_float(va[4 * q]), __uint_as_float(va[4 * q + 1]), yv.x,
                                      yv.y, d[0], d[1]);
-                            ffma2_m2(__uint_as_float(vv[4 * q + 2]), __uint_as_float(vv[4 * q + 3]),
+                            ffma2_m2(__uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]),
                                      yv.z, yv.w, d[2], d[3]);
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
@@ -387,16 +390,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                     }
                                 }
                         }
-                    };
-                    // chunks in pairs: one wait per pair, as in the pass-1 drain
-#pragma unroll 1
-                    for (int ch = 0; ch < nch; ch += 2) {
-                        tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
-                        if (ch + 1 < nch) tmem_ld32_issue(tbase + uint32_t((ch + 1) * 32), vb);
-                        tmem_ld_wait(va);
-                        tmem_pin(vb);
-                        collect32(va, ch);
-                        if (ch + 1 < nch) collect32(vb, ch + 1);
                     }
                     // one append per warp for the tile's register-held candidates
                     int incl = nloc;
