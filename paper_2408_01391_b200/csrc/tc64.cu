@@ -222,16 +222,27 @@ struct RtGeom {
     int stages;     // ring depth
     size_t stage;   // bytes per stage (nbox * 4 KB)
 };
-__global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
+// CT: the centroids live in shared memory for the whole kernel (K*D*8 <= 128
+// KB, d % 16 == 0), 16-byte chunks XOR-swizzled by (row & 7) within each
+// 128-byte group: the per-lane centroid reads (32 different rows per warp)
+// cost a few shared-memory wavefronts instead of 32 L1 wavefronts each -- the
+// gathers from L2 saturated the L1 (ncu: L1/TEX 97 %, DRAM 49 %).  One CTA
+// per SM then, with NC = 6 consumer slots beside the table.
+constexpr int RT_CONS_CT = 6;
+constexpr int64_t RT_CT_MAX_BYTES = 128 * 1024;
+
+template <int NC, bool CT>
+__global__ void __launch_bounds__(32 * (NC + 1)) tc64_refine_tma_kernel(
     const __grid_constant__ CUtensorMap tmx, const double *y, const double *yn, int64_t m, int64_t d,
     int nbox, const int2 *rec, const float *a64, int32_t *out_idx, double *out_val, int32_t *fb,
-    unsigned *fb_count, float *fb_thr) {
+    unsigned *fb_count, float *fb_thr, int64_t k) {
     extern __shared__ __align__(1024) unsigned char rt_raw[];
     unsigned char *smem = rt_raw + ((1024u - (smem_u32(rt_raw) & 1023u)) & 1023u);
-    constexpr int stages = RT_CONS;  // slot w belongs to consumer w
+    constexpr int stages = NC;  // slot w belongs to consumer w
     const size_t stage_bytes = size_t(nbox) * 4096;
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + size_t(stages) * stage_bytes);
     uint64_t *empty = full + stages;
+    unsigned char *ctab = smem + size_t(stages) * stage_bytes + 128;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntile = (m + 31) / 32;
     if (threadIdx.x == 0) {
@@ -241,8 +252,17 @@ __global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
         }
         fence_barrier_init();
     }
+    if (CT) {
+        const int64_t cpr = d / 2;  // 16-byte chunks per centroid row
+        const double2 *y2 = reinterpret_cast<const double2 *>(y);
+        for (int64_t e = threadIdx.x; e < k * cpr; e += blockDim.x) {
+            const int64_t j = e / cpr, c = e % cpr;
+            const int64_t cs = (c & ~int64_t(7)) | ((c ^ j) & 7);
+            *reinterpret_cast<double2 *>(ctab + (j * cpr + cs) * 16) = __ldg(y2 + e);
+        }
+    }
     __syncthreads();
-    if (warp == RT_CONS) {
+    if (warp == NC) {
         // ----------------------------------------------------- producer --
         if (lane == 0) {
             prefetch_tmap(&tmx);
@@ -261,18 +281,24 @@ __global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
     // ------------------------------------------------------- consumers --
     int q = warp;
     for (int64_t tile = int64_t(blockIdx.x) + int64_t(warp) * gridDim.x; tile < ntile;
-         tile += int64_t(gridDim.x) * RT_CONS, q += RT_CONS) {
+         tile += int64_t(gridDim.x) * NC, q += NC) {
         const int s = q % stages;
         const int64_t row = tile * 32 + lane;
         const int2 r = row < m ? rec[row] : make_int2(-1, 0);
         const int j = r.x;
         const double *cr = y + int64_t(j < 0 ? 0 : j) * d;
+        const unsigned char *crs = ctab + size_t(j < 0 ? 0 : j) * size_t(d) * 8;
+        const int jsw = (j < 0 ? 0 : j) & 7;
         double cv[16];
+        auto c_chunk = [&](int f0, int u) -> double2 {  // features f0 + 2u, f0 + 2u + 1 (f0 % 16 == 0)
+            if (CT) return *reinterpret_cast<const double2 *>(crs + size_t(f0) * 8 + ((u ^ jsw) << 4));
+            return __ldg(reinterpret_cast<const double2 *>(cr + f0) + u);
+        };
         auto load_c = [&](int f0) {
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const bool ok = j >= 0 && f0 + 2 * u + 1 < d;
-                const double2 c2 = ok ? __ldg(reinterpret_cast<const double2 *>(cr + f0) + u) : make_double2(0.0, 0.0);
+                const double2 c2 = ok ? c_chunk(f0, u) : make_double2(0.0, 0.0);
                 cv[2 * u] = c2.x;
                 cv[2 * u + 1] = c2.y;
             }
@@ -290,8 +316,7 @@ __global__ void __launch_bounds__(32 * (RT_CONS + 1)) tc64_refine_tma_kernel(
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
                     const bool ok = j >= 0 && f0 + 16 + 2 * u + 1 < d;
-                    const double2 c2 = ok ? __ldg(reinterpret_cast<const double2 *>(cr + f0 + 16) + u)
-                                          : make_double2(0.0, 0.0);
+                    const double2 c2 = ok ? c_chunk(f0 + 16, u) : make_double2(0.0, 0.0);
                     cn[2 * u] = c2.x;
                     cn[2 * u + 1] = c2.y;
                 }
@@ -536,16 +561,27 @@ int tc64_assign_run(ftk_ctx *ctx, const double *x, const double *y, const double
         const size_t ring = size_t(RT_CONS) * stage;  // one slot per consumer warp
         CUtensorMap tx;
         const bool tma = ring <= 200 * 1024 && !getenv("FTK_T64_REFINE_LDG") && !make_f64_map(&tx, x, m, d, 32);
-        if (tma) {
+        const int64_t ct_bytes = k * d * 8;
+        const char *cte = getenv("FTK_T64_CTAB");  // A/B knob: 0 = centroids gathered from L2
+        const size_t ct_smem = size_t(RT_CONS_CT) * stage + 128 + size_t(ct_bytes) + 1024;
+        const bool ctab = tma && d % 16 == 0 && ct_bytes <= RT_CT_MAX_BYTES && ct_smem <= 227 * 1024 &&
+                          !(cte && atoi(cte) == 0) && (reinterpret_cast<uintptr_t>(y) & 15) == 0;
+        const int64_t ntile = (m + 31) / 32;
+        if (ctab) {
+            const size_t smem = ct_smem;
+            auto kern = tc64_refine_tma_kernel<RT_CONS_CT, true>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            kern<<<unsigned(std::min<int64_t>(ntile, int64_t(current_sm_count()))), 32 * (RT_CONS_CT + 1), smem, st>>>(
+                tx, y, yn, m, d, nbox, rec, p2 ? a64 : nullptr, out_idx, out_val, fb, cnt, p2 ? fb_thr : nullptr, k);
+            FTK_LAUNCHED("tc64_refine_tma_kernel");
+        } else if (tma) {
             const int per_sm = int(std::min<size_t>(3, (200 * 1024) / ring));  // CTAs per SM
-            const size_t smem = ring + 16 * RT_CONS + 1024;
-            FTK_CUDA(cudaFuncSetAttribute(tc64_refine_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          int(smem)));
-            const int64_t ntile = (m + 31) / 32;
-            tc64_refine_tma_kernel<<<unsigned(std::min<int64_t>(ntile, int64_t(148) * per_sm)),
-                                     32 * (RT_CONS + 1), smem, st>>>(tx, y, yn, m, d, nbox, rec,
-                                                                     p2 ? a64 : nullptr, out_idx, out_val,
-                                                                     fb, cnt, p2 ? fb_thr : nullptr);
+            const size_t smem = ring + 128 + 1024;
+            auto kern = tc64_refine_tma_kernel<RT_CONS, false>;
+            FTK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            kern<<<unsigned(std::min<int64_t>(ntile, int64_t(current_sm_count()) * per_sm)), 32 * (RT_CONS + 1), smem,
+                   st>>>(tx, y, yn, m, d, nbox, rec, p2 ? a64 : nullptr, out_idx, out_val, fb, cnt,
+                         p2 ? fb_thr : nullptr, k);
             FTK_LAUNCHED("tc64_refine_tma_kernel");
         } else {
             tc64_refine_kernel<<<unsigned(std::min<int64_t>((m + 32 * R64_WARPS - 1) / (32 * R64_WARPS), 148 * 6)),

@@ -51,6 +51,20 @@ def test_tc64_random_bit_exact(m, d, k, pair64):
     assert r.min_dists.tobytes() == val.tobytes()
 
 
+@pytest.mark.parametrize("ctab", ["0", "1"])
+@pytest.mark.parametrize("m,d,k", [(70000, 64, 256), (40000, 32, 500), (30000, 48, 7)])
+def test_tc64_refine_centroid_table_both_ways(m, d, k, ctab, pair64, monkeypatch):
+    """The float64 refine with the centroids in shared memory (K*D*8 <= 128 KB,
+    d % 16 == 0; swizzled 16-byte chunks) and gathered from L2 (FTK_T64_CTAB=0)
+    give the oracle's labels and distances bit for bit."""
+    monkeypatch.setenv("FTK_T64_CTAB", ctab)
+    x, y = _blobs(m, d, k, 5)
+    r = P.fused_assign(x, y)
+    lab, val = O.assign(x, y)
+    assert np.array_equal(r.assignments, lab)
+    assert r.min_dists.tobytes() == val.tobytes()
+
+
 @pytest.mark.parametrize("m,d,k", [(100000, 64, 256), (70000, 128, 64)])
 def test_tc64_blobs_certified_and_exact(m, d, k, pair64):
     """Near-converged blobs: almost every row is certified by the screen."""
