@@ -1,0 +1,5 @@
+# r6p: candidate evaluation dealt across blocks first; tests + launch breakdown
+OUT=gpurun_out/r6p; mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_tc.py tests/test_gpu_abft_tc.py tests/test_gpu_parity.py tests/test_gpu_configs.py -q -x > $OUT/pytest.log 2>&1; tail -1 $OUT/pytest.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv python tools/prof_lloyd.py --steps 8 --ft abft > /dev/null 2>&1
+python tools/iter_breakdown.py $OUT/launches.csv 12
