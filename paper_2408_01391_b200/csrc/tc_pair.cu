@@ -142,11 +142,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
     // on the host (pass 2 over the rows pass 1 left uncertified)
     const int64_t M = P.m_dev ? (int64_t(*P.m_dev) < P.m ? int64_t(*P.m_dev) : P.m) : P.m;
     const int64_t npt = (M + 2 * PR_BM - 1) / (2 * PR_BM);  // row pair-tiles
-    // work items: a row pair-tile with all its column tiles, or (COLLECT: the
-    // few rows of pass 2) one column tile, so pass 2 spreads over every SM
+    // work items: a row pair-tile with all its column tiles, or (COLLECT, when
+    // pass 2 has few rows) a group of column tiles, so the few row tiles still
+    // spread over every SM: about two items per cluster.  Many pass-2 rows
+    // (c5: ~3e6) keep whole row tiles -- splitting them re-reads each X tile
+    // once per column group (c5 pass 2: 22 ms with one column tile per item)
     const bool csplit = COLLECT && FTK_PAIR_COLLECT_SPLIT;
-    const int TPS = csplit ? P.ntiles : 1;   // items per row pair-tile
-    const int TPW = csplit ? 1 : P.ntiles;   // column tiles per item
+    int tsplit = 1;
+    if (csplit && npt > 0 && npt < 2 * int64_t(ncluster_x()))
+        tsplit = int(std::min<int64_t>(P.ntiles, (2 * int64_t(ncluster_x()) + npt - 1) / npt));
+    const int TPW = csplit ? (P.ntiles + tsplit - 1) / tsplit : P.ntiles;  // column tiles per item
+    const int TPS = csplit ? (P.ntiles + TPW - 1) / TPW : 1;               // items per row pair-tile
     const int64_t nwi = npt * TPS;
     const int64_t pt0 = cluster_id_x(), pstride = ncluster_x();
 
