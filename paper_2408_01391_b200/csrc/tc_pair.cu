@@ -324,6 +324,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
             float inj_b = 0.0f, inj_a = 0.0f;
             const float thr = (COLLECT && grow < M) ? P.thr[grow] : -INFINITY;
             unsigned ncand = 0;  // COLLECT: this thread's candidates of the row
+            // COLLECT: the first four candidates of the row wait in registers
+            // for one warp-wide append per work item (a same-address atomic per
+            // warp and tile serialised in L2 at c5's ~3e6 pass-2 rows)
+            int nloc = 0, lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0;
             if (INJ && P.inj_col && grow < M) {
                 inj_c = P.inj_col[grow];
                 if (inj_c >= 0) {
@@ -362,7 +366,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                     // pass 2: every column whose screened value can still beat
                     // the row's threshold becomes an exact-evaluation candidate
                     uint32_t va[32];
-                    int nloc = 0, lc0 = 0, lc1 = 0, lc2 = 0, lc3 = 0;
 #pragma unroll 1
                     for (int ch = 0; ch < nch; ++ch) {
                         tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
@@ -396,24 +399,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                                     }
                                 }
                         }
-                    }
-                    // one append per warp for the tile's register-held candidates
-                    int incl = nloc;
-#pragma unroll
-                    for (int off = 1; off < 32; off <<= 1) {
-                        const int o = __shfl_up_sync(0xffffffffu, incl, off);
-                        if (lane >= off) incl += o;
-                    }
-                    const int total = __shfl_sync(0xffffffffu, incl, 31);
-                    if (total) {
-                        unsigned base = 0;
-                        if (lane == 31) base = atomicAdd(P.cand_count, unsigned(total));
-                        base = __shfl_sync(0xffffffffu, base, 31) + unsigned(incl - nloc);
-                        const int cols[4] = {lc0, lc1, lc2, lc3};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            if (i < nloc && base + i < P.cand_cap)
-                                P.cand[base + i] = make_int2(int(grow), cols[i]);
                     }
                 } else if (!(P.dbg & 1)) {
                     // software-pipelined TMEM drain, two 32-column chunks per
@@ -526,6 +511,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                 ybuf ^= 1;
             }
             if (COLLECT && ncand) atomicAdd(P.row_cnt + grow, ncand);
+            if (COLLECT) {
+                int incl = nloc;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int o = __shfl_up_sync(0xffffffffu, incl, off);
+                    if (lane >= off) incl += o;
+                }
+                const int total = __shfl_sync(0xffffffffu, incl, 31);
+                if (total) {
+                    unsigned base = 0;
+                    if (lane == 31) base = atomicAdd(P.cand_count, unsigned(total));
+                    base = __shfl_sync(0xffffffffu, base, 31) + unsigned(incl - nloc);
+                    const int cols[4] = {lc0, lc1, lc2, lc3};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (i < nloc && base + i < P.cand_cap)
+                            P.cand[base + i] = make_int2(int(grow), cols[i]);
+                }
+            }
             // publish this warpgroup's partial for the row tile
             mbar_wait(&p_empty[pb], (uint32_t(it >> 1) & 1) ^ 1);
             PairPart pp;
