@@ -371,6 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                         tmem_ld32_issue(tbase + uint32_t(ch * 32), va);
                         tmem_ld_wait(va);
                         const float4 *yn4 = reinterpret_cast<const float4 *>(ynt + ch * 32);
+                        uint32_t hit = 0;
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
                             const float4 yv = yn4[q];
@@ -380,24 +381,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PR_THREADS, 1)
                             ffma2_m2(__uint_as_float(va[4 * q + 2]), __uint_as_float(va[4 * q + 3]),
                                      yv.z, yv.w, d[2], d[3]);
 #pragma unroll
-                            for (int u = 0; u < 4; ++u)
-                                if (d[u] <= thr && c0 + ch * 32 + 4 * q + u < P.k) {
-                                    const int col = int(c0) + ch * 32 + 4 * q + u;
-                                    ++ncand;  // row count: one atomic per row and warpgroup
-                                    // the first few per thread wait in registers for one
-                                    // warp-wide append per tile (~2 candidates per row at c2:
-                                    // a same-address atomic each would serialise in L2)
-                                    if (nloc < 4) {
-                                        lc0 = nloc == 0 ? col : lc0;
-                                        lc1 = nloc == 1 ? col : lc1;
-                                        lc2 = nloc == 2 ? col : lc2;
-                                        lc3 = nloc == 3 ? col : lc3;
-                                        ++nloc;
-                                    } else {
-                                        const unsigned slot = atomicAdd(P.cand_count, 1u);
-                                        if (slot < P.cand_cap) P.cand[slot] = make_int2(int(grow), col);
-                                    }
-                                }
+                            for (int u = 0; u < 4; ++u) hit |= (d[u] <= thr ? 1u : 0u) << (4 * q + u);
+                        }
+                        // branch-free compare above, then one pass over the set bits
+                        // (a row has ~2 candidates among K columns); columns past the
+                        // last centroid never count
+                        const int64_t cb = c0 + ch * 32;
+                        const int64_t live = P.k - cb;
+                        if (live < 32) hit &= live <= 0 ? 0u : ((1u << live) - 1u);
+                        while (hit) {
+                            const int col = int(cb) + __ffs(hit) - 1;
+                            hit &= hit - 1u;
+                            ++ncand;  // row count: one atomic per row and warpgroup
+                            // the first few per thread wait in registers for one
+                            // warp-wide append per work item
+                            if (nloc < 4) {
+                                lc0 = nloc == 0 ? col : lc0;
+                                lc1 = nloc == 1 ? col : lc1;
+                                lc2 = nloc == 2 ? col : lc2;
+                                lc3 = nloc == 3 ? col : lc3;
+                                ++nloc;
+                            } else {
+                                const unsigned slot = atomicAdd(P.cand_count, 1u);
+                                if (slot < P.cand_cap) P.cand[slot] = make_int2(int(grow), col);
+                            }
                         }
                     }
                 } else if (!(P.dbg & 1)) {
